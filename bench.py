@@ -1,0 +1,414 @@
+"""SSB q1.1-q4.3 on B200: ms/query and scan GB/s vs the HBM roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--sf SF] [--impl ours|reference]
+
+One STEP = the full 13-query Star Schema Benchmark suite (q1.1 ... q4.3), each
+query exactly as the reference's `tq ssb` times it (tools/tq_main.cpp:198-200):
+dimension hash builds + one fused lineorder pass + group compaction + result
+copy to the host.  Workload: SF=20 on one GPU (BASELINE configs[3]); with
+N > 1 GPUs (torchrun, one rank per GPU) SF=100 with lineorder sharded by row
+range and the partial aggregates merged with one NCCL reduce per query
+(configs[4]).  Inputs are synthetic and deterministic (generate_ssb(sf, 42),
+generated bit-exactly in HBM).  Every lineorder column is 480 MB (SF=20) or
+more, far larger than the 126 MB L2, so no flush is needed between steps.
+
+value     = whole-job fact-column bytes the 13 plans reference / step time (GB/s)
+e2e       = same metric through the C ABI with HOST columns (pinned), the H2D
+            copy of every referenced column and the D2H of results inside the
+            timed region
+roofline  = the fused lineorder kernels (dominant): algorithmic bytes / their
+            CUDA-event time vs MEASURED_PEAKS.json hbm_gbs
+cpu_baseline = the reference's own run_query (oracle/_ref, compiled from the
+            reference sources) on the host cores, one SF=20 suite pass
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+QUERY_NAMES = ["q11", "q12", "q13", "q21", "q22", "q23", "q31", "q32", "q33", "q34",
+               "q41", "q42", "q43"]
+# fact columns each plan references (ssb_queries.cpp:184-199, :237-251): 4 or 6 int32
+FACT_COLS = [4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 6, 6, 6]
+METRIC = "SSB q1.1-q4.3 ms/query and scan GB/s vs HBM roofline"
+
+
+def fact_bytes(q, rows):
+    return 4 * FACT_COLS[q] * rows
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device=0):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------- CPU arms
+
+def reference_suite(ref, h, workers, rows):
+    """One pass of the 13 queries through the reference's own run_query."""
+    t0 = time.perf_counter()
+    per = []
+    for q in range(13):
+        _, _, ms = ref.query(h, q, reference=False, bt=128, ipt=4, workers=workers)
+        per.append(ms)
+    t = time.perf_counter() - t0
+    return t, per
+
+
+def cpu_baseline(sf):
+    """The reference CPU path timed on this host (bounded: one suite pass)."""
+    try:
+        from oracle.oracle import RefImpl
+        ref = RefImpl()
+    except Exception as e:  # pragma: no cover
+        return {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference",
+                "sample": f"unavailable: {e}"}
+    cores = os.cpu_count() or 1
+    h = ref.generate(sf, 42)
+    rows = 6_000_000 * sf
+    t, per = reference_suite(ref, h, cores, rows)
+    ref.free(h)
+    total = sum(fact_bytes(q, rows) for q in range(13))
+    return {"value": round(total / t / 1e9, 3), "unit": "GB/s", "cores": cores, "kind": "reference",
+            "sample": f"one pass of all 13 queries at SF={sf}: tq::run_query(TileConfig{{128,4}}, "
+                      f"workers={cores}) incl. dimension builds",
+            "ms_per_query": [round(x, 2) for x in per], "seconds": round(t, 2)}
+
+
+def run_reference_arm(args, rank, world):
+    """--impl reference: the reference's CPU implementation (oracle/_ref,
+    compiled from the unmodified reference sources) on the host cores."""
+    if rank != 0:
+        return
+    from oracle.oracle import RefImpl
+    ref = RefImpl()
+    cores = os.cpu_count() or 1
+    sf = args.sf or 20
+    # bound the run to a few minutes: sample a smaller SF when the host is slow
+    h = ref.generate(sf, 42)
+    t1, _ = reference_suite(ref, h, cores, 6_000_000 * sf)
+    budget = 150.0
+    if t1 * (args.steps + args.warmup) > budget and sf > 1:
+        ref.free(h)
+        sf_s = max(1, int(sf * budget / (t1 * (args.steps + args.warmup))))
+        h = ref.generate(sf_s, 42)
+        sample_sf = sf_s
+    else:
+        sample_sf = sf
+    rows = 6_000_000 * sample_sf
+    for _ in range(max(0, args.warmup - 1)):
+        reference_suite(ref, h, cores, rows)
+    times = []
+    per_all = []
+    for _ in range(args.steps):
+        t, per = reference_suite(ref, h, cores, rows)
+        times.append(t)
+        per_all.append(per)
+    ref.free(h)
+    total = sum(fact_bytes(q, rows) for q in range(13))
+    tt = sum(times)
+    value = total * args.steps / tt / 1e9
+    ms_q = [round(statistics.mean(p[q] for p in per_all), 2) for q in range(13)]
+    sample = (f"SF={sample_sf} (workload SF={sf}) full 13-query suite per step: tq::run_query("
+              f"TileConfig{{128,4}}, workers={cores}) incl. dimension builds")
+    line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1000 * tt / args.steps, 3),
+            "higher_is_better": True, "scaling": "weak" if world > 1 else "strong",
+            "vs_baseline": None, "dtype": "int32/int64", "data": "synthetic generate_ssb(sf, 42)",
+            "config": {"workload": f"SSB 13-query suite SF={sf}", "sf": sf, "sample_sf": sample_sf,
+                       "queries": QUERY_NAMES},
+            "impl": "reference",
+            "ms_per_query": dict(zip(QUERY_NAMES, ms_q)),
+            "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": cores,
+                             "kind": "reference", "sample": sample},
+            "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- GPU arm
+
+def host_columns_needed(q):
+    from paper_2003_01178_b200 import tq  # noqa: F401
+    # plan column sets (ssb_plans.cpp): used only to count H2D bytes
+    lo = {0: ["lo_orderdate", "lo_discount", "lo_quantity", "lo_extendedprice"]}
+    if q < 3:
+        return {"lineorder": lo[0]}
+    if q < 6:
+        return {"lineorder": ["lo_suppkey", "lo_partkey", "lo_orderdate", "lo_revenue"],
+                "supplier": ["s_suppkey", "s_region"],
+                "part": ["p_partkey", "p_category" if q == 3 else "p_brand1", "p_brand1"],
+                "date": ["d_datekey", "d_year"]}
+    if q < 10:
+        geo = {6: ("region", "nation"), 7: ("nation", "city"), 8: ("city", "city"), 9: ("city", "city")}[q]
+        return {"lineorder": ["lo_suppkey", "lo_custkey", "lo_orderdate", "lo_revenue"],
+                "supplier": ["s_suppkey", "s_" + geo[0], "s_" + geo[1]],
+                "customer": ["c_custkey", "c_" + geo[0], "c_" + geo[1]],
+                "date": ["d_datekey", "d_year"] + (["d_yearmonth"] if q == 9 else [])}
+    return {"lineorder": ["lo_suppkey", "lo_custkey", "lo_partkey", "lo_orderdate", "lo_revenue",
+                          "lo_supplycost"],
+            "supplier": ["s_suppkey", "s_region", "s_nation", "s_city"],
+            "customer": ["c_custkey", "c_region", "c_nation"],
+            "part": ["p_partkey", "p_mfgr", "p_category", "p_brand1"],
+            "date": ["d_datekey", "d_year"]}
+
+
+def run_ours(args, rank, world):
+    import torch
+    import torch.distributed as dist
+    from paper_2003_01178_b200 import dist as cdist
+    from paper_2003_01178_b200 import tq
+
+    dev = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev)
+    sf = args.sf or (20 if world == 1 else 100)
+    cfg = tq.TileConfig(args.bt, args.ipt)
+    sh = cdist.ShardedSSB(sf, 42, device=dev)
+    ctx = sh.ctx
+    rows_shard = sh.lo_end - sh.lo_begin
+    rows_total = cdist.lineorder_rows(sf)
+
+    def step(per_kernel=None, per_total=None):
+        for q in range(13):
+            if world == 1:
+                r = tq.run_query(sh.db, q, cfg)
+                if per_kernel is not None:
+                    k, t = ctx.last_timing()
+                    per_kernel[q].append(k)
+                    per_total[q].append(t)
+            else:
+                r = sh.run_query(q, cfg)
+        return r
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    ctx.bind_torch_stream()
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    ctx.enable_timing(False)
+    launches0 = ctx.launches()
+    with ClockSampler(dev) as clk:
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        barrier()
+    launches = ctx.launches() - launches0
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    total_bytes = sum(fact_bytes(q, rows_total) for q in range(13))
+    value = total_bytes / (ms_step * 1e-3) / 1e9
+
+    # per-query device timing (fused kernel + whole query), separate pass
+    per_kernel = [[] for _ in range(13)]
+    per_total = [[] for _ in range(13)]
+    if world == 1:
+        ctx.enable_timing(True)
+        for _ in range(max(1, min(args.steps, 5))):
+            step(per_kernel, per_total)
+        ctx.enable_timing(False)
+
+    out = None
+    if rank == 0:
+        hbm, peak_kind = peaks()
+        clocks = clk.summary()
+        line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+                "higher_is_better": True, "scaling": "strong" if world > 1 else "strong",
+                "vs_baseline": None, "dtype": "int32/int64",
+                "data": "synthetic: generate_ssb(sf, seed=42) generated bit-exactly in HBM",
+                "config": {"workload": f"SSB 13-query suite SF={sf}"
+                                       + (f", lineorder sharded over {world} GPUs + NCCL reduce" if world > 1 else ""),
+                           "sf": sf, "lineorder_rows": rows_total, "tile": [cfg.block_threads, cfg.items_per_thread],
+                           "l2": "inputs larger than L2 (each lineorder column >= 480 MB vs 126 MB L2); no flush",
+                           "queries": QUERY_NAMES},
+                "gpu_launches": int(launches),
+                "clocks": clocks}
+        if world == 1:
+            kern_ms = [statistics.median(v) for v in per_kernel]
+            tot_ms = [statistics.median(v) for v in per_total]
+            line["ms_per_query"] = dict(zip(QUERY_NAMES, [round(x, 4) for x in tot_ms]))
+            line["fused_kernel_ms"] = dict(zip(QUERY_NAMES, [round(x, 4) for x in kern_ms]))
+            alg = sum(fact_bytes(q, rows_total) for q in range(13))
+            achieved = alg / (sum(kern_ms) * 1e-3) / 1e9
+            line["roofline"] = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
+                                "unit": "GB/s", "frac": round(achieved / hbm, 4),
+                                "traffic": None, "peak_kind": peak_kind,
+                                "kernel": "ssb_flight1_kernel / ssb_join_kernel (fused lineorder pass)",
+                                "algorithmic_bytes": "4 B x referenced fact columns x lineorder rows "
+                                                     "(16 B/row q1-q3, 24 B/row q4), summed over the 13 launches"}
+        out = line
+    return out, sh, sf
+
+
+def e2e_host(args, sh, sf):
+    """Same metric through the C ABI with HOST (pinned) columns: every query
+    copies its referenced columns H2D and its result D2H inside the timed region."""
+    import torch
+    from paper_2003_01178_b200 import tq
+    cfg = tq.TileConfig(args.bt, args.ipt)
+    host = {}
+    for t, cols in [("lineorder", tq.LO_COLS)] + list(tq.DIM_COLS.items()):
+        host[t] = {}
+        for c in cols:
+            a = sh.db.download(t, c)
+            pt = torch.empty(len(a), dtype=torch.int32, pin_memory=True)
+            pt.numpy()[:] = a
+            host[t][c] = pt.numpy()
+    h2d = 0
+    for q in range(13):
+        for t, cols in host_columns_needed(q).items():
+            for c in set(cols):
+                h2d += 4 * len(host[t][c])
+    d2h = 0
+    for q in range(13):
+        cells = tq.query_shape(q)[0]
+        d2h += 64 + 16 * min(cells, 2048)
+    ctx = sh.ctx
+    for _ in range(1):
+        for q in range(13):
+            tq.run_query(host, q, cfg, ctx=ctx)
+    torch.cuda.synchronize()
+    steps = max(1, min(args.steps, 3))
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    ctx.bind_torch_stream()
+    e0.record()
+    for _ in range(steps):
+        for q in range(13):
+            tq.run_query(host, q, cfg, ctx=ctx)
+    e1.record()
+    torch.cuda.synchronize()
+    ms_step = e0.elapsed_time(e1) / steps
+    rows = 6_000_000 * sf
+    total = sum(fact_bytes(q, rows) for q in range(13))
+    return {"value": round(total / (ms_step * 1e-3) / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "ms_per_step": round(ms_step, 3), "steps": steps}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--sf", type=int, default=0)
+    ap.add_argument("--bt", type=int, default=256)
+    ap.add_argument("--ipt", type=int, default=16)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: >= 3 warm-up steps
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    line, sh, sf = run_ours(args, rank, world)
+    if rank == 0:
+        if world == 1 and not args.no_e2e:
+            line["e2e"] = e2e_host(args, sh, sf)
+        elif world > 1:
+            line["e2e"] = None
+        if world == 1 and not args.no_cpu:
+            line["cpu_baseline"] = cpu_baseline(sf)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,191 @@
+/*
+ * crystal_b200.h -- the drop-in C ABI of the B200-native Crystal hot path.
+ *
+ * Plain C: raw pointers, sizes and status codes; no torch or C++ types.  One
+ * shared library (paper_2003_01178_b200/libcrystal_b200.so) exports every
+ * symbol below.  Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/proj).
+ *
+ * Memory: "d_" pointers are DEVICE pointers owned by the caller; "h_"
+ * pointers are host pointers.  Contexts, databases and hash tables are opaque
+ * handles with explicit free.  All calls are synchronous with respect to the
+ * host unless stated (they run on the context's stream and synchronise before
+ * returning when a host-visible result is produced).
+ *
+ * Errors: no C++ exception crosses this boundary.  The reference throws
+ * ConfigError / ContractError / BuildError / IoError (include/tq/common.hpp:16-34);
+ * these map to CRYS_ECONFIG / CRYS_ECONTRACT / CRYS_EBUILD / CRYS_EIO.  The
+ * message is available from crys_last_error().
+ */
+#ifndef CRYSTAL_B200_H
+#define CRYSTAL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  CRYS_OK = 0,
+  CRYS_ECONFIG = 1,   /* tq::ConfigError   (common.hpp:17)  */
+  CRYS_ECONTRACT = 2, /* tq::ContractError (common.hpp:22)  */
+  CRYS_EBUILD = 3,    /* tq::BuildError    (common.hpp:27)  */
+  CRYS_EIO = 4,       /* tq::IoError       (common.hpp:32)  */
+  CRYS_ECUDA = 5,     /* CUDA runtime failure (no reference analogue) */
+  CRYS_ENOTBUILT = 6  /* kernel shape not compiled for sm_100a */
+} crys_status;
+
+/* PredOp (tile.hpp:92): comparison against lo (or inclusive [lo,hi]). */
+typedef enum { CRYS_LT = 0, CRYS_LE, CRYS_GT, CRYS_GE, CRYS_EQ, CRYS_BETWEEN } crys_pred_op;
+
+typedef struct {
+  int32_t op; /* crys_pred_op */
+  int32_t lo;
+  int32_t hi;
+} crys_pred;
+
+/* Output order of a selection (select.hpp:1-17):
+ *   CRYS_ORDER_INPUT   = select_branching/predicated_into(workers=1): input order
+ *   CRYS_ORDER_CRYSTAL = select_tile_into(kDeterministic): blocks in order, each
+ *                        block thread-major over strided items (block_ops.hpp:98-122) */
+typedef enum { CRYS_ORDER_INPUT = 0, CRYS_ORDER_CRYSTAL = 1 } crys_order;
+
+typedef enum { CRYS_SORT_LSB = 0, CRYS_SORT_MSB = 1 } crys_sort_algo;
+
+typedef struct crys_ctx crys_ctx;
+typedef struct crys_db crys_db;
+typedef struct crys_ht crys_ht;
+
+/* ------------------------------------------------------------ context */
+
+/* Thread-local message of the last failing call (any handle). */
+const char* crys_last_error(void);
+/* Library / build identification ("sm_100a ..."). */
+const char* crys_version(void);
+
+/* Bind to CUDA device `device`, create a stream and scratch.  Replaces the
+ * per-call std::thread pool of parallel_for_blocks (kernel.cpp:60-103). */
+crys_status crys_init(int device, crys_ctx** out);
+void crys_destroy(crys_ctx* ctx);
+/* Run subsequent work on `cuda_stream` (a cudaStream_t; NULL = ctx stream). */
+crys_status crys_set_stream(crys_ctx* ctx, void* cuda_stream);
+crys_status crys_synchronize(crys_ctx* ctx);
+/* Number of kernels this ctx launched since creation (telemetry for bench). */
+int64_t crys_kernel_launches(const crys_ctx* ctx);
+
+/* ------------------------------------------------------------ database
+ * An HBM-resident SSB database (columnar int32).  Lineorder may be a row-range
+ * SHARD [lo_begin, lo_end) of the full fact table; dimensions are always whole
+ * (replicated per GPU). Table names: "lineorder","date","supplier","customer",
+ * "part"; column names as ssb_gen.cpp:60-157. */
+
+/* Generate generate_ssb(sf, seed) (ssb_gen.cpp:243-270) directly in HBM,
+ * bit-identical to the host generator; lineorder rows [lo_begin, lo_end) only
+ * (lo_end < 0 means the whole table). */
+crys_status crys_db_generate(crys_ctx* ctx, int64_t sf, uint64_t seed, int64_t lo_begin,
+                             int64_t lo_end, crys_db** out);
+/* Empty database; columns then come from crys_db_upload_column. */
+crys_status crys_db_create(crys_ctx* ctx, int64_t sf, uint64_t seed, crys_db** out);
+/* Copy one host column into HBM (replacing any previous one of that name). */
+crys_status crys_db_upload_column(crys_db* db, const char* table, const char* column,
+                                  const int32_t* h_data, int64_t rows);
+/* Device pointer + rows of a column (borrowed; valid until the db is freed). */
+crys_status crys_db_column(const crys_db* db, const char* table, const char* column,
+                           const int32_t** d_data, int64_t* rows);
+/* Copy a column back to the host (h_out must hold `rows` values). */
+crys_status crys_db_download_column(const crys_db* db, const char* table, const char* column,
+                                    int32_t* h_out, int64_t rows);
+void crys_db_free(crys_db* db);
+
+/* ------------------------------------------------------------ SSB queries
+ * qid: 0..12 = q11 q12 q13 q21 q22 q23 q31 q32 q33 q34 q41 q42 q43 (all_query_ids,
+ * ssb_plans.cpp:301-306).  bt/ipt: TileConfig (tile.hpp:24-36). */
+
+/* Number of dense aggregate cells (AggregateTable::cells, ssb_queries.cpp:17-27)
+ * and group arity of qid. */
+crys_status crys_query_shape(int qid, int64_t* cells, int32_t* ngroup, int32_t* njoins);
+
+/* Replaces tq::run_query(db, id, config, workers, stats) (ssb_queries.hpp:76-78,
+ * ssb_queries.cpp:277-286) on one GPU: dimension hash builds, one fused
+ * lineorder pass, group compaction.  Rows come back lexicographically ordered
+ * (grouped_result, ssb_queries.cpp:145-155): groups row-major [max_rows][3]
+ * (ngroup used), sums [max_rows].  survivors[4] = QueryStats.survivors
+ * (ssb_queries.hpp:70-74).  ECONTRACT (with *nrows set) if max_rows is short. */
+crys_status crys_run_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt,
+                           int32_t* h_groups, int64_t* h_sums, int64_t max_rows,
+                           int64_t* nrows, int64_t* h_survivors);
+
+/* End-to-end variant over HOST columns (the reference's `const SsbDatabase&`):
+ * the query's referenced columns are copied H2D inside the call, then as
+ * crys_run_query.  Tables are described by parallel arrays of names/pointers. */
+typedef struct {
+  const char* table;
+  const char* column;
+  const int32_t* h_data;
+  int64_t rows;
+} crys_host_column;
+crys_status crys_run_query_host(crys_ctx* ctx, const crys_host_column* cols, int ncols, int qid,
+                                int bt, int ipt, int32_t* h_groups, int64_t* h_sums,
+                                int64_t max_rows, int64_t* nrows, int64_t* h_survivors);
+
+/* Multi-GPU building blocks (lineorder row-range shards):
+ * the shard's dense partial aggregate -> d_agg = int64[2*cells] laid out as
+ * [sums | counts] (the payload of the one NCCL reduce), survivors accumulated
+ * into d_survivors (int64[4]).  Asynchronous on the ctx stream. */
+crys_status crys_query_partial(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt,
+                               int64_t* d_agg, int64_t* d_survivors);
+/* Compact a (reduced) dense aggregate on the device into result rows. */
+crys_status crys_query_finalize(crys_ctx* ctx, int qid, const int64_t* d_agg,
+                                int32_t* h_groups, int64_t* h_sums, int64_t max_rows,
+                                int64_t* nrows);
+/* Same compaction on the host (pure CPU; no device needed). */
+crys_status crys_query_finalize_host(int qid, const int64_t* h_agg, int32_t* h_groups,
+                                     int64_t* h_sums, int64_t max_rows, int64_t* nrows);
+
+/* ------------------------------------------------------------ operators */
+
+/* Replaces select_{branching,predicated}_into(workers=1) (order INPUT) and
+ * select_tile_into(config, kDeterministic) (order CRYSTAL), select.hpp:56-135.
+ * d_out must hold n values; *count = matches. */
+crys_status crys_select_i32(crys_ctx* ctx, const int32_t* d_in, int64_t n, crys_pred pred,
+                            int32_t* d_out, int64_t* count, int order, int bt, int ipt);
+
+/* Replaces project_linear_into / project_sigmoid_into (project.hpp:49-64). */
+crys_status crys_project_f32(crys_ctx* ctx, const float* d_x1, const float* d_x2, int64_t n,
+                             float a, float b, float* d_out, int sigmoid, int bt, int ipt);
+
+/* Replaces HashTable::build (hash_table.hpp:29-30, hash_table.cpp:20-94):
+ * capacity a power of two >= 2 (ECONFIG), n*2 <= capacity, no INT32_MIN or
+ * duplicate keys (EBUILD).  Slots are interleaved {key, payload} int2. */
+crys_status crys_ht_build(crys_ctx* ctx, const int32_t* d_keys, const int32_t* d_payloads,
+                          int64_t n, int64_t capacity, crys_ht** out);
+/* Slot arrays back to the host (for layout checks): capacity keys/payloads. */
+crys_status crys_ht_download(const crys_ht* ht, int32_t* h_keys, int32_t* h_payloads);
+int64_t crys_ht_capacity(const crys_ht* ht);
+void crys_ht_free(crys_ht* ht);
+
+/* Replaces join_probe_{scalar,prefetch,tile} (join.hpp:17-32, join.cpp:53-96):
+ * *checksum = sum over hits of (build payload + probe payload), int64. */
+crys_status crys_join_probe_sum(crys_ctx* ctx, const int32_t* d_keys, const int32_t* d_payloads,
+                                int64_t n, const crys_ht* ht, int bt, int ipt, int64_t* checksum);
+
+/* Replaces lsb_radix_sort / msb_radix_sort (radix.hpp:90-93, radix.cpp:138-216),
+ * in place on device key/payload arrays.  LSB: stable, bits_per_pass in [1,8]
+ * (== std::stable_sort by key).  MSB: keys ascending, pairs preserved. */
+crys_status crys_sort_pairs(crys_ctx* ctx, int32_t* d_keys, int32_t* d_payloads, int64_t n,
+                            int algo, int bits_per_pass);
+
+/* ------------------------------------------------------------ timing hooks
+ * Device-timed (CUDA events on the ctx stream) duration of the last call's
+ * dominant kernel (the fused lineorder pass / select / probe / sort passes)
+ * and of the whole call, in milliseconds. */
+crys_status crys_last_timing(const crys_ctx* ctx, double* kernel_ms, double* total_ms);
+/* Enable per-call event timing (adds two event records per call). */
+crys_status crys_enable_timing(crys_ctx* ctx, int enable);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CRYSTAL_B200_H */

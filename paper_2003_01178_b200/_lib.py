@@ -1,0 +1,82 @@
+"""ctypes binding of the C ABI in include/crystal_b200.h.
+
+The product path has exactly one implementation: libcrystal_b200.so (sm_100a
+CUDA kernels).  If the library is missing this module raises at import time;
+there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcrystal_b200.so")
+
+CRYS_OK, CRYS_ECONFIG, CRYS_ECONTRACT, CRYS_EBUILD, CRYS_EIO, CRYS_ECUDA, CRYS_ENOTBUILT = range(7)
+CRYS_LT, CRYS_LE, CRYS_GT, CRYS_GE, CRYS_EQ, CRYS_BETWEEN = range(6)
+CRYS_ORDER_INPUT, CRYS_ORDER_CRYSTAL = 0, 1
+CRYS_SORT_LSB, CRYS_SORT_MSB = 0, 1
+
+
+class crys_pred(C.Structure):
+    _fields_ = [("op", C.c_int32), ("lo", C.c_int32), ("hi", C.c_int32)]
+
+
+class crys_host_column(C.Structure):
+    _fields_ = [("table", C.c_char_p), ("column", C.c_char_p), ("h_data", C.c_void_p),
+                ("rows", C.c_int64)]
+
+
+# (name, restype, argtypes) for every exported symbol of crystal_b200.h
+_P = C.c_void_p
+_I32P = C.POINTER(C.c_int32)
+_I64P = C.POINTER(C.c_int64)
+SIGNATURES = [
+    ("crys_last_error", C.c_char_p, []),
+    ("crys_version", C.c_char_p, []),
+    ("crys_init", C.c_int, [C.c_int, C.POINTER(_P)]),
+    ("crys_destroy", None, [_P]),
+    ("crys_set_stream", C.c_int, [_P, _P]),
+    ("crys_synchronize", C.c_int, [_P]),
+    ("crys_kernel_launches", C.c_int64, [_P]),
+    ("crys_db_generate", C.c_int, [_P, C.c_int64, C.c_uint64, C.c_int64, C.c_int64, C.POINTER(_P)]),
+    ("crys_db_create", C.c_int, [_P, C.c_int64, C.c_uint64, C.POINTER(_P)]),
+    ("crys_db_upload_column", C.c_int, [_P, C.c_char_p, C.c_char_p, _P, C.c_int64]),
+    ("crys_db_column", C.c_int, [_P, C.c_char_p, C.c_char_p, C.POINTER(_P), _I64P]),
+    ("crys_db_download_column", C.c_int, [_P, C.c_char_p, C.c_char_p, _P, C.c_int64]),
+    ("crys_db_free", None, [_P]),
+    ("crys_query_shape", C.c_int, [C.c_int, _I64P, _I32P, _I32P]),
+    ("crys_run_query", C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, _P, _P, C.c_int64, _I64P, _P]),
+    ("crys_run_query_host", C.c_int, [_P, C.POINTER(crys_host_column), C.c_int, C.c_int, C.c_int,
+                                      C.c_int, _P, _P, C.c_int64, _I64P, _P]),
+    ("crys_query_partial", C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, _P, _P]),
+    ("crys_query_finalize", C.c_int, [_P, C.c_int, _P, _P, _P, C.c_int64, _I64P]),
+    ("crys_query_finalize_host", C.c_int, [C.c_int, _P, _P, _P, C.c_int64, _I64P]),
+    ("crys_select_i32", C.c_int, [_P, _P, C.c_int64, crys_pred, _P, _I64P, C.c_int, C.c_int, C.c_int]),
+    ("crys_project_f32", C.c_int, [_P, _P, _P, C.c_int64, C.c_float, C.c_float, _P, C.c_int,
+                                   C.c_int, C.c_int]),
+    ("crys_ht_build", C.c_int, [_P, _P, _P, C.c_int64, C.c_int64, C.POINTER(_P)]),
+    ("crys_ht_download", C.c_int, [_P, _P, _P]),
+    ("crys_ht_capacity", C.c_int64, [_P]),
+    ("crys_ht_free", None, [_P]),
+    ("crys_join_probe_sum", C.c_int, [_P, _P, _P, C.c_int64, _P, C.c_int, C.c_int, _I64P]),
+    ("crys_sort_pairs", C.c_int, [_P, _P, _P, C.c_int64, C.c_int, C.c_int]),
+    ("crys_last_timing", C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    ("crys_enable_timing", C.c_int, [_P, C.c_int]),
+]
+
+
+def _load() -> C.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: the B200 kernels are not built "
+            "(run `make lib` or __graft_entry__.build()); there is no CPU fallback")
+    lib = C.CDLL(LIB_PATH)
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+LIB = _load()

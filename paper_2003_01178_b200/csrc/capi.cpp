@@ -1,0 +1,501 @@
+// capi.cpp -- the extern "C" boundary (include/crystal_b200.h).
+//
+// Every entry point catches internal errors and maps them to crys_status, the
+// C-ABI image of the reference's exception taxonomy (include/tq/common.hpp:
+// 16-34).  No C++ exception crosses this boundary.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.hpp"
+
+namespace {
+thread_local std::string g_last_error;
+
+template <class F>
+crys_status guarded(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return CRYS_OK;
+  } catch (const crys::Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return CRYS_ECUDA;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return CRYS_ECONTRACT;
+  }
+}
+
+void bind(crys_ctx* ctx) {
+  CRYS_CHECK(ctx != nullptr, CRYS_ECONFIG, "null context");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+}
+}  // namespace
+
+crys_ctx::~crys_ctx() {
+  for (auto& e : ev)
+    if (e) cudaEventDestroy(e);
+  qws.reset();
+  sws.reset();
+  delete staging;
+  if (own_stream) cudaStreamDestroy(own_stream);
+}
+
+const int32_t* crys_db::col(const std::string& table, const std::string& column, int64_t* rows) const {
+  auto it = cols.find(table + "." + column);
+  CRYS_CHECK(it != cols.end(), CRYS_ECONTRACT, "table " + table + ": no column " + column);
+  if (rows) *rows = it->second.rows;
+  return it->second.buf->as<int32_t>();
+}
+
+int64_t crys_db::table_rows(const std::string& table) const {
+  for (auto& kv : cols)
+    if (kv.first.compare(0, table.size() + 1, table + ".") == 0) return kv.second.rows;
+  return 0;
+}
+
+namespace crys {
+
+void timing_begin(crys_ctx* c) {
+  if (c->timing) CUDA_TRY(cudaEventRecord(c->ev[0], c->stream));
+}
+void timing_kernel_begin(crys_ctx* c) {
+  if (c->timing) CUDA_TRY(cudaEventRecord(c->ev[1], c->stream));
+}
+void timing_kernel_end(crys_ctx* c) {
+  if (c->timing) CUDA_TRY(cudaEventRecord(c->ev[2], c->stream));
+}
+void timing_end(crys_ctx* c) {
+  if (!c->timing) return;
+  CUDA_TRY(cudaEventRecord(c->ev[3], c->stream));
+  CUDA_TRY(cudaEventSynchronize(c->ev[3]));
+  float k = 0, t = 0;
+  CUDA_TRY(cudaEventElapsedTime(&k, c->ev[1], c->ev[2]));
+  CUDA_TRY(cudaEventElapsedTime(&t, c->ev[0], c->ev[3]));
+  c->kernel_ms = k;
+  c->total_ms = t;
+}
+
+// Result rows -> (groups, sums) in lexicographic order.
+void emit_rows(int qid, const std::vector<int64_t>& cell, const std::vector<int64_t>& sums,
+               int32_t* h_groups, int64_t* h_sums, int64_t max_rows, int64_t* nrows) {
+  const QueryPlan& plan = plan_for(qid);
+  const int64_t n = (int64_t)cell.size();
+  *nrows = n;
+  CRYS_CHECK(n <= max_rows, CRYS_ECONTRACT, "result has more rows than the caller's buffer");
+  std::vector<int64_t> strides(plan.group.size(), 1);
+  int64_t s = 1;
+  for (int g = (int)plan.group.size() - 1; g >= 0; --g) {
+    strides[g] = s;
+    s *= (int64_t)(plan.group[g].hi - plan.group[g].lo + 1);
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t idx = cell[(size_t)i];
+    for (size_t g = 0; g < plan.group.size(); ++g) {  // AggregateTable::key_of (ssb_queries.cpp:49-56)
+      if (h_groups) h_groups[i * 3 + (int64_t)g] = plan.group[g].lo + (int32_t)(idx / strides[g]);
+      idx %= strides[g];
+    }
+    if (h_sums) h_sums[i] = sums[(size_t)i];
+  }
+}
+
+}  // namespace crys
+
+extern "C" {
+
+const char* crys_last_error(void) { return g_last_error.c_str(); }
+
+const char* crys_version(void) {
+  return "crystal_b200 1.0 (sm_100a; fused SSB q1.1-q4.3, select/project, hash join, radix sort)";
+}
+
+crys_status crys_init(int device, crys_ctx** out) {
+  return guarded([&] {
+    CRYS_CHECK(out != nullptr, CRYS_ECONFIG, "null output handle");
+    int n = 0;
+    CUDA_TRY(cudaGetDeviceCount(&n));
+    CRYS_CHECK(device >= 0 && device < n, CRYS_ECONFIG, "no such CUDA device");
+    CUDA_TRY(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    CRYS_CHECK(prop.major == 10, CRYS_ENOTBUILT,
+               std::string("library is compiled for sm_100a only; device is ") + prop.name);
+    auto* ctx = new crys_ctx();
+    ctx->device = device;
+    ctx->num_sms = prop.multiProcessorCount;
+    cudaError_t e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      delete ctx;
+      crys::fail(CRYS_ECUDA, cudaGetErrorString(e));
+    }
+    ctx->stream = ctx->own_stream;
+    for (auto& ev : ctx->ev) CUDA_TRY(cudaEventCreate(&ev));
+    *out = ctx;
+  });
+}
+
+void crys_destroy(crys_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  delete ctx;
+}
+
+crys_status crys_set_stream(crys_ctx* ctx, void* s) {
+  return guarded([&] {
+    bind(ctx);
+    ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own_stream;
+  });
+}
+
+crys_status crys_synchronize(crys_ctx* ctx) {
+  return guarded([&] {
+    bind(ctx);
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int64_t crys_kernel_launches(const crys_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+crys_status crys_enable_timing(crys_ctx* ctx, int enable) {
+  return guarded([&] {
+    bind(ctx);
+    ctx->timing = enable != 0;
+  });
+}
+
+crys_status crys_last_timing(const crys_ctx* ctx, double* kernel_ms, double* total_ms) {
+  return guarded([&] {
+    CRYS_CHECK(ctx != nullptr, CRYS_ECONFIG, "null context");
+    if (kernel_ms) *kernel_ms = ctx->kernel_ms;
+    if (total_ms) *total_ms = ctx->total_ms;
+  });
+}
+
+// ---------------------------------------------------------------- database
+
+crys_status crys_db_generate(crys_ctx* ctx, int64_t sf, uint64_t seed, int64_t lo_begin,
+                             int64_t lo_end, crys_db** out) {
+  return guarded([&] {
+    bind(ctx);
+    CRYS_CHECK(out != nullptr, CRYS_ECONFIG, "null output handle");
+    CRYS_CHECK(sf >= 1, CRYS_ECONFIG, "scale factor must be >= 1");
+    auto* db = new crys_db();
+    db->ctx = ctx;
+    db->sf = sf;
+    db->seed = seed;
+    db->lo_begin = lo_begin;
+    db->lo_end = lo_end;
+    try {
+      crys::ssb_generate(ctx, db);
+    } catch (...) {
+      delete db;
+      throw;
+    }
+    *out = db;
+  });
+}
+
+crys_status crys_db_create(crys_ctx* ctx, int64_t sf, uint64_t seed, crys_db** out) {
+  return guarded([&] {
+    bind(ctx);
+    CRYS_CHECK(out != nullptr, CRYS_ECONFIG, "null output handle");
+    auto* db = new crys_db();
+    db->ctx = ctx;
+    db->sf = sf;
+    db->seed = seed;
+    *out = db;
+  });
+}
+
+crys_status crys_db_upload_column(crys_db* db, const char* table, const char* column,
+                                  const int32_t* h_data, int64_t rows) {
+  return guarded([&] {
+    CRYS_CHECK(db && table && column, CRYS_ECONFIG, "null argument");
+    bind(db->ctx);
+    CRYS_CHECK(rows >= 0 && (rows == 0 || h_data), CRYS_ECONFIG, "bad column data");
+    auto& c = db->cols[std::string(table) + "." + column];
+    if (!c.buf) c.buf.reset(new crys::DevBuf());
+    c.buf->reserve(sizeof(int32_t) * (size_t)std::max<int64_t>(rows, 1));
+    c.rows = rows;
+    if (rows)
+      CUDA_TRY(cudaMemcpyAsync(c.buf->p, h_data, sizeof(int32_t) * (size_t)rows,
+                               cudaMemcpyHostToDevice, db->ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(db->ctx->stream));
+    if (std::string(table) == "lineorder") {
+      db->lo_begin = 0;
+      db->lo_end = rows;
+    }
+  });
+}
+
+crys_status crys_db_column(const crys_db* db, const char* table, const char* column,
+                           const int32_t** d_data, int64_t* rows) {
+  return guarded([&] {
+    CRYS_CHECK(db && table && column && d_data, CRYS_ECONFIG, "null argument");
+    *d_data = db->col(table, column, rows);
+  });
+}
+
+crys_status crys_db_download_column(const crys_db* db, const char* table, const char* column,
+                                    int32_t* h_out, int64_t rows) {
+  return guarded([&] {
+    CRYS_CHECK(db && table && column && h_out, CRYS_ECONFIG, "null argument");
+    bind(db->ctx);
+    int64_t n = 0;
+    const int32_t* d = db->col(table, column, &n);
+    CRYS_CHECK(rows == n, CRYS_ECONTRACT, "row count mismatch");
+    if (n)
+      CUDA_TRY(cudaMemcpyAsync(h_out, d, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToHost,
+                               db->ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(db->ctx->stream));
+  });
+}
+
+void crys_db_free(crys_db* db) {
+  if (!db) return;
+  cudaSetDevice(db->ctx->device);
+  cudaStreamSynchronize(db->ctx->stream);
+  delete db;
+}
+
+// ---------------------------------------------------------------- queries
+
+crys_status crys_query_shape(int qid, int64_t* cells, int32_t* ngroup, int32_t* njoins) {
+  return guarded([&] {
+    const crys::QueryPlan& p = crys::plan_for(qid);
+    if (cells) *cells = p.cells();
+    if (ngroup) *ngroup = (int32_t)p.group.size();
+    if (njoins) *njoins = (int32_t)p.joins.size();
+  });
+}
+
+static void fill_survivors(int qid, const crys::ResultRows& r, int64_t* h_survivors) {
+  if (!h_survivors) return;
+  const crys::QueryPlan& p = crys::plan_for(qid);
+  const int ns = p.joins.empty() ? 1 : (int)p.joins.size();
+  for (int j = 0; j < 4; ++j) h_survivors[j] = j < ns ? r.survivors[j] : 0;
+}
+
+crys_status crys_run_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt,
+                           int32_t* h_groups, int64_t* h_sums, int64_t max_rows, int64_t* nrows,
+                           int64_t* h_survivors) {
+  return guarded([&] {
+    bind(ctx);
+    CRYS_CHECK(db != nullptr && nrows != nullptr, CRYS_ECONFIG, "null argument");
+    CRYS_CHECK(bt > 0 && ipt > 0, CRYS_ECONFIG, "TileConfig: block_threads/items_per_thread must be positive");
+    crys::ResultRows r;
+    crys::ssb_run_query(ctx, db, qid, bt, ipt, &r);
+    fill_survivors(qid, r, h_survivors);
+    crys::emit_rows(qid, r.cell, r.sum, h_groups, h_sums, max_rows, nrows);
+  });
+}
+
+crys_status crys_run_query_host(crys_ctx* ctx, const crys_host_column* cols, int ncols, int qid,
+                                int bt, int ipt, int32_t* h_groups, int64_t* h_sums,
+                                int64_t max_rows, int64_t* nrows, int64_t* h_survivors) {
+  return guarded([&] {
+    bind(ctx);
+    CRYS_CHECK(cols != nullptr && ncols > 0 && nrows != nullptr, CRYS_ECONFIG, "null argument");
+    CRYS_CHECK(bt > 0 && ipt > 0, CRYS_ECONFIG, "TileConfig: block_threads/items_per_thread must be positive");
+    const crys::QueryPlan& plan = crys::plan_for(qid);
+    // The columns the plan references: fact keys / filters / aggregates and
+    // each joined dimension's key, filter and payload columns.
+    std::vector<std::pair<std::string, std::string>> need;
+    for (auto& f : plan.fact_filters) need.push_back({"lineorder", f.column});
+    for (auto& j : plan.joins) {
+      need.push_back({"lineorder", j.fact_key});
+      need.push_back({j.dim_table, j.dim_key});
+      for (auto& f : j.filters) need.push_back({j.dim_table, f.column});
+      if (!j.payload.empty()) need.push_back({j.dim_table, j.payload});
+    }
+    if (plan.agg == crys::kAggExtPriceTimesDiscount) {
+      need.push_back({"lineorder", "lo_extendedprice"});
+      need.push_back({"lineorder", "lo_discount"});
+    } else {
+      need.push_back({"lineorder", "lo_revenue"});
+      if (plan.agg == crys::kAggRevenueMinusSupplyCost) need.push_back({"lineorder", "lo_supplycost"});
+    }
+    // Staging database owned by the context: device buffers are reused across
+    // calls, but every call copies its inputs H2D (the reference takes a host
+    // `const SsbDatabase&`).
+    if (!ctx->staging) {
+      ctx->staging = new crys_db();
+      ctx->staging->ctx = ctx;
+    }
+    crys_db* staging = ctx->staging;
+    for (auto& tc : need) {
+      const crys_host_column* hc = nullptr;
+      for (int i = 0; i < ncols; ++i)
+        if (tc.first == cols[i].table && tc.second == cols[i].column) hc = &cols[i];
+      CRYS_CHECK(hc != nullptr, CRYS_ECONTRACT, "table " + tc.first + ": no column " + tc.second);
+      auto& c = staging->cols[tc.first + "." + tc.second];
+      if (!c.buf) c.buf.reset(new crys::DevBuf());
+      c.buf->reserve(sizeof(int32_t) * (size_t)std::max<int64_t>(hc->rows, 1));
+      c.rows = hc->rows;
+      if (hc->rows)
+        CUDA_TRY(cudaMemcpyAsync(c.buf->p, hc->h_data, sizeof(int32_t) * (size_t)hc->rows,
+                                 cudaMemcpyHostToDevice, ctx->stream));
+    }
+    crys::ResultRows r;
+    crys::ssb_run_query(ctx, staging, qid, bt, ipt, &r);
+    fill_survivors(qid, r, h_survivors);
+    crys::emit_rows(qid, r.cell, r.sum, h_groups, h_sums, max_rows, nrows);
+  });
+}
+
+crys_status crys_query_partial(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt,
+                               int64_t* d_agg, int64_t* d_survivors) {
+  return guarded([&] {
+    bind(ctx);
+    CRYS_CHECK(db && d_agg && d_survivors, CRYS_ECONFIG, "null argument");
+    ctx->scratch2.reserve(64);
+    int32_t* err = ctx->scratch2.as<int32_t>();
+    CUDA_TRY(cudaMemsetAsync(err, 0, sizeof(int32_t), ctx->stream));
+    crys::ssb_query_partial(ctx, db, qid, bt, ipt, reinterpret_cast<unsigned long long*>(d_agg),
+                            reinterpret_cast<unsigned long long*>(d_survivors), err);
+  });
+}
+
+crys_status crys_query_finalize(crys_ctx* ctx, int qid, const int64_t* d_agg, int32_t* h_groups,
+                                int64_t* h_sums, int64_t max_rows, int64_t* nrows) {
+  return guarded([&] {
+    bind(ctx);
+    CRYS_CHECK(d_agg && nrows, CRYS_ECONFIG, "null argument");
+    crys::ResultRows r;
+    crys::ssb_finalize_device(ctx, qid, reinterpret_cast<const unsigned long long*>(d_agg), &r);
+    crys::emit_rows(qid, r.cell, r.sum, h_groups, h_sums, max_rows, nrows);
+  });
+}
+
+crys_status crys_query_finalize_host(int qid, const int64_t* h_agg, int32_t* h_groups,
+                                     int64_t* h_sums, int64_t max_rows, int64_t* nrows) {
+  return guarded([&] {
+    CRYS_CHECK(h_agg && nrows, CRYS_ECONFIG, "null argument");
+    const crys::QueryPlan& plan = crys::plan_for(qid);
+    const int64_t cells = plan.cells();
+    std::vector<int64_t> cell, sums;
+    for (int64_t c = 0; c < cells; ++c) {
+      if (h_agg[cells + c] != 0 || (plan.joins.empty() && c == 0)) {
+        cell.push_back(c);
+        sums.push_back(h_agg[c]);
+      }
+    }
+    crys::emit_rows(qid, cell, sums, h_groups, h_sums, max_rows, nrows);
+  });
+}
+
+// ---------------------------------------------------------------- operators
+
+crys_status crys_select_i32(crys_ctx* ctx, const int32_t* d_in, int64_t n, crys_pred pred,
+                            int32_t* d_out, int64_t* count, int order, int bt, int ipt) {
+  return guarded([&] {
+    bind(ctx);
+    CRYS_CHECK(count != nullptr, CRYS_ECONFIG, "null argument");
+    CRYS_CHECK(n == 0 || (d_in && d_out), CRYS_ECONFIG, "null argument");
+    int32_t lo, hi;
+    crys::lower_pred(pred, &lo, &hi);
+    crys::timing_begin(ctx);
+    *count = crys::select_i32(ctx, d_in, n, lo, hi, d_out, order, bt, ipt);
+    crys::timing_end(ctx);
+  });
+}
+
+crys_status crys_project_f32(crys_ctx* ctx, const float* d_x1, const float* d_x2, int64_t n,
+                             float a, float b, float* d_out, int sigmoid, int bt, int ipt) {
+  return guarded([&] {
+    bind(ctx);
+    CRYS_CHECK(bt > 0 && ipt > 0, CRYS_ECONFIG, "TileConfig: block_threads/items_per_thread must be positive");
+    CRYS_CHECK(n == 0 || (d_x1 && d_x2 && d_out), CRYS_ECONFIG, "null argument");
+    crys::timing_begin(ctx);
+    crys::project_f32(ctx, d_x1, d_x2, n, a, b, d_out, sigmoid);
+    crys::timing_end(ctx);
+  });
+}
+
+crys_status crys_ht_build(crys_ctx* ctx, const int32_t* d_keys, const int32_t* d_payloads,
+                          int64_t n, int64_t capacity, crys_ht** out) {
+  return guarded([&] {
+    bind(ctx);
+    CRYS_CHECK(out != nullptr, CRYS_ECONFIG, "null output handle");
+    // shift_for_capacity (hash_table.cpp:12-16) and the 50% fill rule (:24-26)
+    CRYS_CHECK(capacity >= 2 && (capacity & (capacity - 1)) == 0 && capacity <= (1LL << 31),
+               CRYS_ECONFIG, "HashTable: capacity must be a power of two >= 2");
+    CRYS_CHECK(n >= 0, CRYS_ECONFIG, "HashTable: negative build size");
+    if (n * 2 > capacity) crys::fail(CRYS_EBUILD, "HashTable: capacity overflow (fill would exceed 50%)");
+    CRYS_CHECK(n == 0 || (d_keys && d_payloads), CRYS_ECONFIG, "null argument");
+    auto* ht = new crys_ht();
+    ht->ctx = ctx;
+    ht->capacity = capacity;
+    int lg = 0;
+    while ((1LL << lg) < capacity) ++lg;
+    ht->shift = 32 - lg;
+    try {
+      ht->slots.reserve(sizeof(int2) * (size_t)capacity);
+      crys::ht_build(ctx, ht, d_keys, d_payloads, n);
+    } catch (...) {
+      delete ht;
+      throw;
+    }
+    *out = ht;
+  });
+}
+
+crys_status crys_ht_download(const crys_ht* ht, int32_t* h_keys, int32_t* h_payloads) {
+  return guarded([&] {
+    CRYS_CHECK(ht != nullptr, CRYS_ECONFIG, "null hash table");
+    bind(ht->ctx);
+    std::vector<int2> v((size_t)ht->capacity);
+    CUDA_TRY(cudaMemcpy(v.data(), ht->slots.p, sizeof(int2) * v.size(), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < v.size(); ++i) {
+      if (h_keys) h_keys[i] = v[i].x;
+      if (h_payloads) h_payloads[i] = v[i].y;
+    }
+  });
+}
+
+int64_t crys_ht_capacity(const crys_ht* ht) { return ht ? ht->capacity : 0; }
+
+void crys_ht_free(crys_ht* ht) {
+  if (!ht) return;
+  cudaSetDevice(ht->ctx->device);
+  cudaStreamSynchronize(ht->ctx->stream);
+  delete ht;
+}
+
+crys_status crys_join_probe_sum(crys_ctx* ctx, const int32_t* d_keys, const int32_t* d_payloads,
+                                int64_t n, const crys_ht* ht, int bt, int ipt, int64_t* checksum) {
+  return guarded([&] {
+    bind(ctx);
+    CRYS_CHECK(ht && checksum, CRYS_ECONFIG, "null argument");
+    CRYS_CHECK(bt > 0 && ipt > 0, CRYS_ECONFIG, "TileConfig: block_threads/items_per_thread must be positive");
+    CRYS_CHECK(n >= 0 && (n == 0 || (d_keys && d_payloads)), CRYS_ECONFIG, "bad probe input");
+    crys::timing_begin(ctx);
+    *checksum = crys::join_probe_sum(ctx, d_keys, d_payloads, n, ht);
+    crys::timing_end(ctx);
+  });
+}
+
+crys_status crys_sort_pairs(crys_ctx* ctx, int32_t* d_keys, int32_t* d_payloads, int64_t n,
+                            int algo, int bits_per_pass) {
+  return guarded([&] {
+    bind(ctx);
+    CRYS_CHECK(n >= 0 && (n == 0 || (d_keys && d_payloads)), CRYS_ECONFIG, "bad sort input");
+    CRYS_CHECK(algo == CRYS_SORT_LSB || algo == CRYS_SORT_MSB, CRYS_ECONFIG, "unknown sort algorithm");
+    if (algo == CRYS_SORT_LSB)
+      CRYS_CHECK(bits_per_pass >= 1 && bits_per_pass <= 8, CRYS_ECONFIG,
+                 "lsb_radix_sort: bits_per_pass must be in [1,8]");
+    crys::timing_begin(ctx);
+    crys::sort_pairs(ctx, d_keys, d_payloads, n, algo, bits_per_pass);
+    crys::timing_end(ctx);
+  });
+}
+
+}  // extern "C"

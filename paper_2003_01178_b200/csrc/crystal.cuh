@@ -1,0 +1,334 @@
+// crystal.cuh -- the Crystal block-wide primitives (PAPER Table 1) for sm_100a.
+//
+// The reference restates them for a CPU "block" in include/tq/block_ops.hpp
+// (block_load :23-32, block_load_sel :36-50, block_pred :54-69, block_scan
+// :73-82, block_thread_counts :85-96, block_shuffle :101-122, block_store
+// :125-131, block_aggregate :141-173) and include/tq/hash_table.hpp (probe
+// :41-51, block_lookup :68-87, build hash_table.cpp:20-94).  Here a tile lives
+// in REGISTERS: each of the BT threads of a CTA owns IPT items, and flags are a
+// per-thread bitmask (bit k = item k) instead of a 1-byte-per-slot bitmap.
+//
+// Two ownership layouts:
+//   Striped   item k of thread t is tile slot t + k*BT (the reference's
+//             logical-thread ownership, tile.hpp:3-8; coalesced scalar loads).
+//   VecLayout item k of thread t is slot (k/VEC)*BT*VEC + t*VEC + k%VEC: every
+//             load instruction is one VEC-wide vector per lane and a warp
+//             covers 32*VEC*4 contiguous bytes -> 128-bit coalesced HBM reads.
+//             A selective load (BlockLoadSel) skips a whole vector when none of
+//             its VEC flags is set, so dead 32 B sectors are never requested.
+#pragma once
+
+#include "common.cuh"
+
+namespace crys {
+
+template <int BT, int IPT>
+struct VecLayout {
+  static constexpr int VEC = (IPT % 4 == 0) ? 4 : ((IPT % 2 == 0) ? 2 : 1);
+  static constexpr int NV = IPT / VEC;
+  static constexpr int TILE = BT * IPT;
+  static_assert(IPT >= 1 && IPT <= 32, "flags are a 32-bit mask");
+  __device__ __forceinline__ static int slot(int t, int k) {
+    return (k / VEC) * BT * VEC + t * VEC + (k % VEC);
+  }
+  __device__ __forceinline__ static unsigned vec_bits(unsigned flags, int v) {
+    return (flags >> (v * VEC)) & ((1u << VEC) - 1u);
+  }
+};
+
+// Items of this thread that fall inside a partial tile of `valid` slots.
+template <int BT, int IPT>
+__device__ __forceinline__ unsigned BlockValidMask(int valid) {
+  using L = VecLayout<BT, IPT>;
+  if (valid >= L::TILE) return IPT == 32 ? 0xffffffffu : ((1u << IPT) - 1u);
+  unsigned m = 0;
+#pragma unroll
+  for (int k = 0; k < IPT; ++k)
+    if (L::slot(threadIdx.x, k) < valid) m |= 1u << k;
+  return m;
+}
+
+// BlockLoad (block_ops.hpp:23-32): the thread's items of a tile, VecLayout.
+// Slots at/after `valid` are not read (their items stay undefined, like the
+// reference's poisoned slots).
+template <int BT, int IPT>
+__device__ __forceinline__ void BlockLoad(const int32_t* __restrict__ tile, int valid,
+                                          int32_t (&items)[IPT]) {
+  using L = VecLayout<BT, IPT>;
+#pragma unroll
+  for (int v = 0; v < L::NV; ++v) {
+    const int s = v * BT * L::VEC + threadIdx.x * L::VEC;
+    const int32_t* p = tile + s;
+    if (s + L::VEC <= valid) {
+      if constexpr (L::VEC == 4) {
+        int4 x = ld_stream4(p);
+        items[v * 4 + 0] = x.x; items[v * 4 + 1] = x.y; items[v * 4 + 2] = x.z; items[v * 4 + 3] = x.w;
+      } else if constexpr (L::VEC == 2) {
+        int2 x = ld_stream2(p);
+        items[v * 2 + 0] = x.x; items[v * 2 + 1] = x.y;
+      } else {
+        items[v] = ld_stream1(p);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < L::VEC; ++e)
+        if (s + e < valid) items[v * L::VEC + e] = ld_stream1(p + e);
+    }
+  }
+}
+
+// BlockLoadSel (block_ops.hpp:36-50): load only vectors holding a set flag.
+// A fully false bitmap touches no source memory, as in the reference.
+template <int BT, int IPT>
+__device__ __forceinline__ void BlockLoadSel(const int32_t* __restrict__ tile, int valid,
+                                             unsigned flags, int32_t (&items)[IPT]) {
+  using L = VecLayout<BT, IPT>;
+#pragma unroll
+  for (int v = 0; v < L::NV; ++v) {
+    if (L::vec_bits(flags, v) == 0) continue;
+    const int s = v * BT * L::VEC + threadIdx.x * L::VEC;
+    const int32_t* p = tile + s;
+    if (s + L::VEC <= valid) {
+      if constexpr (L::VEC == 4) {
+        int4 x = ld_stream4(p);
+        items[v * 4 + 0] = x.x; items[v * 4 + 1] = x.y; items[v * 4 + 2] = x.z; items[v * 4 + 3] = x.w;
+      } else if constexpr (L::VEC == 2) {
+        int2 x = ld_stream2(p);
+        items[v * 2 + 0] = x.x; items[v * 2 + 1] = x.y;
+      } else {
+        items[v] = ld_stream1(p);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < L::VEC; ++e)
+        if (s + e < valid) items[v * L::VEC + e] = ld_stream1(p + e);
+    }
+  }
+}
+
+// Striped BlockLoad: item k of thread t = tile[t + k*BT] (tile.hpp:3-8 ownership).
+template <int IPT>
+__device__ __forceinline__ void BlockLoadStriped(const int32_t* __restrict__ tile, int bt,
+                                                 int valid, int32_t (&items)[IPT]) {
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    const int s = threadIdx.x + k * bt;
+    if (s < valid) items[k] = ld_stream1(tile + s);
+  }
+}
+
+// BlockPred / BlockPredAnd (block_ops.hpp:54-69).  Every PredicateSpec op
+// (tile.hpp:122-132) is lowered on the host to an inclusive range [lo, hi]
+// (lo > hi encodes "never"), so the device evaluates one form.
+template <int IPT>
+__device__ __forceinline__ unsigned BlockPred(const int32_t (&items)[IPT], int32_t lo, int32_t hi,
+                                              unsigned valid_mask) {
+  unsigned f = 0;
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) f |= (unsigned)(items[k] >= lo && items[k] <= hi) << k;
+  return f & valid_mask;
+}
+
+template <int IPT>
+__device__ __forceinline__ unsigned BlockPredAnd(const int32_t (&items)[IPT], int32_t lo,
+                                                 int32_t hi, unsigned flags) {
+  unsigned f = 0;
+#pragma unroll
+  for (int k = 0; k < IPT; ++k)
+    if ((flags >> k) & 1u) f |= (unsigned)(items[k] >= lo && items[k] <= hi) << k;
+  return f;
+}
+
+// BlockScan (block_ops.hpp:73-82): exclusive prefix over the CTA's threads in
+// thread order, plus the block total.  T is an integer type; `smem` holds
+// BT/32 values.  Ends with a barrier so smem can be reused.
+template <int BT, class T>
+__device__ __forceinline__ T BlockScan(T v, T* smem, T& total) {
+  constexpr int W = BT / 32;
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  T x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= (unsigned)o) x += y;
+  }
+  if constexpr (W == 1) {
+    total = __shfl_sync(0xffffffffu, x, 31);
+    return x - v;
+  } else {
+    if (lane == 31) smem[warp] = x;
+    __syncthreads();
+    T w = lane < W ? smem[lane] : T(0);
+    if (warp == 0) {
+      T s = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        T y = __shfl_up_sync(0xffffffffu, s, o);
+        if (lane >= (unsigned)o) s += y;
+      }
+      if (lane < W) smem[lane] = s - w;  // exclusive warp offsets
+      if (lane == W - 1) smem[W] = s;
+    }
+    __syncthreads();
+    T off = smem[warp];
+    total = smem[W];
+    __syncthreads();
+    return off + x - v;
+  }
+}
+
+// BlockAggregate SUM (block_ops.hpp:141-173): flagged items summed in 8 bytes.
+template <int IPT>
+__device__ __forceinline__ long long BlockAggregateSum(const int32_t (&items)[IPT], unsigned flags) {
+  long long s = 0;
+#pragma unroll
+  for (int k = 0; k < IPT; ++k)
+    if ((flags >> k) & 1u) s += items[k];
+  return s;
+}
+
+// BlockProbeHashTable = block_lookup (hash_table.hpp:68-87) over interleaved
+// {key,payload} slots.  `flags` is both the probe mask (in) and the found
+// bitmap (out); payloads[k] is set for hits.  All first-slot loads are issued
+// before any is consumed (IPT independent requests in flight per thread);
+// collisions then walk linearly (hash_table.hpp:41-51).
+template <int IPT>
+__device__ __forceinline__ void BlockProbeHashTable(const int32_t (&keys)[IPT], unsigned& flags,
+                                                    int32_t (&payloads)[IPT],
+                                                    const int2* __restrict__ slots, uint32_t mask,
+                                                    int shift) {
+  uint32_t s[IPT];
+  int2 e[IPT];
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    if ((flags >> k) & 1u) {
+      s[k] = ht_slot_of(keys[k], shift);
+      e[k] = __ldg(slots + s[k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    if ((flags >> k) & 1u) {
+      const int32_t key = keys[k];
+      int2 x = e[k];
+      uint32_t sl = s[k];
+      while (x.x != key && x.x != kEmptyKey) {
+        sl = (sl + 1) & mask;
+        x = __ldg(slots + sl);
+      }
+      // INT32_MIN is unstorable and aliases empty slots: always a miss.
+      if (x.x == key && key != kEmptyKey)
+        payloads[k] = x.y;
+      else
+        flags &= ~(1u << k);
+    }
+  }
+}
+
+// Same probe against a table staged in shared memory.
+template <int IPT>
+__device__ __forceinline__ void BlockProbeHashTableSmem(const int32_t (&keys)[IPT],
+                                                        unsigned& flags, int32_t (&payloads)[IPT],
+                                                        const int2* slots, uint32_t mask,
+                                                        int shift) {
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    if ((flags >> k) & 1u) {
+      const int32_t key = keys[k];
+      uint32_t sl = ht_slot_of(key, shift);
+      int2 x = slots[sl];
+      while (x.x != key && x.x != kEmptyKey) {
+        sl = (sl + 1) & mask;
+        x = slots[sl];
+      }
+      if (x.x == key && key != kEmptyKey)
+        payloads[k] = x.y;
+      else
+        flags &= ~(1u << k);
+    }
+  }
+}
+
+// BlockBuildHashTable (hash_table.cpp:51-93, the CAS-parallel build): claim a
+// slot with ONE 64-bit compare-and-swap of {EMPTY,0} -> {key,payload}, so key
+// and payload publish together.  err: 1 = sentinel key, 2 = duplicate key.
+__device__ __forceinline__ void ht_insert(int2* slots, uint32_t mask, int shift, int32_t key,
+                                          int32_t payload, int32_t* err) {
+  if (key == kEmptyKey) {
+    atomicCAS(err, 0, 1);
+    return;
+  }
+  const unsigned long long empty = pack_slot(kEmptyKey, 0);
+  const unsigned long long want = pack_slot(key, payload);
+  uint32_t s = ht_slot_of(key, shift);
+  for (uint32_t step = 0; step <= mask; ++step, s = (s + 1) & mask) {
+    unsigned long long* p = reinterpret_cast<unsigned long long*>(slots + s);
+    unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(p);
+    if ((int32_t)(uint32_t)old == key) {
+      atomicCAS(err, 0, 2);
+      return;
+    }
+    if ((int32_t)(uint32_t)old != kEmptyKey) continue;
+    old = atomicCAS(p, empty, want);
+    if (old == empty) return;
+    if ((int32_t)(uint32_t)old == key) {
+      atomicCAS(err, 0, 2);
+      return;
+    }
+  }
+}
+
+template <int IPT>
+__device__ __forceinline__ void BlockBuildHashTable(const int32_t (&keys)[IPT],
+                                                    const int32_t (&payloads)[IPT], unsigned flags,
+                                                    int2* slots, uint32_t mask, int shift,
+                                                    int32_t* err) {
+#pragma unroll
+  for (int k = 0; k < IPT; ++k)
+    if ((flags >> k) & 1u) ht_insert(slots, mask, shift, keys[k], payloads[k], err);
+}
+
+// ----------------------------------------------------------------------
+// Decoupled look-back (single-pass chained scan) -- the B200 replacement for
+// GlobalCursor in deterministic mode (kernel.cpp:22-40): block-ordered output
+// offsets without a host-side sequencer.  One 64-bit status word per tile:
+// bits 63:62 = 0 invalid / 1 aggregate / 2 inclusive prefix, bits 61:0 value.
+// Called by warp 0 of the CTA; returns the tile's exclusive offset.
+__device__ __forceinline__ long long tile_lookback(unsigned long long* status, long long tile,
+                                                   long long aggregate) {
+  const unsigned lane = lane_id();
+  constexpr unsigned long long kAgg = 1ull << 62, kPre = 2ull << 62, kVal = (1ull << 62) - 1;
+  volatile unsigned long long* st = status;
+  if (tile == 0) {
+    if (lane == 0) st[0] = kPre | (unsigned long long)aggregate;
+    return 0;
+  }
+  if (lane == 0) st[tile] = kAgg | (unsigned long long)aggregate;
+  long long excl = 0;
+  long long look = tile - 1;
+  while (true) {
+    const long long idx = look - (long long)lane;
+    unsigned long long w = kPre;  // lanes before tile 0 act as an empty prefix
+    if (idx >= 0) {
+      do {
+        w = st[idx];
+      } while ((w >> 62) == 0);
+    } else {
+      w = kPre;
+    }
+    const unsigned pre = __ballot_sync(0xffffffffu, (w >> 62) == 2);
+    const long long val = (long long)(w & kVal);
+    if (pre) {
+      const int first = __ffs(pre) - 1;  // closest predecessor with a prefix
+      long long v = (int)lane <= first ? val : 0;
+      excl += warp_sum(v);
+      break;
+    }
+    excl += warp_sum(val);
+    look -= 32;
+  }
+  if (lane == 0) st[tile] = kPre | (unsigned long long)(excl + aggregate);
+  return excl;
+}
+
+}  // namespace crys

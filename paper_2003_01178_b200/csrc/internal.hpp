@@ -1,0 +1,196 @@
+// internal.hpp -- host-side runtime objects behind the C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace crys {
+
+// ------------------------------------------------------------ device memory
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  // Grow-only reservation (contents not preserved).
+  void reserve(size_t n) {
+    if (n <= bytes) return;
+    release();
+    CUDA_TRY(cudaMalloc(&p, n < 256 ? 256 : n));
+    bytes = n < 256 ? 256 : n;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct PinnedBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  void reserve(size_t n) {
+    if (n <= bytes) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    CUDA_TRY(cudaMallocHost(&p, n));
+    bytes = n;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+// ------------------------------------------------------------ SSB plans
+// Restatement of the reference's hand-built plans (ssb_plans.hpp:19-87,
+// ssb_plans.cpp:21-275): this is the contract each fused kernel implements.
+enum Dim { kSupplier = 0, kCustomer = 1, kPart = 2, kDate = 3 };
+enum AggKind { kAggRevenue = 0, kAggExtPriceTimesDiscount = 1, kAggRevenueMinusSupplyCost = 2 };
+
+struct RangeFilter {  // DimFilter (ssb_plans.hpp:39-48): union of inclusive ranges
+  std::string column;
+  std::vector<std::pair<int32_t, int32_t>> ranges;
+};
+
+struct FactFilter {  // FactFilter (ssb_plans.hpp:31-34), op lowered to [lo, hi]
+  std::string column;
+  int32_t lo, hi;
+};
+
+struct DimJoin {  // DimJoin (ssb_plans.hpp:50-56)
+  Dim dim;
+  std::string dim_table, dim_key, fact_key;
+  std::vector<RangeFilter> filters;
+  std::string payload;  // empty: no payload (0)
+};
+
+struct GroupPart {  // GroupPart (ssb_plans.hpp:60-67)
+  int join_index;
+  int32_t lo, hi;
+  std::string label;
+};
+
+struct QueryPlan {  // QueryPlan (ssb_plans.hpp:78-85)
+  int qid;
+  std::string name;
+  std::vector<FactFilter> fact_filters;
+  std::vector<DimJoin> joins;
+  std::vector<GroupPart> group;
+  AggKind agg;
+  int64_t cells() const {
+    int64_t c = 1;
+    for (auto& g : group) c *= (int64_t)(g.hi - g.lo + 1);
+    return c;
+  }
+};
+
+const QueryPlan& plan_for(int qid);  // ConfigError for an unknown id
+int dict_code(const std::string& dict, const std::string& value);
+
+// Lowers PredicateSpec (tile.hpp:92-133) to an inclusive range.
+void lower_pred(const crys_pred& p, int32_t* lo, int32_t* hi);
+
+// ------------------------------------------------------------ runtime
+struct QueryWorkspace;
+struct SortWorkspace;
+// Workspaces are complete only in their own .cu file.
+struct WsDeleter {
+  void operator()(QueryWorkspace* p) const;
+  void operator()(SortWorkspace* p) const;
+};
+
+}  // namespace crys
+
+struct crys_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;
+  bool timing = false;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  double kernel_ms = 0, total_ms = 0;
+  // generic scratch
+  crys::DevBuf scratch, scratch2, status;
+  crys::PinnedBuf pinned;
+  std::unique_ptr<crys::QueryWorkspace, crys::WsDeleter> qws;
+  std::unique_ptr<crys::SortWorkspace, crys::WsDeleter> sws;
+  crys_db* staging = nullptr;  // device copies for crys_run_query_host
+  ~crys_ctx();
+};
+
+struct crys_db {
+  crys_ctx* ctx = nullptr;
+  int64_t sf = 0;
+  uint64_t seed = 0;
+  int64_t lo_begin = 0, lo_end = 0;  // shard of the full lineorder
+  struct Col {
+    std::unique_ptr<crys::DevBuf> buf;
+    int64_t rows = 0;
+  };
+  std::map<std::string, Col> cols;  // "table.column"
+  const int32_t* col(const std::string& table, const std::string& column, int64_t* rows) const;
+  int64_t table_rows(const std::string& table) const;
+};
+
+struct crys_ht {
+  crys_ctx* ctx = nullptr;
+  crys::DevBuf slots;  // int2[capacity]
+  int64_t capacity = 0;
+  int32_t shift = 0;
+  int64_t size = 0;
+};
+
+namespace crys {
+
+// Launch accounting + event timing helpers.
+inline void count_launch(crys_ctx* c, int n = 1) { c->launches += n; }
+void timing_begin(crys_ctx* c);
+void timing_kernel_begin(crys_ctx* c);
+void timing_kernel_end(crys_ctx* c);
+void timing_end(crys_ctx* c);  // synchronises and fills kernel_ms/total_ms when enabled
+
+// Entry points implemented in the .cu files.
+void ssb_generate(crys_ctx* ctx, crys_db* db);
+void ssb_query_partial(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt,
+                       unsigned long long* d_agg, unsigned long long* d_surv, int32_t* d_err);
+struct ResultRows {
+  std::vector<int64_t> cell;
+  std::vector<int64_t> sum;
+  int64_t survivors[4] = {0, 0, 0, 0};
+  int32_t err = 0;
+};
+void ssb_run_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt, ResultRows* out);
+void ssb_finalize_device(crys_ctx* ctx, int qid, const unsigned long long* d_agg,
+                         ResultRows* out);
+void emit_rows(int qid, const std::vector<int64_t>& cell, const std::vector<int64_t>& sums,
+               int32_t* h_groups, int64_t* h_sums, int64_t max_rows, int64_t* nrows);
+
+int64_t select_i32(crys_ctx* ctx, const int32_t* d_in, int64_t n, int32_t lo, int32_t hi,
+                   int32_t* d_out, int order, int bt, int ipt);
+void project_f32(crys_ctx* ctx, const float* x1, const float* x2, int64_t n, float a, float b,
+                 float* out, int sigmoid);
+void ht_build(crys_ctx* ctx, crys_ht* ht, const int32_t* d_keys, const int32_t* d_payloads,
+              int64_t n);
+int64_t join_probe_sum(crys_ctx* ctx, const int32_t* d_keys, const int32_t* d_payloads, int64_t n,
+                       const crys_ht* ht);
+void sort_pairs(crys_ctx* ctx, int32_t* d_keys, int32_t* d_payloads, int64_t n, int algo,
+                int bits_per_pass);
+
+}  // namespace crys

@@ -1,0 +1,296 @@
+"""GPU parity of the operator microbenchmark kernels (pytest -m gpu):
+select (input order + exact Crystal order), project, hash build/probe, LSB/MSB
+radix sort -- against the oracle and the reference's golden vectors."""
+import numpy as np
+import pytest
+
+from helpers import col_digest, golden
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    from oracle.oracle import Oracle
+    from paper_2003_01178_b200 import tq
+    return torch, tq, Oracle()
+
+
+def _cuda(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+# ------------------------------------------------------------------ select
+
+def test_figure5(env):
+    torch, tq, _ = env
+    g = golden("ops")["figure5"]
+    x = _cuda(torch, np.array(g["input"], np.int32))
+    out = torch.empty_like(x)
+    n = tq.select_tile_into(x, tq.PredicateSpec.gt(5), out, tq.TileConfig(4, 4))
+    assert out[:n].cpu().tolist() == g["crystal_order"]
+    n = tq.select_branching_into(x, tq.PredicateSpec.gt(5), out)
+    assert out[:n].cpu().tolist() == g["input_order"]
+
+
+def test_select_golden_all_shapes(env):
+    torch, tq, orc = env
+    for rec in golden("ops")["select"]:
+        xh = orc.random_i32(rec["n"], 42, 1, 0, (1 << 20) - 1)
+        x = _cuda(torch, xh)
+        out = torch.empty_like(x)
+        pred = tq.PredicateSpec.lt(rec["lt"])
+        n = tq.select_branching_into(x, pred, out)
+        assert n == rec["count"]
+        assert col_digest(out[:n].cpu().numpy()) == rec["input_order"]
+        for key, dig in rec.items():
+            if key.startswith("crystal_"):
+                bt, ipt = map(int, key[len("crystal_"):].split("x"))
+                n2 = tq.select_tile_into(x, pred, out, tq.TileConfig(bt, ipt))
+                assert n2 == n
+                assert col_digest(out[:n2].cpu().numpy()) == dig, key
+
+
+@pytest.mark.parametrize("n", [0, 1, 3, 4095, 4096, 4097, 100_000, 1 << 22])
+@pytest.mark.parametrize("op", ["lt", "le", "gt", "ge", "eq", "between"])
+def test_select_edges_vs_oracle(env, n, op):
+    torch, tq, orc = env
+    xh = orc.random_i32(n, 7, 11, -50, 50) if n else np.zeros(0, np.int32)
+    x = _cuda(torch, xh) if n else torch.zeros(0, dtype=torch.int32, device="cuda")
+    out = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    pred = tq.PredicateSpec.between(-10, 20) if op == "between" else getattr(tq.PredicateSpec, op)(3)
+    lo, hi = (pred.lo, pred.hi)
+    k = tq.select_branching_into(x, pred, out)
+    exp = orc.select(xh, op, lo, hi) if n else np.zeros(0, np.int32)
+    assert k == len(exp) and np.array_equal(out[:k].cpu().numpy(), exp)
+    for bt, ipt in ((128, 4), (3, 5), (1024, 8)):
+        k = tq.select_tile_into(x, pred, out, tq.TileConfig(bt, ipt))
+        exp = orc.select(xh, op, lo, hi, order="crystal", bt=bt, ipt=ipt) if n else np.zeros(0, np.int32)
+        assert k == len(exp) and np.array_equal(out[:k].cpu().numpy(), exp)
+
+
+def test_select_extreme_predicates(env):
+    torch, tq, orc = env
+    xh = orc.random_i32(10_000, 1, 2, -(2 ** 31), 2 ** 31 - 1)
+    x = _cuda(torch, xh)
+    out = torch.empty_like(x)
+    assert tq.select_branching_into(x, tq.PredicateSpec.lt(-(2 ** 31)), out) == 0
+    assert tq.select_branching_into(x, tq.PredicateSpec.gt(2 ** 31 - 1), out) == 0
+    assert tq.select_branching_into(x, tq.PredicateSpec.ge(-(2 ** 31)), out) == 10_000
+    assert np.array_equal(out.cpu().numpy(), xh)
+
+
+def test_select_host_span(env):
+    _, tq, orc = env
+    xh = orc.random_i32(50_000, 3, 4, 0, 1000)
+    out = np.empty_like(xh)
+    n = tq.select_branching_into(xh, tq.PredicateSpec.lt(250), out)
+    assert np.array_equal(out[:n], orc.select(xh, "lt", 250))
+
+
+@pytest.mark.slow
+def test_select_2e29_counts(env):
+    torch, tq, orc = env
+    n = 1 << 29
+    x = _cuda(torch, orc.random_i32(n, 42, 1, 0, (1 << 20) - 1))
+    out = torch.empty_like(x)
+    for s, cnt in golden("ops")["select_2e29_counts"].items():
+        lo = int(round(float(s) * (1 << 20)))
+        assert tq.select_branching_into(x, tq.PredicateSpec.lt(lo), out) == cnt
+    # sortedness-free property: output is exactly the input filtered, in order
+    lo = 1 << 19
+    k = tq.select_branching_into(x, tq.PredicateSpec.lt(lo), out)
+    xs = x[x < lo]
+    assert k == xs.numel() and torch.equal(out[:k], xs)
+
+
+# ------------------------------------------------------------------ project
+
+def test_project_golden(env):
+    torch, tq, orc = env
+    g = golden("ops")["project"]
+    x1, x2 = orc.project_inputs(g["n"], 42)
+    d1, d2 = _cuda(torch, x1), _cuda(torch, x2)
+    out = torch.empty_like(d1)
+    tq.project_linear_into(d1, d2, g["a"], g["b"], out)
+    assert col_digest(out.cpu().numpy().view(np.int32)) == g["linear"]
+    tq.project_sigmoid_into(d1, d2, g["a"], g["b"], out)
+    got = out.cpu().numpy()
+    exp = orc.project(x1, x2, g["a"], g["b"], sigmoid=True)
+    # sigmoid: CUDA's double exp vs glibc's may differ in the last double bit,
+    # which survives rounding to float only ~2^-29 of the time; tolerance = 0
+    # mismatching elements at this size, |diff| <= 1 float ulp if any ever do.
+    mism = np.count_nonzero(got.view(np.int32) != exp.view(np.int32))
+    assert mism == 0
+    if mism == 0:
+        assert col_digest(got.view(np.int32)) == g["sigmoid"]
+
+
+@pytest.mark.parametrize("n", [0, 1, 5, 1023, 1 << 20])
+def test_project_linear_bit_exact(env, n):
+    torch, tq, orc = env
+    x1, x2 = orc.project_inputs(n, 9)
+    d1, d2 = _cuda(torch, x1), _cuda(torch, x2)
+    out = torch.empty_like(d1)
+    tq.project_linear_into(d1, d2, 0.75, -1.25, out)
+    assert np.array_equal(out.cpu().numpy().view(np.int32),
+                          orc.project(x1, x2, 0.75, -1.25).view(np.int32))
+
+
+# ------------------------------------------------------------------ join
+
+def test_join_golden_sweep(env):
+    torch, tq, orc = env
+    P = 1 << 20
+    pp = _cuda(torch, orc.random_i32(P, 42, 3, 0, 999))
+    for rec in golden("ops")["join_p2e20"]:
+        cap = rec["ht_bytes"] // 8
+        bn = rec["build"]
+        bk = torch.arange(1, bn + 1, dtype=torch.int32, device="cuda")
+        bp = _cuda(torch, orc.random_i32(bn, 42, 4, 0, 999))
+        pk = _cuda(torch, orc.random_i32(P, 42, 5, 1, bn))
+        ht = tq.HashTable.build(bk, bp, cap)
+        assert ht.capacity() == cap
+        assert tq.join_probe_tile(pk, pp, ht) == rec["checksum"], rec["ht_bytes"]
+        ht.free()
+
+
+def test_hash_table_layout_is_a_valid_linear_probe_table(env):
+    torch, tq, orc = env
+    bn, cap = 5000, 16384
+    bk = orc.random_i32(bn, 5, 6, -(2 ** 30), 2 ** 30)
+    bk = np.unique(bk).astype(np.int32)
+    bp = orc.random_i32(len(bk), 5, 7, 0, 999)
+    ht = tq.HashTable.build(_cuda(torch, bk), _cuda(torch, bp), cap)
+    sk, sp = ht.slots()
+    empty = -(2 ** 31)
+    assert np.count_nonzero(sk != empty) == len(bk)
+    got = dict(zip(sk[sk != empty].tolist(), sp[sk != empty].tolist()))
+    assert got == dict(zip(bk.tolist(), bp.tolist()))
+    # every key is reachable from its home slot without crossing an empty slot
+    shift = 32 - int(np.log2(cap))
+    for k in bk[:500].tolist():
+        s = ((k & 0xFFFFFFFF) * 2654435769 & 0xFFFFFFFF) >> shift
+        while sk[s] != k:
+            assert sk[s] != empty
+            s = (s + 1) & (cap - 1)
+
+
+def test_join_vs_oracle_misses_and_extremes(env):
+    torch, tq, orc = env
+    bk = np.array([1, 7, -5, 2 ** 31 - 1, -(2 ** 31) + 1, 123456], np.int32)
+    bp = np.array([10, 20, 30, 40, 50, 60], np.int32)
+    pk = np.array([1, 2, 7, -5, 2 ** 31 - 1, -(2 ** 31), 0, -(2 ** 31) + 1, 99], np.int32)
+    pp = np.arange(len(pk), dtype=np.int32)
+    ht = tq.HashTable.build(_cuda(torch, bk), _cuda(torch, bp), 16)
+    rc, sk, sp = orc.ht_build(bk, bp, 16)
+    assert tq.join_probe_tile(_cuda(torch, pk), _cuda(torch, pp), ht) == orc.join_checksum(pk, pp, sk, sp)
+
+
+def test_hash_build_errors(env):
+    torch, tq, _ = env
+    k = _cuda(torch, np.array([1, 2, 3], np.int32))
+    with pytest.raises(tq.ConfigError):
+        tq.HashTable.build(k, k, 6)
+    with pytest.raises(tq.BuildError):
+        tq.HashTable.build(k, k, 4)
+    d = _cuda(torch, np.array([5, 5], np.int32))
+    with pytest.raises(tq.BuildError):
+        tq.HashTable.build(d, d, 8)
+    s = _cuda(torch, np.array([-(2 ** 31)], np.int32))
+    with pytest.raises(tq.BuildError):
+        tq.HashTable.build(s, s, 4)
+
+
+@pytest.mark.slow
+def test_join_golden_p2e28(env):
+    torch, tq, orc = env
+    P = 1 << 28
+    pp = _cuda(torch, orc.random_i32(P, 42, 3, 0, 999))
+    for rec in golden("ops")["join_p2e28"]:
+        if rec["ht_bytes"] not in (8192, 1 << 20, 1 << 26, 1 << 30):
+            continue
+        cap = rec["ht_bytes"] // 8
+        bn = rec["build"]
+        bk = torch.arange(1, bn + 1, dtype=torch.int32, device="cuda")
+        bp = _cuda(torch, orc.random_i32(bn, 42, 4, 0, 999))
+        pk = _cuda(torch, orc.random_i32(P, 42, 5, 1, bn))
+        ht = tq.HashTable.build(bk, bp, cap)
+        assert tq.join_probe_tile(pk, pp, ht) == rec["checksum"], rec["ht_bytes"]
+        ht.free()
+        del pk, bk, bp
+
+
+# ------------------------------------------------------------------ sort
+
+def test_radix_worked_example(env):
+    torch, tq, _ = env
+    g = golden("ops")["radix_example"]
+    k = _cuda(torch, np.array(g["keys"], np.int32))
+    p = _cuda(torch, np.array(g["payloads"], np.int32))
+    tq.lsb_radix_sort(k, p, bits_per_pass=2)
+    assert k.cpu().tolist() == g["sorted_keys"] and p.cpu().tolist() == g["sorted_payloads"]
+
+
+def test_lsb_golden(env):
+    torch, tq, orc = env
+    for rec in golden("ops")["lsb"]:
+        kh = orc.random_i32(rec["n"], 42, 6, -(2 ** 31) // 2, (2 ** 31 - 1) // 2)
+        k = _cuda(torch, kh)
+        p = torch.arange(rec["n"], dtype=torch.int32, device="cuda")
+        tq.lsb_radix_sort(k, p, bits_per_pass=rec["bits"])
+        assert col_digest(k.cpu().numpy()) == rec["keys"]
+        assert col_digest(p.cpu().numpy()) == rec["payloads"]
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 3, 255, 256, 257, 8191, 8192, 8193, 100_000, 1 << 21])
+@pytest.mark.parametrize("dist", ["uniform", "narrow", "constant", "sorted", "reversed", "full"])
+def test_sorts_vs_stable_sort(env, n, dist):
+    torch, tq, orc = env
+    if dist == "uniform":
+        kh = orc.random_i32(n, 1, 2, -(2 ** 31) // 2, (2 ** 31 - 1) // 2)
+    elif dist == "narrow":
+        kh = orc.random_i32(n, 1, 3, 0, 5)
+    elif dist == "constant":
+        kh = np.full(n, -7, np.int32)
+    elif dist == "sorted":
+        kh = np.sort(orc.random_i32(n, 1, 4, -1000, 1000))
+    elif dist == "reversed":
+        kh = np.sort(orc.random_i32(n, 1, 5, -1000, 1000))[::-1].copy()
+    else:
+        kh = orc.random_i32(n, 1, 6, -(2 ** 31), 2 ** 31 - 1)
+    ph = np.arange(n, dtype=np.int32)
+    order = np.argsort(kh, kind="stable")
+    for bits in (8, 3):
+        k, p = _cuda(torch, kh.copy()), _cuda(torch, ph.copy())
+        tq.lsb_radix_sort(k, p, bits_per_pass=bits)
+        assert np.array_equal(k.cpu().numpy(), kh[order]), bits
+        assert np.array_equal(p.cpu().numpy(), ph[order]), bits
+    k, p = _cuda(torch, kh.copy()), _cuda(torch, ph.copy())
+    tq.msb_radix_sort(k, p)
+    km, pm = k.cpu().numpy(), p.cpu().numpy()
+    assert np.array_equal(km, kh[order])
+    # pairing preserved: each payload still carries its own key
+    assert np.array_equal(np.sort(pm), ph) and np.array_equal(kh[pm], km)
+
+
+@pytest.mark.slow
+def test_sorts_2e28(env):
+    torch, tq, orc = env
+    from oracle.oracle import sort_digest
+    g = golden("ops")["lsb_2e28"]
+    n = g["n"]
+    kh = orc.random_i32(n, 42, 6, -(2 ** 31) // 2, (2 ** 31 - 1) // 2)
+    k = _cuda(torch, kh)
+    p = torch.arange(n, dtype=torch.int32, device="cuda")
+    tq.lsb_radix_sort(k, p)
+    kc, pc = k.cpu().numpy(), p.cpu().numpy()
+    assert sort_digest(kc, pc) == g["digest"]
+    k = _cuda(torch, kh)
+    p = torch.arange(n, dtype=torch.int32, device="cuda")
+    tq.msb_radix_sort(k, p)
+    km, pm = k.cpu().numpy(), p.cpu().numpy()
+    assert np.array_equal(km, kc)
+    assert np.array_equal(kh[pm], km)
+    assert np.array_equal(np.bincount(pm, minlength=n), np.ones(n, np.int64))

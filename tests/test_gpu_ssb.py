@@ -1,0 +1,145 @@
+"""GPU parity of the fused SSB path through the C ABI (pytest -m gpu).
+
+Golden vectors: tests/golden/{fixture,sf1,sf20,sf100}.json, produced by the
+reference's own run_reference/run_query (make_golden.py).  The oracle
+(oracle/oracle.c) is the second checker at sizes it finishes in seconds."""
+import numpy as np
+import pytest
+
+from helpers import QUERY_NAMES, col_digest, fixture_tables, golden, golden_rows
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tq():
+    from paper_2003_01178_b200 import tq as _tq
+    return _tq
+
+
+@pytest.fixture(scope="module")
+def sf1(tq):
+    db = tq.DeviceDatabase.generate(1, 42)
+    yield db
+    db.free()
+
+
+def test_gpu_generator_bit_exact_sf1(tq, sf1):
+    cols = golden("sf1")["columns"]
+    for key, g in cols.items():
+        t, c = key.split(".")
+        a = sf1.download(t, c)
+        assert len(a) == g["rows"], key
+        assert col_digest(a) == g["digest"], key
+
+
+@pytest.mark.parametrize("q", range(13))
+def test_ssb_sf1_matches_reference(tq, sf1, q):
+    rec = golden("sf1")["queries"][QUERY_NAMES[q]]
+    stats = tq.QueryStats()
+    res = tq.run_query(sf1, q, tq.TileConfig(), 1, stats)
+    assert res.as_tuples() == golden_rows(rec)
+    assert stats.survivors == rec["survivors"]
+
+
+@pytest.mark.parametrize("q", range(13))
+def test_ssb_fixture_matches_reference(tq, q):
+    rec = golden("fixture")["queries"][QUERY_NAMES[q]]
+    db = tq.DeviceDatabase.from_host(fixture_tables())
+    stats = tq.QueryStats()
+    res = tq.run_query(db, q, tq.TileConfig(), 1, stats)
+    assert res.as_tuples() == golden_rows(rec)
+    assert stats.survivors == rec["survivors"]
+    db.free()
+
+
+def test_fixture_q41_every_tile_shape(tq):
+    # test_ssb.cpp:184-208: the same answer under every decomposition
+    rec = golden("fixture")["queries"]["q41"]
+    db = tq.DeviceDatabase.from_host(fixture_tables())
+    for cfg in (tq.TileConfig(2, 2), tq.TileConfig(3, 1), tq.TileConfig(128, 4), tq.TileConfig(256, 8),
+                tq.TileConfig(256, 16), tq.TileConfig(128, 16), tq.TileConfig(512, 8)):
+        for workers in (1, 2, 4):
+            assert tq.run_query(db, 10, cfg, workers).as_tuples() == golden_rows(rec)
+    db.free()
+
+
+def test_run_query_rejects_bad_parameters(tq):
+    # test_ssb.cpp:229-233
+    db = tq.DeviceDatabase.from_host(fixture_tables())
+    with pytest.raises(tq.ConfigError):
+        tq.run_query(db, 0, tq.TileConfig(), 0)
+    with pytest.raises(tq.ConfigError):
+        tq.run_query(db, 0, tq.TileConfig(0, 4))
+    with pytest.raises(tq.ConfigError):
+        tq.run_query(db, 42)
+    db.free()
+
+
+def test_host_database_end_to_end(tq):
+    """run_query over HOST columns (copies H2D inside the call)."""
+    from oracle.oracle import Oracle
+    host = Oracle().generate(1, 42)
+    for q in (0, 4, 9, 12):
+        rec = golden("sf1")["queries"][QUERY_NAMES[q]]
+        stats = tq.QueryStats()
+        assert tq.run_query(host, q, tq.TileConfig(), 1, stats).as_tuples() == golden_rows(rec)
+        assert stats.survivors == rec["survivors"]
+
+
+@pytest.mark.parametrize("cfg", [(128, 4), (256, 8), (256, 16), (128, 16), (512, 8), (32, 1)])
+def test_ssb_sf1_tile_invariance(tq, sf1, cfg):
+    # test_ssb.cpp:251-261
+    for q in (0, 3, 9, 12):
+        rec = golden("sf1")["queries"][QUERY_NAMES[q]]
+        assert tq.run_query(sf1, q, tq.TileConfig(*cfg)).as_tuples() == golden_rows(rec)
+
+
+def test_ssb_sf1_vs_oracle_on_shard(tq):
+    """A lineorder shard on the device == the oracle over the same rows."""
+    from oracle.oracle import Oracle
+    from paper_2003_01178_b200 import dist as cdist
+    import torch
+    orc = Oracle()
+    lo, hi = 1_000_003, 4_500_017
+    host = orc.generate(1, 42, lo_begin=lo, lo_end=hi)
+    db = tq.DeviceDatabase.generate(1, 42, lo, hi)
+    for c in ("lo_orderdate", "lo_revenue", "lo_partkey"):
+        assert np.array_equal(db.download("lineorder", c), host["lineorder"][c])
+    sh = cdist.ShardedSSB.__new__(cdist.ShardedSSB)
+    sh.ctx, sh.db, sh.device, sh._bufs, sh.world = db.ctx, db, torch.cuda.current_device(), {}, 1
+    for q in range(13):
+        s, c, v = orc.partial(host, q, 0, hi - lo)
+        buf = sh.partial(q)
+        torch.cuda.synchronize()
+        got = buf.cpu().numpy()
+        cells = len(s)
+        assert np.array_equal(got[:cells], s), QUERY_NAMES[q]
+        assert np.array_equal(got[cells:2 * cells], c), QUERY_NAMES[q]
+        res = cdist.reduce_local(buf, q, db.ctx)
+        assert res.as_tuples() == orc.query(host, q)[0], QUERY_NAMES[q]
+    db.free()
+
+
+@pytest.fixture(scope="module")
+def sf20(tq):
+    db = tq.DeviceDatabase.generate(20, 42)
+    yield db
+    db.free()
+
+
+@pytest.mark.parametrize("q", range(13))
+def test_ssb_sf20_matches_reference(tq, sf20, q):
+    rec = golden("sf20")["queries"][QUERY_NAMES[q]]
+    stats = tq.QueryStats()
+    res = tq.run_query(sf20, q, tq.TileConfig(), 1, stats)
+    assert res.as_tuples() == golden_rows(rec)
+    assert stats.survivors == rec["survivors"]
+
+
+def test_gpu_generator_bit_exact_sf20(tq, sf20):
+    cols = golden("sf20")["columns"]
+    for key in ("lineorder.lo_orderdate", "lineorder.lo_supplycost", "part.p_brand1",
+                "customer.c_city", "supplier.s_city"):
+        t, c = key.split(".")
+        assert col_digest(sf20.download(t, c)) == cols[key]["digest"], key
