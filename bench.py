@@ -377,7 +377,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--sf", type=int, default=0)
     ap.add_argument("--bt", type=int, default=256)
-    ap.add_argument("--ipt", type=int, default=16)
+    ap.add_argument("--ipt", type=int, default=8)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -7,6 +7,8 @@
 
 #include <algorithm>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -55,6 +57,30 @@ const int32_t* crys_db::col(const std::string& table, const std::string& column,
   return it->second.buf->as<int32_t>();
 }
 
+bool crys_db::col_range(const std::string& table, const std::string& column, int32_t* lo,
+                        int32_t* hi) const {
+  auto it = cols.find(table + "." + column);
+  if (it == cols.end() || !it->second.stats) return false;
+  *lo = it->second.vmin;
+  *hi = it->second.vmax;
+  return true;
+}
+
+// Dimension columns get value-range statistics on upload (they are small;
+// lineorder columns are not scanned on the host).
+static void host_stats(crys_db::Col& c, const std::string& table, const int32_t* h, int64_t rows) {
+  c.stats = false;
+  if (table == "lineorder" || rows <= 0) return;
+  int32_t lo = h[0], hi = h[0];
+  for (int64_t i = 1; i < rows; ++i) {
+    lo = h[i] < lo ? h[i] : lo;
+    hi = h[i] > hi ? h[i] : hi;
+  }
+  c.stats = true;
+  c.vmin = lo;
+  c.vmax = hi;
+}
+
 int64_t crys_db::table_rows(const std::string& table) const {
   for (auto& kv : cols)
     if (kv.first.compare(0, table.size() + 1, table + ".") == 0) return kv.second.rows;
@@ -62,6 +88,17 @@ int64_t crys_db::table_rows(const std::string& table) const {
 }
 
 namespace crys {
+
+void ensure_dyn_smem(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::map<const void*, size_t> set_to;
+  if (bytes <= 48 * 1024) return;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& cur = set_to[fn];
+  if (bytes <= cur) return;
+  CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  cur = bytes;
+}
 
 void timing_begin(crys_ctx* c) {
   if (c->timing) CUDA_TRY(cudaEventRecord(c->ev[0], c->stream));
@@ -225,6 +262,7 @@ crys_status crys_db_upload_column(crys_db* db, const char* table, const char* co
     if (!c.buf) c.buf.reset(new crys::DevBuf());
     c.buf->reserve(sizeof(int32_t) * (size_t)std::max<int64_t>(rows, 1));
     c.rows = rows;
+    host_stats(c, table, h_data, rows);
     if (rows)
       CUDA_TRY(cudaMemcpyAsync(c.buf->p, h_data, sizeof(int32_t) * (size_t)rows,
                                cudaMemcpyHostToDevice, db->ctx->stream));
@@ -340,6 +378,7 @@ crys_status crys_run_query_host(crys_ctx* ctx, const crys_host_column* cols, int
       if (!c.buf) c.buf.reset(new crys::DevBuf());
       c.buf->reserve(sizeof(int32_t) * (size_t)std::max<int64_t>(hc->rows, 1));
       c.rows = hc->rows;
+      host_stats(c, tc.first, hc->h_data, hc->rows);
       if (hc->rows)
         CUDA_TRY(cudaMemcpyAsync(c.buf->p, hc->h_data, sizeof(int32_t) * (size_t)hc->rows,
                                  cudaMemcpyHostToDevice, ctx->stream));

@@ -33,6 +33,14 @@ struct Error : std::runtime_error {
       ::crys::fail(CRYS_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
   } while (0)
 
+// Checks the launch that was just enqueued, naming it in the error.
+#define CRYS_LAUNCHED(name)                                                          \
+  do {                                                                               \
+    cudaError_t _e = cudaGetLastError();                                             \
+    if (_e != cudaSuccess)                                                           \
+      ::crys::fail(CRYS_ECUDA, std::string("launch ") + (name) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
 // ------------------------------------------------------------ constants
 // HashTable::kEmptyKey / kFibonacci (hash_table.hpp:23-24).
 constexpr int32_t kEmptyKey = INT32_MIN;

@@ -191,27 +191,22 @@ __device__ __forceinline__ long long BlockAggregateSum(const int32_t (&items)[IP
 // {key,payload} slots.  `flags` is both the probe mask (in) and the found
 // bitmap (out); payloads[k] is set for hits.  All first-slot loads are issued
 // before any is consumed (IPT independent requests in flight per thread);
-// collisions then walk linearly (hash_table.hpp:41-51).
+// collisions then walk linearly per item (hash_table.hpp:41-51).
 template <int IPT>
 __device__ __forceinline__ void BlockProbeHashTable(const int32_t (&keys)[IPT], unsigned& flags,
                                                     int32_t (&payloads)[IPT],
                                                     const int2* __restrict__ slots, uint32_t mask,
                                                     int shift) {
-  uint32_t s[IPT];
   int2 e[IPT];
 #pragma unroll
-  for (int k = 0; k < IPT; ++k) {
-    if ((flags >> k) & 1u) {
-      s[k] = ht_slot_of(keys[k], shift);
-      e[k] = __ldg(slots + s[k]);
-    }
-  }
+  for (int k = 0; k < IPT; ++k)
+    if ((flags >> k) & 1u) e[k] = __ldg(slots + ht_slot_of(keys[k], shift));
 #pragma unroll
   for (int k = 0; k < IPT; ++k) {
     if ((flags >> k) & 1u) {
       const int32_t key = keys[k];
       int2 x = e[k];
-      uint32_t sl = s[k];
+      uint32_t sl = ht_slot_of(key, shift);
       while (x.x != key && x.x != kEmptyKey) {
         sl = (sl + 1) & mask;
         x = __ldg(slots + sl);
@@ -231,20 +226,38 @@ __device__ __forceinline__ void BlockProbeHashTableSmem(const int32_t (&keys)[IP
                                                         unsigned& flags, int32_t (&payloads)[IPT],
                                                         const int2* slots, uint32_t mask,
                                                         int shift) {
+  uint32_t s[IPT];
+  int2 e[IPT];
+  unsigned pending = 0;
 #pragma unroll
   for (int k = 0; k < IPT; ++k) {
-    if ((flags >> k) & 1u) {
-      const int32_t key = keys[k];
-      uint32_t sl = ht_slot_of(key, shift);
-      int2 x = slots[sl];
-      while (x.x != key && x.x != kEmptyKey) {
-        sl = (sl + 1) & mask;
-        x = slots[sl];
+    if (((flags >> k) & 1u) && keys[k] != kEmptyKey) {
+      pending |= 1u << k;
+      s[k] = ht_slot_of(keys[k], shift);
+      e[k] = slots[s[k]];
+    }
+  }
+  flags = 0;
+  while (pending) {
+    unsigned next = 0;
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      if ((pending >> k) & 1u) {
+        if (e[k].x == keys[k]) {
+          payloads[k] = e[k].y;
+          flags |= 1u << k;
+        } else if (e[k].x != kEmptyKey) {
+          next |= 1u << k;
+        }
       }
-      if (x.x == key && key != kEmptyKey)
-        payloads[k] = x.y;
-      else
-        flags &= ~(1u << k);
+    }
+    pending = next;
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      if ((pending >> k) & 1u) {
+        s[k] = (s[k] + 1) & mask;
+        e[k] = slots[s[k]];
+      }
     }
   }
 }

@@ -26,11 +26,12 @@ struct DevBuf {
     bytes = 0;
   }
   // Grow-only reservation (contents not preserved).
+  // 256 B of slack past `n` lets bulk copies round a column tail up to 16 B.
   void reserve(size_t n) {
     if (n <= bytes) return;
     release();
-    CUDA_TRY(cudaMalloc(&p, n < 256 ? 256 : n));
-    bytes = n < 256 ? 256 : n;
+    CUDA_TRY(cudaMalloc(&p, n + 256));
+    bytes = n;
   }
   template <class T>
   T* as() const {
@@ -143,9 +144,15 @@ struct crys_db {
   struct Col {
     std::unique_ptr<crys::DevBuf> buf;
     int64_t rows = 0;
+    // value range (catalog statistics, kept for dimension columns): sizes the
+    // exact key-range membership bitmaps of the SSB dimension builds
+    bool stats = false;
+    int32_t vmin = 0, vmax = -1;
   };
   std::map<std::string, Col> cols;  // "table.column"
   const int32_t* col(const std::string& table, const std::string& column, int64_t* rows) const;
+  // false when the column carries no statistics
+  bool col_range(const std::string& table, const std::string& column, int32_t* lo, int32_t* hi) const;
   int64_t table_rows(const std::string& table) const;
 };
 
@@ -158,6 +165,11 @@ struct crys_ht {
 };
 
 namespace crys {
+
+// Raise (never lower) a kernel's dynamic shared-memory limit; the attribute
+// is per function, so one kernel shared by plans of different sizes must keep
+// the largest value it has ever been launched with.
+void ensure_dyn_smem(const void* fn, size_t bytes);
 
 // Launch accounting + event timing helpers.
 inline void count_launch(crys_ctx* c, int n = 1) { c->launches += n; }

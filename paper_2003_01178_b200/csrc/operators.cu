@@ -235,8 +235,7 @@ int occupancy(const void* fn, int bt, size_t smem) {
   auto key = std::make_pair(fn, smem);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
-  if (smem > 48 * 1024)
-    CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ensure_dyn_smem(fn, smem);
   int nb = 0;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, bt, smem));
   cache[key] = std::max(nb, 1);

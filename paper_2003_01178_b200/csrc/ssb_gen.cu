@@ -94,11 +94,15 @@ void date_columns(std::vector<int32_t> (&c)[5]) {
   }
 }
 
-int32_t* new_col(crys_db* db, const std::string& table, const std::string& col, int64_t rows) {
+int32_t* new_col(crys_db* db, const std::string& table, const std::string& col, int64_t rows,
+                 int32_t vmin = 0, int32_t vmax = -1) {
   auto& c = db->cols[table + "." + col];
   c.buf.reset(new DevBuf());
   c.buf->reserve(sizeof(int32_t) * (size_t)std::max<int64_t>(rows, 1));
   c.rows = rows;
+  c.stats = vmin <= vmax;  // value ranges are closed forms of the generator
+  c.vmin = vmin;
+  c.vmax = vmax;
   return c.buf->as<int32_t>();
 }
 
@@ -126,18 +130,19 @@ void ssb_generate(crys_ctx* ctx, crys_db* db) {
   static const char* kDateCols[5] = {"d_datekey", "d_year", "d_yearmonthnum", "d_yearmonth",
                                      "d_weeknuminyear"};
   for (int i = 0; i < 5; ++i) {
-    int32_t* d = new_col(db, "date", kDateCols[i], 2556);
+    int32_t* d = i == 0 ? new_col(db, "date", kDateCols[i], 2556, date[0].front(), date[0].back())
+                        : new_col(db, "date", kDateCols[i], 2556);
     CUDA_TRY(cudaMemcpyAsync(d, date[i].data(), sizeof(int32_t) * 2556, cudaMemcpyHostToDevice, st));
   }
-  int32_t* s[4] = {new_col(db, "supplier", "s_suppkey", supp), new_col(db, "supplier", "s_city", supp),
+  int32_t* s[4] = {new_col(db, "supplier", "s_suppkey", supp, 1, (int32_t)supp), new_col(db, "supplier", "s_city", supp),
                    new_col(db, "supplier", "s_nation", supp), new_col(db, "supplier", "s_region", supp)};
   gen_geo_kernel<<<grid_for(ctx, supp), 256, 0, st>>>(s[0], s[1], s[2], s[3], supp,
                                                        rng_base(seed, (uint64_t)sf, kTSupplier, 0));
-  int32_t* c[4] = {new_col(db, "customer", "c_custkey", cust), new_col(db, "customer", "c_city", cust),
+  int32_t* c[4] = {new_col(db, "customer", "c_custkey", cust, 1, (int32_t)cust), new_col(db, "customer", "c_city", cust),
                    new_col(db, "customer", "c_nation", cust), new_col(db, "customer", "c_region", cust)};
   gen_geo_kernel<<<grid_for(ctx, cust), 256, 0, st>>>(c[0], c[1], c[2], c[3], cust,
                                                        rng_base(seed, (uint64_t)sf, kTCustomer, 0));
-  int32_t* p[4] = {new_col(db, "part", "p_partkey", part), new_col(db, "part", "p_brand1", part),
+  int32_t* p[4] = {new_col(db, "part", "p_partkey", part, 1, (int32_t)part), new_col(db, "part", "p_brand1", part),
                    new_col(db, "part", "p_category", part), new_col(db, "part", "p_mfgr", part)};
   gen_part_kernel<<<grid_for(ctx, part), 256, 0, st>>>(p[0], p[1], p[2], p[3], part,
                                                         rng_base(seed, (uint64_t)sf, kTPart, 0));

@@ -1,0 +1,11 @@
+"""Run the given queries once for warm-up and once more (the profiled launch)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2003_01178_b200 import tq
+sf = int(os.environ.get("SF", "20"))
+bt, ipt = map(int, os.environ.get("TILE", "256x16").split("x"))
+db = tq.DeviceDatabase.generate(sf, 42)
+for q in map(int, sys.argv[1:]):
+    tq.run_query(db, q, tq.TileConfig(bt, ipt))
+    tq.run_query(db, q, tq.TileConfig(bt, ipt))
+print("done")
