@@ -1,0 +1,102 @@
+"""Summarise ncu output for profiles/ (run here, on the CPU box).
+
+  python tools/summarize_ncu.py launches gpurun_out/launches.csv   # per-kernel share of a launch list
+  python tools/summarize_ncu.py full gpurun_out/prof.ncu-rep        # key counters per profiled launch
+  python tools/summarize_ncu.py sass gpurun_out/prof.ncu-rep [k]    # opcode mix + stall reasons of launch k
+"""
+import csv
+import io
+import subprocess
+import sys
+from collections import Counter, defaultdict
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    h = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    hdr = rows[h]
+    ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    agg = defaultdict(lambda: [0, 0.0])
+    for r in rows[h + 1:]:
+        if len(r) <= vi:
+            continue
+        scale = {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "nsecond": 1e-3, "ms": 1e3}.get(r[ui], 1e-3)
+        name = r[ki].split("(")[0].replace("void ", "").replace("(anonymous namespace)::", "")
+        agg[name][0] += 1
+        agg[name][1] += float(r[vi].replace(",", "")) * scale
+    tot = sum(v[1] for v in agg.values())
+    print(f"{'launches':>8} {'total_us':>12} {'avg_us':>10} {'share':>7}  kernel")
+    for k, (n, us) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        print(f"{n:8d} {us:12.1f} {us / n:10.1f} {100 * us / tot:6.1f}%  {k}")
+    print(f"{'':8} {tot:12.1f} us total (ncu, cold-cache, serialised)")
+
+
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+        "lts__t_sector_hit_rate.pct", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+        "launch__grid_size", "launch__block_size", "launch__shared_mem_per_block_dynamic",
+        "smsp__inst_executed.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
+
+
+def raw(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    return rows[0], rows[1], rows[2:]
+
+
+def full(rep):
+    hdr, units, data = raw(rep)
+    for r in data:
+        print("----", r[hdr.index("Kernel Name")][:110])
+        for k in KEYS:
+            if k in hdr:
+                i = hdr.index(k)
+                print(f"  {k:60s} {r[i]:>18s} {units[i]}")
+
+
+def sass(rep, which=0):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True, check=True).stdout
+    kern, cur, hdr = [], None, None
+    for r in csv.reader(io.StringIO(out)):
+        if r and r[0] == "Kernel Name":
+            cur = [r[1], []]
+            kern.append(cur)
+        elif r and r[0] == "Address":
+            hdr = r
+        elif cur is not None and len(r) > 5:
+            cur[1].append(r)
+    name, ins = kern[which]
+    ie = hdr.index("Instructions Executed")
+    smp = hdr.index("Warp Stall Sampling (All Samples)")
+    tot = sum(int(x[ie]) for x in ins)
+    ts = sum(int(x[smp]) for x in ins) or 1
+    print(name[:120])
+    print(f"warp instructions executed {tot}, stall samples {ts}")
+    op = Counter()
+    for x in ins:
+        t = x[1].split()
+        o = t[1] if t[0].startswith("@") else t[0]
+        op[o.split(".")[0]] += int(x[ie])
+    for o, c in op.most_common(16):
+        print(f"  {o:10s} {c:12d} {100 * c / tot:5.1f}%")
+    print("stall reasons (share of samples):")
+    for col in hdr:
+        if col.startswith("stall_") and "(Not" not in col:
+            i = hdr.index(col)
+            s = sum(int(x[i]) for x in ins)
+            if s * 100 >= ts:
+                print(f"  {col:28s} {100 * s / ts:5.1f}%")
+
+
+if __name__ == "__main__":
+    mode, path = sys.argv[1], sys.argv[2]
+    if mode == "launches":
+        launches(path)
+    elif mode == "full":
+        full(path)
+    else:
+        sass(path, int(sys.argv[3]) if len(sys.argv) > 3 else 0)
