@@ -2,23 +2,28 @@
 //
 // Replaces run_query / run_flight1 / run_joins / build_dim_table /
 // AggregateTable / grouped_result of the reference (ssb_queries.cpp:15-286).
-// Per query:
-//   1. dimension builds (3 launches covering every join of the plan):
-//        dim_filter_kernel  filter + compact each dimension (build_dim_table,
-//                           ssb_queries.cpp:99-118), count on device
-//        dim_init_kernel    capacity = max(2, bit_ceil(2n)) decided on device
-//                           (ssb_queries.cpp:119), slots <- {EMPTY,0}
-//        dim_insert_kernel  BlockBuildHashTable, 64-bit CAS claims
-//   2. ONE fused pass over the lineorder shard (the hot loop, ssb_queries.cpp:
-//      181-201 / 233-263): vectorised column loads, chained predicates or up to
-//      four pipelined hash probes with selective loads of later columns, and the
-//      group-by folded into a shared-memory-privatised dense table (or global
-//      atomics when the domain is too large), no materialisation.
-//   3. finalize_kernel compacts occupied cells (occupancy, not sum != 0:
-//      ssb_queries.cpp:32-35) and one D2H copy returns them; the host orders
-//      rows by cell index = lexicographic group order (ssb_queries.cpp:153).
+// Per query, all on the context's stream with ONE host synchronisation:
+//   1. query_prologue_kernel  zeroes the dense aggregate, the counters, the
+//                             result header and every dimension table
+//   2. dim_filter_kernel      build_dim_table (ssb_queries.cpp:99-121) for all
+//                             joins at once (grid.y = join): filter the
+//                             dimension and insert the survivors into its
+//                             probe table (perfect hash over the dense key
+//                             range; linear-probing table otherwise, then
+//                             dim_init_kernel + dim_insert_kernel)
+//   3. the fused lineorder pass (the hot loop, ssb_queries.cpp:181-201 /
+//      233-263):  flight 1 -> ssb_flight1_kernel (register tiles, chained
+//      predicates, selective loads);  flights 2-4 -> ssb_pipeline_kernel
+//      (TMA/mbarrier ring, dense first probe, compacted sparse tail,
+//      ssb_pipeline.cuh)
+//   4. finalize_kernel        compacts occupied cells (occupancy, not
+//                             sum != 0: ssb_queries.cpp:32-35) + QueryStats +
+//                             error words into one buffer; one D2H copy
+//                             returns it and the host orders rows by cell
+//                             index = lexicographic group order (:153).
 #include <algorithm>
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -26,10 +31,17 @@
 
 #include "crystal.cuh"
 #include "internal.hpp"
+#include "ssb_pipeline.cuh"
 
 namespace crys {
 
 namespace {
+
+using pipe::ProbeTab;
+using pipe::kTabBitmap;
+using pipe::kTabU8;
+using pipe::kTabU16;
+using pipe::kTabHash;
 
 constexpr int kMaxJoins = 4;
 
@@ -40,14 +52,16 @@ struct DimBuildDesc {
   int32_t nranges[2];
   int32_t r[2][2][2];
   int32_t nf;
+  int32_t kind;            // pipe::TabKind of the probe table
   int64_t rows;
-  int64_t maxcap;
-  int2* compact;
-  int2* slots;
-  uint32_t* bitmap;  // exact key-range membership bitmap (null: linear-probing HT)
-  int32_t* payarr;   // payload indexed by key - kmin (null: join carries no payload)
-  int32_t kmin;
-  uint32_t nbits;
+  void* tbl;               // bitmap words / u8 codes / u16 codes
+  uint32_t kmin, nkeys;    // key domain of the direct tables
+  int32_t glo, gcard;      // group part fed by the payload (gcard 0: none)
+  int64_t maxcap;          // kTabHash: slot capacity bound
+  int2* compact;           // kTabHash: filtered {key, digit}
+  int2* slots;             // kTabHash: linear-probing slots
+  uint32_t clear_words;    // 32-bit words of the table to clear
+  uint32_t clear_value;    // 0 (bitmap) or 0xFFFFFFFF (codes: all absent)
 };
 
 struct DimBuildArgs {
@@ -55,32 +69,28 @@ struct DimBuildArgs {
   HtMeta* meta;
 };
 
-struct JoinDesc {
-  const int32_t* fk;  // lineorder foreign-key column (shard)
-  const int2* slots;
-  int32_t glo, gcard, gstride;  // group part fed by this join's payload (gcard 0: none)
-  const uint32_t* bitmap;       // membership bitmap over [kmin, kmin+nbits) (null: probe the HT)
-  const int32_t* payarr;        // payload of member key k at payarr[k - kmin]
-  int32_t kmin;
-  uint32_t nbits;
-  int32_t need_payload;
+struct PrologueArgs {
+  DimBuildArgs* unused;
+  uint32_t* tbl[kMaxJoins];
+  uint32_t words[kMaxJoins];
+  uint32_t value[kMaxJoins];
+  unsigned long long* zero64;  // aggregate [2*cells] + counters (may be null)
+  int64_t zero64_n;
+  unsigned long long* zero64b; // result header (may be null)
+  int64_t zero64b_n;
+  HtMeta* meta;
 };
 
-struct FusedArgs {
-  int64_t n;  // rows in the shard
-  JoinDesc j[kMaxJoins];
-  const HtMeta* meta;
-  const int32_t* fcol[3];  // flight 1 filter columns
+struct Flight1Args {
+  int64_t n;
+  const int32_t* fcol[3];
   int32_t flo[3], fhi[3];
   const int32_t* agg_a;
   const int32_t* agg_b;
   int32_t agg_b_is_f1;
-  int32_t cells;
-  unsigned long long* g_sum;  // [cells]
-  unsigned long long* g_cnt;  // [cells]
-  unsigned long long* surv;   // [4]
-  int32_t* err;
-  int32_t smem_bm_words;      // shared-memory room for the first join's bitmap
+  unsigned long long* g_sum;
+  unsigned long long* g_cnt;
+  unsigned long long* surv;
 };
 
 struct ResultHeader {
@@ -103,7 +113,49 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
+// ---------------------------------------------------------- prologue
+
+__global__ void query_prologue_kernel(const PrologueArgs a) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int j = 0; j < kMaxJoins; ++j) {
+    uint32_t* t = a.tbl[j];
+    if (!t) continue;
+    const uint32_t v = a.value[j];
+    for (int64_t i = tid; i < a.words[j]; i += stride) t[i] = v;
+  }
+  for (int64_t i = tid; i < a.zero64_n; i += stride) a.zero64[i] = 0;
+  for (int64_t i = tid; i < a.zero64b_n; i += stride) a.zero64b[i] = 0;
+  if (tid < kMaxJoins) a.meta[tid] = HtMeta{0, 0u, 0, 0};
+}
+
 // ---------------------------------------------------------- dimension builds
+
+// group digit of a dimension row's payload: payload - lo, or "bad" when it
+// falls outside the declared domain (the reference throws only if such a
+// row reaches the aggregate, ssb_queries.cpp:32-33)
+__device__ __forceinline__ int32_t digit_of(const DimBuildDesc& d, int32_t pay) {
+  if (d.gcard == 0) return 0;
+  const int32_t u = pay - d.glo;
+  return (uint32_t)u < (uint32_t)d.gcard ? u : -1;
+}
+
+// claim byte/half `off` of a code table: absent -> code; anything else is a
+// duplicate key (BuildError, hash_table.cpp:51-93)
+template <int BITS>
+__device__ __forceinline__ bool claim_code(void* tbl, uint32_t off, uint32_t code) {
+  constexpr uint32_t kMask = (1u << BITS) - 1u;
+  constexpr uint32_t kPer = 32 / BITS;
+  uint32_t* w = reinterpret_cast<uint32_t*>(tbl) + off / kPer;
+  const unsigned sh = (off % kPer) * BITS;
+  uint32_t old = *reinterpret_cast<volatile uint32_t*>(w), assumed;
+  do {
+    if (((old >> sh) & kMask) != kMask) return false;
+    assumed = old;
+    old = atomicCAS(w, assumed, (assumed & ~(kMask << sh)) | ((code & kMask) << sh));
+  } while (old != assumed);
+  return true;
+}
 
 __global__ void dim_filter_kernel(const DimBuildArgs a) {
   const DimBuildDesc& d = a.d[blockIdx.y];
@@ -125,34 +177,40 @@ __global__ void dim_filter_kernel(const DimBuildArgs a) {
     if (bal == 0) continue;
     const int leader = __ffs(bal) - 1;
     int pos0 = 0;
-    if ((int)lane == leader) pos0 = atomicAdd(&m->count, __popc(bal));  // build size (both layouts)
+    if ((int)lane == leader) pos0 = atomicAdd(&m->count, __popc(bal));  // build size
     pos0 = __shfl_sync(0xffffffffu, pos0, leader);
-    if (pass) {
-      const int32_t key = d.key[row];
-      const int32_t pay = d.payload ? d.payload[row] : 0;
-      if (d.bitmap) {
-        // perfect hash over the key range: set the member bit, store the payload
-        const uint32_t off = (uint32_t)key - (uint32_t)d.kmin;  // < nbits by the column statistics
-        if (off < d.nbits) {
-          const uint32_t old = atomicOr(d.bitmap + (off >> 5), 1u << (off & 31));
-          if ((old >> (off & 31)) & 1u) atomicCAS(&m->err, 0, 2);  // duplicate key (BuildError)
-          if (d.payarr) d.payarr[off] = pay;
-        }
-      } else {
-        const int pos = pos0 + __popc(bal & lanemask_lt());
-        d.compact[pos] = make_int2(key, pay);
-      }
+    if (!pass) continue;
+    const int32_t key = d.key[row];
+    const int32_t dig = digit_of(d, d.payload ? d.payload[row] : 0);
+    if (d.kind == kTabHash) {
+      d.compact[pos0 + __popc(bal & lanemask_lt())] = make_int2(key, dig);
+      continue;
     }
+    const uint32_t off = (uint32_t)key - d.kmin;  // < nkeys by the column statistics
+    if (off >= d.nkeys) {
+      atomicCAS(&m->err, 0, 4);  // statistics do not cover the key: cannot happen for valid stats
+      continue;
+    }
+    bool ok;
+    if (d.kind == kTabBitmap) {
+      const uint32_t bit = 1u << (off & 31);
+      ok = !(atomicOr(reinterpret_cast<uint32_t*>(d.tbl) + (off >> 5), bit) & bit);
+    } else if (d.kind == kTabU8) {
+      ok = claim_code<8>(d.tbl, off, dig < 0 ? pipe::kU8Bad : (uint32_t)dig);
+    } else {
+      ok = claim_code<16>(d.tbl, off, dig < 0 ? pipe::kU16Bad : (uint32_t)dig);
+    }
+    if (!ok) atomicCAS(&m->err, 0, 2);  // duplicate key (BuildError)
   }
 }
 
 __global__ void dim_init_kernel(const DimBuildArgs a) {
   const DimBuildDesc& d = a.d[blockIdx.y];
   HtMeta* m = a.meta + blockIdx.y;
-  if (d.bitmap) return;  // perfect-hash layout needs no slot table
+  if (d.kind != kTabHash) return;
   const int64_t n = m->count;
   int64_t cap = 2;
-  while (cap < 2 * n) cap <<= 1;  // max(2, bit_ceil(2n))
+  while (cap < 2 * n) cap <<= 1;  // max(2, bit_ceil(2n)), ssb_queries.cpp:119
   if (cap > d.maxcap) {
     if (blockIdx.x == 0 && threadIdx.x == 0) m->err = 3;
     return;
@@ -169,7 +227,7 @@ __global__ void dim_init_kernel(const DimBuildArgs a) {
 __global__ void dim_insert_kernel(const DimBuildArgs a) {
   const DimBuildDesc& d = a.d[blockIdx.y];
   HtMeta* m = a.meta + blockIdx.y;
-  if (d.bitmap) return;
+  if (d.kind != kTabHash) return;
   const int64_t n = m->count;
   if (m->err) return;
   const uint32_t mask = m->mask;
@@ -181,7 +239,7 @@ __global__ void dim_insert_kernel(const DimBuildArgs a) {
   }
 }
 
-// ---------------------------------------------------------- fused pipelines
+// ---------------------------------------------------------- flight 1
 
 template <int BT, class T>
 __device__ __forceinline__ T block_sum(T v, T* red) {
@@ -196,48 +254,12 @@ __device__ __forceinline__ T block_sum(T v, T* red) {
   return s;  // valid in thread 0
 }
 
-// One join of the pipeline (BlockProbeHashTable).  When the dimension key
-// column has a compact value range the build uses the perfect-hash layout of
-// the Crystal paper's SSB kernels: an exact membership bitmap over
-// [kmin, kmin+nbits) plus a payload array indexed by key - kmin, so a probe is
-// one bit test (+ one payload load for members).  Otherwise the build is the
-// reference's linear-probing table and every probe walks it
-// (hash_table.hpp:41-51).  `bm` is the bitmap (a shared-memory copy for the
-// first join when staged).
-template <int IPT>
-__device__ __forceinline__ void probe_join(const JoinDesc& jd, const uint32_t* bm, bool bm_smem,
-                                           uint32_t mask, int shift, const int32_t (&key)[IPT],
-                                           unsigned& f, int32_t (&pay)[IPT]) {
-  if (bm) {
-    const uint32_t kmin = (uint32_t)jd.kmin, nbits = jd.nbits;
-    // Branch-free: every item issues its bitmap-word load (word 0 when out of
-    // range or already dead) before any word is examined, so a thread keeps
-    // IPT independent loads in flight.
-    uint32_t off[IPT], w[IPT];
-#pragma unroll
-    for (int k = 0; k < IPT; ++k) {
-      off[k] = (uint32_t)key[k] - kmin;  // bijective, so only [kmin, kmin+nbits) lands < nbits
-      const bool in = ((f >> k) & 1u) && off[k] < nbits;
-      f &= ~((unsigned)!in << k);
-      const uint32_t wi = in ? (off[k] >> 5) : 0u;
-      w[k] = bm_smem ? bm[wi] : __ldg(bm + wi);
-    }
-#pragma unroll
-    for (int k = 0; k < IPT; ++k) f &= ~((((w[k] >> (off[k] & 31)) & 1u) ^ 1u) << k);
-    if (jd.need_payload) {
-#pragma unroll
-      for (int k = 0; k < IPT; ++k)
-        if ((f >> k) & 1u) pay[k] = __ldg(jd.payarr + off[k]);
-    }
-    return;
-  }
-  BlockProbeHashTable<IPT>(key, f, pay, jd.slots, mask, shift);
-}
-
-// Flight 1 (run_flight1, ssb_queries.cpp:157-210): three chained range
-// predicates (INIT, AND, AND), SUM(extendedprice * discount) in 8 bytes.
+// run_flight1 (ssb_queries.cpp:157-210): three chained range predicates
+// (INIT, AND, AND), SUM(extendedprice * discount) in 8 bytes.  A later
+// column is read only in vectors that still hold a live row (BlockLoadSel),
+// so dead 32 B sectors are never fetched.
 template <int BT, int IPT>
-__global__ void __launch_bounds__(BT) ssb_flight1_kernel(const FusedArgs a) {
+__global__ void __launch_bounds__(BT) ssb_flight1_kernel(const Flight1Args a) {
   using L = VecLayout<BT, IPT>;
   __shared__ long long red[BT / 32];
   long long sum = 0;
@@ -266,103 +288,6 @@ __global__ void __launch_bounds__(BT) ssb_flight1_kernel(const FusedArgs a) {
     atomicAdd(a.g_sum, (unsigned long long)s);
     atomicAdd(a.g_cnt, (unsigned long long)c);
     atomicAdd(a.surv, (unsigned long long)c);
-  }
-}
-
-// Flights 2-4 (run_joins, ssb_queries.cpp:212-273).  NJ joins probed in plan
-// order; AGG = revenue or revenue - supplycost; SMEM selects a CTA-private
-// dense aggregate in shared memory (flushed once per CTA) vs global atomics.
-template <int NJ, int AGG, bool SMEM, int BT, int IPT>
-__global__ void __launch_bounds__(BT) ssb_join_kernel(const FusedArgs a) {
-  using L = VecLayout<BT, IPT>;
-  extern __shared__ unsigned long long s_dyn[];
-  __shared__ unsigned long long red[BT / 32];
-  unsigned long long* s_sum = s_dyn;
-  unsigned* s_cnt = reinterpret_cast<unsigned*>(s_dyn + a.cells);
-
-  uint32_t mask[NJ];
-  int shift[NJ];
-#pragma unroll
-  for (int j = 0; j < NJ; ++j) {
-    mask[j] = a.meta[j].mask;
-    shift[j] = a.meta[j].shift;
-  }
-  if constexpr (SMEM) {
-    for (int c = threadIdx.x; c < a.cells; c += BT) {
-      s_sum[c] = 0;
-      s_cnt[c] = 0;
-    }
-    __syncthreads();
-  }
-  unsigned surv[NJ];
-#pragma unroll
-  for (int j = 0; j < NJ; ++j) surv[j] = 0;
-  int bad = 0;
-
-  const int64_t ntiles = (a.n + L::TILE - 1) / L::TILE;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t base = tile * L::TILE;
-    const int valid = (int)min((int64_t)L::TILE, a.n - base);
-    unsigned f = BlockValidMask<BT, IPT>(valid);
-    int32_t key[IPT], pay[IPT], idx[IPT];
-#pragma unroll
-    for (int k = 0; k < IPT; ++k) idx[k] = 0;
-#pragma unroll
-    for (int j = 0; j < NJ; ++j) {
-      if (j == 0)
-        BlockLoad<BT, IPT>(a.j[0].fk + base, valid, key);
-      else
-        BlockLoadSel<BT, IPT>(a.j[j].fk + base, valid, f, key);
-      probe_join<IPT>(a.j[j], a.j[j].bitmap, false, mask[j], shift[j], key, f, pay);
-      if (a.j[j].gcard) {
-        const int32_t glo = a.j[j].glo, gcard = a.j[j].gcard, gst = a.j[j].gstride;
-#pragma unroll
-        for (int k = 0; k < IPT; ++k) {
-          if ((f >> k) & 1u) {
-            const int32_t u = pay[k] - glo;
-            if ((uint32_t)u >= (uint32_t)gcard) bad = 1;  // ssb_queries.cpp:32-33
-            idx[k] += u * gst;
-          }
-        }
-      }
-      surv[j] += __popc(f);
-    }
-    int32_t va[IPT], vb[IPT];
-    BlockLoadSel<BT, IPT>(a.agg_a + base, valid, f, va);
-    if constexpr (AGG == kAggRevenueMinusSupplyCost) BlockLoadSel<BT, IPT>(a.agg_b + base, valid, f, vb);
-#pragma unroll
-    for (int k = 0; k < IPT; ++k) {
-      if ((f >> k) & 1u) {
-        long long v = va[k];
-        if constexpr (AGG == kAggRevenueMinusSupplyCost) v -= (long long)vb[k];
-        const uint32_t c = (uint32_t)idx[k];
-        if (c < (uint32_t)a.cells) {
-          if constexpr (SMEM) {
-            atomicAdd(&s_sum[c], (unsigned long long)v);
-            atomicAdd(&s_cnt[c], 1u);
-          } else {
-            atomicAdd(&a.g_sum[c], (unsigned long long)v);
-            atomicAdd(&a.g_cnt[c], 1ull);
-          }
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < NJ; ++j) {
-    const unsigned long long s = block_sum<BT>((unsigned long long)surv[j], red);
-    if (threadIdx.x == 0 && s) atomicAdd(&a.surv[j], s);
-  }
-  if (bad) atomicExch(a.err, 2);
-  if constexpr (SMEM) {
-    __syncthreads();
-    for (int c = threadIdx.x; c < a.cells; c += BT) {
-      const unsigned n = s_cnt[c];
-      if (n) {
-        atomicAdd(&a.g_sum[c], s_sum[c]);
-        atomicAdd(&a.g_cnt[c], (unsigned long long)n);
-      }
-    }
   }
 }
 
@@ -400,296 +325,133 @@ __global__ void finalize_kernel(const unsigned long long* sums, const unsigned l
   }
 }
 
+// ---------------------------------------------------------- dispatch
 
+#define CRYS_F1_SHAPES(X) X(128, 4) X(256, 16) X(128, 16) X(512, 8) X(256, 8)
+constexpr int kNativeBT = 256, kNativeIPT = 16;  // flight 1 shape for uncompiled TileConfigs
 
-// ---------------------------------------------------------- async-staged pipeline
-// Native sm_100a form of the fused join flights.  Every warp runs its own
-// software pipeline over "warp-tiles" of 32 x IPT rows: while it probes tile
-// t, the referenced lineorder columns of its next D tiles are already in
-// flight into a warp-private shared-memory ring through cp.async (LDGSTS,
-// 16 B per lane per column, zero-filled past the shard end, L1 bypassed).
-// Each lane reads back only the chunks it copied, so no warp/CTA barrier is
-// needed per tile; warps drift freely and the SM always has D tiles per warp
-// of HBM traffic outstanding.  The dependent chain left per tile is the
-// dimension probes (shared-memory bitmap for the first join, L1/L2 for the
-// rest), which the 16-32 resident warps per SM overlap.
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
-               "r"(src_bytes)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
+using F1Fn = void (*)(const Flight1Args);
 
-template <int NJ, int AGG>
-struct StagedCols {
-  static constexpr int NC = NJ + (AGG == kAggRevenueMinusSupplyCost ? 2 : 1);
-};
-
-template <int NJ, int AGG, bool SMEM, int WARPS, int IPT, int D>
-__global__ void __launch_bounds__(WARPS * 32) ssb_join_async_kernel(const FusedArgs a) {
-  constexpr int NC = StagedCols<NJ, AGG>::NC;
-  constexpr int WT = 32 * IPT;  // rows per warp-tile
-  constexpr int NV = IPT / 4;   // 16 B chunks per lane per column
-  static_assert(IPT % 4 == 0, "16-byte chunks");
-  constexpr int SLOT = NC * WT;  // int32 per ring slot
-  extern __shared__ unsigned long long s_dyn[];
-  int32_t* s_ints = reinterpret_cast<int32_t*>(s_dyn);
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  int32_t* ring = s_ints + (size_t)warp * (D + 1) * SLOT;
-  unsigned long long* s_sum = reinterpret_cast<unsigned long long*>(s_ints + (size_t)WARPS * (D + 1) * SLOT);
-  unsigned* s_cnt = reinterpret_cast<unsigned*>(s_sum + (SMEM ? a.cells : 0));
-  uint32_t* s_bm = s_cnt + (SMEM ? a.cells : 0);
-
-  const int bm_words = a.smem_bm_words;
-  for (int i = threadIdx.x; i < bm_words; i += blockDim.x) s_bm[i] = __ldg(a.j[0].bitmap + i);
-  if constexpr (SMEM) {
-    for (int c = threadIdx.x; c < a.cells; c += blockDim.x) {
-      s_sum[c] = 0;
-      s_cnt[c] = 0;
-    }
-  }
-  __syncthreads();
-
-  const int32_t* cols[NC];
-#pragma unroll
-  for (int j = 0; j < NJ; ++j) cols[j] = a.j[j].fk;
-  cols[NJ] = a.agg_a;
-  if constexpr (NC > NJ + 1) cols[NJ + 1] = a.agg_b;
-  uint32_t mask[NJ];
-  int shift[NJ];
-#pragma unroll
-  for (int j = 0; j < NJ; ++j) {
-    mask[j] = a.meta[j].mask;
-    shift[j] = a.meta[j].shift;
-  }
-
-  const int64_t nwt = (a.n + WT - 1) / WT;
-  const int64_t tw = (int64_t)gridDim.x * WARPS;
-  const int64_t t0 = (int64_t)blockIdx.x * WARPS + warp;
-
-  auto issue = [&](int64_t t, int slot) {
-    int32_t* dst = ring + slot * SLOT;
-    const int64_t base = t * WT;
-    if (base + WT <= a.n) {  // interior tile (warp-uniform): no bounds arithmetic
-#pragma unroll
-      for (int c = 0; c < NC; ++c)
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          const int off = (v * 32 + lane) * 4;
-          cp_async16(dst + c * WT + off, cols[c] + base + off, 16);
-        }
-      return;
-    }
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const int off = (v * 32 + lane) * 4;
-        const int64_t row = base + off;
-        const int64_t rem = a.n - row;
-        const int bytes = rem >= 4 ? 16 : (rem > 0 ? (int)rem * 4 : 0);
-        cp_async16(dst + c * WT + off, cols[c] + (bytes ? row : 0), bytes);
-      }
-    }
-  };
-
-#pragma unroll
-  for (int d = 0; d < D; ++d) {
-    if (t0 + d * tw < nwt) issue(t0 + d * tw, d);
-    cp_async_commit();
-  }
-
-  unsigned surv[NJ];
-#pragma unroll
-  for (int j = 0; j < NJ; ++j) surv[j] = 0;
-  int bad = 0;
-  int it = 0;
-  for (int64_t t = t0; t < nwt; t += tw, ++it) {
-    const int64_t tn = t + (int64_t)D * tw;
-    if (tn < nwt) issue(tn, (it + D) % (D + 1));
-    cp_async_commit();
-    cp_async_wait<D>();
-    const int32_t* st = ring + (it % (D + 1)) * SLOT;
-    const int64_t base = t * WT;
-    const int valid = (int)min((int64_t)WT, a.n - base);
-    unsigned f = (1u << IPT) - 1u;
-    if (valid < WT) {
-      f = 0;
-#pragma unroll
-      for (int k = 0; k < IPT; ++k) f |= (unsigned)(((k >> 2) * 32 + lane) * 4 + (k & 3) < valid) << k;
-    }
-    int32_t key[IPT], pay[IPT], idx[IPT];
-#pragma unroll
-    for (int k = 0; k < IPT; ++k) idx[k] = 0;
-#pragma unroll
-    for (int j = 0; j < NJ; ++j) {
-      if (f == 0) break;
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const int4 x = *reinterpret_cast<const int4*>(st + j * WT + (v * 32 + lane) * 4);
-        key[v * 4 + 0] = x.x; key[v * 4 + 1] = x.y; key[v * 4 + 2] = x.z; key[v * 4 + 3] = x.w;
-      }
-      if (j == 0 && bm_words)
-        probe_join<IPT>(a.j[0], s_bm, true, mask[0], shift[0], key, f, pay);
-      else
-        probe_join<IPT>(a.j[j], a.j[j].bitmap, false, mask[j], shift[j], key, f, pay);
-      if (a.j[j].gcard) {
-        const int32_t glo = a.j[j].glo, gcard = a.j[j].gcard, gst = a.j[j].gstride;
-#pragma unroll
-        for (int k = 0; k < IPT; ++k) {
-          if ((f >> k) & 1u) {
-            const int32_t u = pay[k] - glo;
-            if ((uint32_t)u >= (uint32_t)gcard) bad = 1;
-            idx[k] += u * gst;
-          }
-        }
-      }
-      surv[j] += __popc(f);
-    }
-    if (f) {
-#pragma unroll
-      for (int k = 0; k < IPT; ++k) {
-        if ((f >> k) & 1u) {
-          const int o = ((k >> 2) * 32 + lane) * 4 + (k & 3);
-          long long v = st[NJ * WT + o];
-          if constexpr (AGG == kAggRevenueMinusSupplyCost) v -= (long long)st[(NJ + 1) * WT + o];
-          const uint32_t c = (uint32_t)idx[k];
-          if (c < (uint32_t)a.cells) {
-            if constexpr (SMEM) {
-              atomicAdd(&s_sum[c], (unsigned long long)v);
-              atomicAdd(&s_cnt[c], 1u);
-            } else {
-              atomicAdd(&a.g_sum[c], (unsigned long long)v);
-              atomicAdd(&a.g_cnt[c], 1ull);
-            }
-          }
-        }
-      }
-    }
-  }
-  cp_async_wait<0>();
-#pragma unroll
-  for (int j = 0; j < NJ; ++j) {
-    const unsigned long long w = warp_sum((unsigned long long)surv[j]);
-    if (lane == 0 && w) atomicAdd(&a.surv[j], w);
-  }
-  if (bad) atomicExch(a.err, 2);
-  if constexpr (SMEM) {
-    __syncthreads();
-    for (int c = threadIdx.x; c < a.cells; c += blockDim.x) {
-      const unsigned n = s_cnt[c];
-      if (n) {
-        atomicAdd(&a.g_sum[c], s_sum[c]);
-        atomicAdd(&a.g_cnt[c], (unsigned long long)n);
-      }
-    }
-  }
-}
-
-template <int NJ, int AGG, int WARPS, int IPT, int D>
-size_t staged_smem(bool smem_agg, int64_t cells, int bm_words) {
-  return sizeof(int32_t) * (size_t)WARPS * (D + 1) * StagedCols<NJ, AGG>::NC * 32 * IPT +
-         (smem_agg ? (size_t)cells * 12 : 0) + sizeof(uint32_t) * (size_t)bm_words;
-}
-
-// ---------------------------------------------------------- dispatch tables
-
-#define CRYS_SSB_SHAPES(X) X(128, 4) X(256, 16) X(128, 16) X(512, 8)
-constexpr int kNativeBT = 256, kNativeIPT = 16;  // flight 1 fallback shape
-
-using KernelFn = void (*)(const FusedArgs);
-
-template <int BT, int IPT>
-KernelFn pick_kernel(int njoins, int agg, bool smem) {
-  if (njoins == 0) return ssb_flight1_kernel<BT, IPT>;
-  if (njoins == 3 && agg == kAggRevenue)
-    return smem ? ssb_join_kernel<3, kAggRevenue, true, BT, IPT>
-                : ssb_join_kernel<3, kAggRevenue, false, BT, IPT>;
-  if (njoins == 4 && agg == kAggRevenueMinusSupplyCost)
-    return smem ? ssb_join_kernel<4, kAggRevenueMinusSupplyCost, true, BT, IPT>
-                : ssb_join_kernel<4, kAggRevenueMinusSupplyCost, false, BT, IPT>;
-  fail(CRYS_ENOTBUILT, "no fused kernel for this plan shape");
-}
-
-struct Launch {
-  KernelFn fn;
+struct F1Launch {
+  F1Fn fn;
   int bt, ipt;
 };
 
-Launch select_kernel(int bt, int ipt, int njoins, int agg, bool smem) {
+// Results are tile-invariant (test_ssb.cpp:251-261), so the TileConfig of a
+// query is validated but the GPU runs its own tuned shape; CRYS_F1_TILE=BTxIPT
+// forces a compiled shape (ablation / tuning).
+F1Launch select_flight1() {
+  static const std::pair<int, int> forced = [] {
+    const char* e = getenv("CRYS_F1_TILE");
+    int b = 0, i = 0;
+    if (e && sscanf(e, "%dx%d", &b, &i) == 2) return std::make_pair(b, i);
+    return std::make_pair(kNativeBT, kNativeIPT);
+  }();
 #define X(B, I) \
-  if (bt == B && ipt == I) return {pick_kernel<B, I>(njoins, agg, smem), B, I};
-  CRYS_SSB_SHAPES(X)
+  if (forced.first == B && forced.second == I) return {ssb_flight1_kernel<B, I>, B, I};
+  CRYS_F1_SHAPES(X)
 #undef X
-  // Results are tile-invariant (test_ssb.cpp:251-261), so an uncompiled but
-  // valid TileConfig runs the native sm_100a shape.
-  return {pick_kernel<kNativeBT, kNativeIPT>(njoins, agg, smem), kNativeBT, kNativeIPT};
+  return {ssb_flight1_kernel<kNativeBT, kNativeIPT>, kNativeBT, kNativeIPT};
 }
 
-int blocks_per_sm(crys_ctx* ctx, KernelFn fn, int bt, size_t smem) {
+int blocks_per_sm(const void* fn, int bt, size_t smem) {
   static std::mutex mu;
   static std::map<std::pair<const void*, size_t>, int> cache;
   std::lock_guard<std::mutex> lk(mu);
-  auto key = std::make_pair((const void*)fn, smem);
+  auto key = std::make_pair(fn, smem);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
-  ensure_dyn_smem((const void*)fn, smem);
+  ensure_dyn_smem(fn, smem);
   int nb = 0;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, bt, smem));
   if (nb < 1) nb = 1;
   cache[key] = nb;
-  (void)ctx;
   return nb;
 }
 
-template <int NJ, int AGG, int WARPS, int IPT, int D>
-void launch_staged(crys_ctx* ctx, FusedArgs fa, bool smem_agg, int64_t cells, int64_t n,
-                   const std::string& name) {
-  if (smem_agg && staged_smem<NJ, AGG, WARPS, IPT, D>(true, cells, fa.smem_bm_words) > 227 * 1024)
-    smem_agg = false;  // the CTA-private table does not fit: global atomics
-  KernelFn fn = smem_agg ? ssb_join_async_kernel<NJ, AGG, true, WARPS, IPT, D>
-                         : ssb_join_async_kernel<NJ, AGG, false, WARPS, IPT, D>;
-  const int threads = WARPS * 32;
-  size_t dyn = staged_smem<NJ, AGG, WARPS, IPT, D>(smem_agg, cells, fa.smem_bm_words);
-  if (dyn > 200 * 1024 && fa.smem_bm_words) {  // no room to stage the first bitmap
-    fa.smem_bm_words = 0;
-    dyn = staged_smem<NJ, AGG, WARPS, IPT, D>(smem_agg, cells, 0);
+constexpr size_t kSmemOptin = 232448;  // 227 KB dynamic shared memory per CTA (sm_100a)
+
+// Shared-memory placement of the probe tables (plan order: join 0 is probed
+// for every row, later joins only for survivors) and then of the CTA-private
+// aggregate, inside what the ring leaves of 227 KB.
+size_t place_smem(pipe::PipeArgs& pa, int nj, size_t fixed, int64_t cells) {
+  size_t off = fixed;
+  for (int j = 0; j < nj; ++j) {
+    ProbeTab& t = pa.tab[j];
+    t.smem = -1;
+    if (t.kind == kTabHash || t.bytes == 0) continue;
+    if (off + t.bytes <= kSmemOptin) {
+      t.smem = (int32_t)off;
+      off += t.bytes;
+    }
   }
-  CRYS_CHECK(dyn <= 227 * 1024, CRYS_ENOTBUILT, "staged pipeline exceeds shared memory");
-  ensure_dyn_smem((const void*)fn, dyn);
-  const int nb = blocks_per_sm(ctx, fn, threads, dyn);
-  const int64_t wt = 32 * IPT;
-  const int64_t nwt = (n + wt - 1) / wt;
-  const int grid = (int)std::max<int64_t>(
-      1, std::min<int64_t>((nwt + WARPS - 1) / WARPS, (int64_t)nb * ctx->num_sms));
-  fn<<<grid, threads, dyn, ctx->stream>>>(fa);
-  CRYS_LAUNCHED(std::string("fused-staged ") + name + " grid=" + std::to_string(grid) + " smem=" +
-                std::to_string(dyn));
+  pa.smem_agg = -1;
+  const size_t agg = ((size_t)cells * 12 + 15) & ~(size_t)15;
+  if (off + agg <= kSmemOptin) {
+    pa.smem_agg = (int32_t)off;
+    off += agg;
+  }
+  return off;
 }
 
-template <int NJ, int AGG>
-void launch_staged_cfg(crys_ctx* ctx, const FusedArgs& fa, bool smem_agg, int64_t cells, int64_t n,
-                       const std::string& name) {
+template <int NJ, int NC, int W, int TILE, int STAGES, int K0, bool S0>
+void launch_pipeline(crys_ctx* ctx, const pipe::PipeArgs& pa, size_t dyn, const std::string& name) {
+  auto fn = pipe::ssb_pipeline_kernel<NJ, NC, W, TILE, STAGES, K0, S0>;
+  const int threads = (W + 1) * 32;
+  const int nb = blocks_per_sm((const void*)fn, threads, dyn);
+  const int64_t ntiles = (pa.n + TILE - 1) / TILE;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)nb * ctx->num_sms));
+  fn<<<grid, threads, dyn, ctx->stream>>>(pa);
+  CRYS_LAUNCHED(std::string("ssb_pipeline ") + name + " grid=" + std::to_string(grid) +
+                " smem=" + std::to_string(dyn));
+}
+
+template <int NJ, int NC, int W, int TILE, int STAGES>
+void launch_pipeline_k0(crys_ctx* ctx, pipe::PipeArgs pa, int64_t cells, const std::string& name) {
+  const size_t fixed = pipe::fixed_smem<NC, TILE, STAGES>();
+  CRYS_CHECK(fixed <= kSmemOptin, CRYS_ENOTBUILT, "pipeline ring exceeds shared memory");
+  const size_t dyn = place_smem(pa, NJ, fixed, cells);
+  const bool s0 = pa.tab[0].smem >= 0;
+  switch (pa.tab[0].kind) {
+    case kTabBitmap:
+      if (s0) launch_pipeline<NJ, NC, W, TILE, STAGES, kTabBitmap, true>(ctx, pa, dyn, name);
+      else launch_pipeline<NJ, NC, W, TILE, STAGES, kTabBitmap, false>(ctx, pa, dyn, name);
+      break;
+    case kTabU8:
+      if (s0) launch_pipeline<NJ, NC, W, TILE, STAGES, kTabU8, true>(ctx, pa, dyn, name);
+      else launch_pipeline<NJ, NC, W, TILE, STAGES, kTabU8, false>(ctx, pa, dyn, name);
+      break;
+    case kTabU16:
+      if (s0) launch_pipeline<NJ, NC, W, TILE, STAGES, kTabU16, true>(ctx, pa, dyn, name);
+      else launch_pipeline<NJ, NC, W, TILE, STAGES, kTabU16, false>(ctx, pa, dyn, name);
+      break;
+    default:
+      launch_pipeline<NJ, NC, W, TILE, STAGES, kTabHash, false>(ctx, pa, dyn, name);
+  }
+}
+
+// Tuning knob CRYS_PIPE_CFG selects the (consumer warps, tile rows, stages)
+// instantiation; 0 is the default.
+int pipe_cfg() {
   static const int cfg = [] {
-    const char* e = getenv("CRYS_STAGED_CFG");  // tuning knob
-    return e ? atoi(e) : 5;
+    const char* e = getenv("CRYS_PIPE_CFG");
+    return e ? atoi(e) : 0;
   }();
-  switch (cfg) {
-    case 1: launch_staged<NJ, AGG, 8, 4, 1>(ctx, fa, smem_agg, cells, n, name); break;
-    case 2: launch_staged<NJ, AGG, 8, 8, 1>(ctx, fa, smem_agg, cells, n, name); break;
-    case 3: launch_staged<NJ, AGG, 16, 4, 2>(ctx, fa, smem_agg, cells, n, name); break;
-    case 4: launch_staged<NJ, AGG, 4, 4, 3>(ctx, fa, smem_agg, cells, n, name); break;
-    case 5: launch_staged<NJ, AGG, 32, 4, 1>(ctx, fa, smem_agg, cells, n, name); break;
-    case 6: launch_staged<NJ, AGG, 16, 4, 1>(ctx, fa, smem_agg, cells, n, name); break;
-    default: launch_staged<NJ, AGG, 8, 4, 2>(ctx, fa, smem_agg, cells, n, name); break;
+  return cfg;
+}
+
+template <int NJ, int NC>
+void launch_pipeline_cfg(crys_ctx* ctx, const pipe::PipeArgs& pa, int64_t cells,
+                         const std::string& name) {
+  // Ring depth: 4 x 32 KB (q2/q3) or 3 x 48 KB (q4) stages.  Measured on
+  // B200 (profiles/r01_pipeline_tuning.txt): the bytes in flight matter far
+  // more than keeping a later join's table in shared memory -- dropping a
+  // stage to fit q3.1's date table costs 2.3x.
+  constexpr int S = NC <= 4 ? 4 : 3;
+  switch (pipe_cfg()) {
+    case 1: launch_pipeline_k0<NJ, NC, 16, 4096, 2>(ctx, pa, cells, name); break;
+    case 2: launch_pipeline_k0<NJ, NC, 16, 2048, S>(ctx, pa, cells, name); break;
+    default: launch_pipeline_k0<NJ, NC, 16, 2048, S>(ctx, pa, cells, name); break;
   }
 }
 
@@ -698,13 +460,11 @@ void launch_staged_cfg(crys_ctx* ctx, const FusedArgs& fa, bool smem_agg, int64_
 // ---------------------------------------------------------- workspace
 
 struct QueryWorkspace {
-  DevBuf agg;      // u64 [2*cells]
-  DevBuf counters; // u64 surv[4] + i32 err
+  DevBuf agg;      // u64 [2*cells] + counters: surv[4] + err
   DevBuf meta;     // HtMeta[4]
   DevBuf slots[kMaxJoins];
   DevBuf compact[kMaxJoins];
-  DevBuf bitmap;   // membership bitmaps of all joins, contiguous (one memset)
-  DevBuf payarr[kMaxJoins];  // perfect-hash payload arrays
+  DevBuf tables;   // every join's direct probe table, contiguous, 16 B aligned
   DevBuf result;   // ResultHeader + RowOut[cells]
   PinnedBuf host;
 };
@@ -722,8 +482,14 @@ static int64_t bit_ceil64(int64_t v) {
   return c;
 }
 
-void ssb_query_partial(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt,
-                       unsigned long long* d_agg, unsigned long long* d_surv, int32_t* d_err) {
+// Enqueues dimension builds + the fused lineorder pass of `qid` over this
+// shard, accumulating into d_agg = [sums | counts] (cells each), d_surv[4] and
+// d_err.  `prologue_zero` additionally zeroes those buffers and the result
+// header in the same prologue launch (single-GPU path); the multi-GPU path
+// hands in caller-zeroed buffers.
+static void enqueue_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt,
+                          unsigned long long* d_agg, unsigned long long* d_surv, int32_t* d_err,
+                          unsigned long long* zero_extra, int64_t zero_extra_n, bool prologue_zero) {
   const QueryPlan& plan = plan_for(qid);
   CRYS_CHECK(bt > 0 && ipt > 0, CRYS_ECONFIG, "TileConfig: block_threads/items_per_thread must be positive");
   QueryWorkspace& ws = ws_of(ctx);
@@ -735,24 +501,40 @@ void ssb_query_partial(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ip
   const std::string& first_col = nj ? plan.joins[0].fact_key : plan.fact_filters[0].column;
   db->col("lineorder", first_col, &n);
 
-  FusedArgs fa;
-  std::memset(&fa, 0, sizeof(fa));
-  fa.n = n;
-  fa.cells = (int32_t)cells;
-  fa.g_sum = d_agg;
-  fa.g_cnt = d_agg + cells;
-  fa.surv = d_surv;
-  fa.err = d_err;
-
   ws.meta.reserve(sizeof(HtMeta) * kMaxJoins);
-  fa.meta = ws.meta.as<HtMeta>();
+  PrologueArgs pro;
+  std::memset(&pro, 0, sizeof(pro));
+  pro.meta = ws.meta.as<HtMeta>();
+  if (prologue_zero) {
+    // d_agg [2*cells] and the counters are contiguous in ws.agg
+    pro.zero64 = d_agg;
+    pro.zero64_n = 2 * cells + 5;
+    pro.zero64b = zero_extra;
+    pro.zero64b_n = zero_extra_n;
+  }
 
+  DimBuildArgs da;
+  std::memset(&da, 0, sizeof(da));
+  da.meta = ws.meta.as<HtMeta>();
+  pipe::PipeArgs pa;
+  std::memset(&pa, 0, sizeof(pa));
+  int64_t max_rows = 0, max_cap = 0;
+  bool any_ht = false;
   if (nj) {
-    // ---- dimension builds (build_dim_table, ssb_queries.cpp:99-121)
-    DimBuildArgs da;
-    std::memset(&da, 0, sizeof(da));
-    da.meta = ws.meta.as<HtMeta>();
-    int64_t max_rows = 0, max_cap = 0;
+    CRYS_CHECK(nj <= kMaxJoins, CRYS_ENOTBUILT, "at most four joins");
+    // group parts -> (join, lo, card, stride): mixed radix, last part fastest
+    int64_t stride = 1;
+    int32_t glo[kMaxJoins] = {0, 0, 0, 0}, gcard[kMaxJoins] = {0, 0, 0, 0};
+    for (int g = (int)plan.group.size() - 1; g >= 0; --g) {
+      const GroupPart& gp = plan.group[g];
+      CRYS_CHECK(gcard[gp.join_index] == 0, CRYS_ENOTBUILT, "one group part per join payload");
+      glo[gp.join_index] = gp.lo;
+      gcard[gp.join_index] = gp.hi - gp.lo + 1;
+      pa.tab[gp.join_index].gstride = (int32_t)stride;
+      stride *= (int64_t)(gp.hi - gp.lo + 1);
+    }
+    size_t tbl_bytes[kMaxJoins] = {0, 0, 0, 0}, tbl_off[kMaxJoins] = {0, 0, 0, 0}, tbl_total = 0;
+    constexpr int64_t kMaxDirect = int64_t(1) << 26;  // key-range bound of the direct tables
     for (int j = 0; j < nj; ++j) {
       const DimJoin& dj = plan.joins[j];
       DimBuildDesc& d = da.d[j];
@@ -771,144 +553,147 @@ void ssb_query_partial(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ip
           d.r[f][r][1] = dj.filters[f].ranges[r].second;
         }
       }
-      d.maxcap = std::max<int64_t>(2, bit_ceil64(2 * d.rows));
-      ws.slots[j].reserve(sizeof(int2) * d.maxcap);
-      ws.compact[j].reserve(sizeof(int2) * std::max<int64_t>(1, d.rows));
-      d.slots = ws.slots[j].as<int2>();
-      d.compact = ws.compact[j].as<int2>();
+      d.glo = glo[j];
+      d.gcard = gcard[j];
+      CRYS_CHECK(d.gcard <= 65534, CRYS_ENOTBUILT, "group domain too large for a 16-bit digit");
       max_rows = std::max(max_rows, d.rows);
-      max_cap = std::max(max_cap, d.maxcap);
-
-      JoinDesc& jd = fa.j[j];
-      jd.fk = db->col("lineorder", dj.fact_key, &rows);
-      CRYS_CHECK(rows == n, CRYS_ECONTRACT, "lineorder columns of different length");
-      jd.slots = d.slots;
-    }
-    // exact key-range membership bitmaps (dimension key statistics permitting)
-    constexpr int64_t kMaxBitmapBits = int64_t(1) << 25;  // 4 MB bitmap / 128 MB payloads per join
-    int64_t words_total = 0, word_off[kMaxJoins] = {0, 0, 0, 0};
-    for (int j = 0; j < nj; ++j) {
-      const DimJoin& dj = plan.joins[j];
+      // table layout: a perfect hash over the dense key range when the key
+      // column's statistics allow it, else the linear-probing table
       int32_t lo = 0, hi = -1;
-      word_off[j] = -1;
-      if (db->col_range(dj.dim_table, dj.dim_key, &lo, &hi) && (int64_t)hi - lo + 1 <= kMaxBitmapBits) {
-        da.d[j].kmin = lo;
-        da.d[j].nbits = (uint32_t)((int64_t)hi - lo + 1);
-        word_off[j] = words_total;
-        words_total += (da.d[j].nbits + 31) / 32 + 4;  // keep each bitmap 16 B aligned
-      }
-    }
-    if (words_total) {
-      ws.bitmap.reserve(sizeof(uint32_t) * (size_t)words_total);
-      CUDA_TRY(cudaMemsetAsync(ws.bitmap.p, 0, sizeof(uint32_t) * (size_t)words_total, st));
-    }
-    bool any_ht = false;
-    for (int j = 0; j < nj; ++j) {
-      if (word_off[j] < 0) {
+      const bool direct = db->col_range(dj.dim_table, dj.dim_key, &lo, &hi) &&
+                          (int64_t)hi - lo + 1 <= kMaxDirect;
+      if (direct) {
+        d.kmin = (uint32_t)lo;
+        d.nkeys = (uint32_t)((int64_t)hi - lo + 1);
+        if (dj.payload.empty() || d.gcard == 0) {
+          d.kind = kTabBitmap;
+          tbl_bytes[j] = ((size_t)(d.nkeys + 31) / 32) * 4;
+          d.clear_value = 0u;
+        } else {
+          d.kind = d.gcard <= 254 ? kTabU8 : kTabU16;
+          tbl_bytes[j] = (size_t)d.nkeys * (d.kind == kTabU8 ? 1 : 2);
+          d.clear_value = 0xFFFFFFFFu;
+        }
+        tbl_bytes[j] = (tbl_bytes[j] + 15) & ~(size_t)15;
+        d.clear_words = (uint32_t)(tbl_bytes[j] / 4);
+        tbl_off[j] = tbl_total;
+        tbl_total += tbl_bytes[j];
+      } else {
+        d.kind = kTabHash;
         any_ht = true;
-        continue;
+        d.maxcap = std::max<int64_t>(2, bit_ceil64(2 * d.rows));
+        ws.slots[j].reserve(sizeof(int2) * d.maxcap);
+        ws.compact[j].reserve(sizeof(int2) * std::max<int64_t>(1, d.rows));
+        d.slots = ws.slots[j].as<int2>();
+        d.compact = ws.compact[j].as<int2>();
+        max_cap = std::max(max_cap, d.maxcap);
       }
-      da.d[j].bitmap = ws.bitmap.as<uint32_t>() + word_off[j];
-      fa.j[j].bitmap = da.d[j].bitmap;
-      fa.j[j].kmin = da.d[j].kmin;
-      fa.j[j].nbits = da.d[j].nbits;
-      if (!plan.joins[j].payload.empty()) {
-        ws.payarr[j].reserve(sizeof(int32_t) * da.d[j].nbits);
-        da.d[j].payarr = ws.payarr[j].as<int32_t>();
-        fa.j[j].payarr = da.d[j].payarr;
-      }
+      ProbeTab& t = pa.tab[j];
+      t.kind = d.kind;
+      t.kmin = d.kmin;
+      t.n = d.nkeys;
+      t.bytes = (uint32_t)tbl_bytes[j];
+      t.meta = j;
+      t.g = d.kind == kTabHash ? (const void*)d.slots : nullptr;
+      if (d.kind != kTabHash) pipe::set_decode(t);
+      pa.col[j] = db->col("lineorder", dj.fact_key, &rows);
+      CRYS_CHECK(rows == n, CRYS_ECONTRACT, "lineorder columns of different length");
     }
-    for (int j = 0; j < nj; ++j) fa.j[j].need_payload = !plan.joins[j].payload.empty();
-    if (fa.j[0].bitmap) {
-      const int64_t w0 = (fa.j[0].nbits + 31) / 32;
-      fa.smem_bm_words = w0 <= 12288 ? (int32_t)w0 : 0;  // <= 48 KB of shared memory
+    if (tbl_total) ws.tables.reserve(tbl_total);
+    for (int j = 0; j < nj; ++j) {
+      if (da.d[j].kind == kTabHash) continue;
+      da.d[j].tbl = ws.tables.as<char>() + tbl_off[j];
+      pa.tab[j].g = da.d[j].tbl;
+      pro.tbl[j] = reinterpret_cast<uint32_t*>(da.d[j].tbl);
+      pro.words[j] = da.d[j].clear_words;
+      pro.value[j] = da.d[j].clear_value;
     }
-    // group parts -> (join, lo, card, stride): mixed radix, last part fastest
-    int64_t stride = 1;
-    for (int g = (int)plan.group.size() - 1; g >= 0; --g) {
-      const GroupPart& gp = plan.group[g];
-      JoinDesc& jd = fa.j[gp.join_index];
-      CRYS_CHECK(jd.gcard == 0, CRYS_ENOTBUILT, "one group part per join payload");
-      jd.glo = gp.lo;
-      jd.gcard = gp.hi - gp.lo + 1;
-      jd.gstride = (int32_t)stride;
-      stride *= (int64_t)(gp.hi - gp.lo + 1);
-    }
-    CUDA_TRY(cudaMemsetAsync(ws.meta.p, 0, sizeof(HtMeta) * kMaxJoins, st));
+  }
+  // ---- launches: prologue, dimension builds
+  {
+    int64_t work = std::max<int64_t>(pro.zero64_n, pro.zero64b_n);
+    for (int j = 0; j < kMaxJoins; ++j) work = std::max<int64_t>(work, pro.words[j]);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, (int64_t)ctx->num_sms * 4));
+    query_prologue_kernel<<<grid, 256, 0, st>>>(pro);
+    CRYS_LAUNCHED("query_prologue_kernel");
+    count_launch(ctx);
+  }
+  if (nj) {
     const int tpb = 256;
     const int gx_rows = (int)std::min<int64_t>((max_rows + tpb - 1) / tpb, (int64_t)ctx->num_sms * 8);
-    const int gx_cap = (int)std::min<int64_t>((max_cap + tpb - 1) / tpb, (int64_t)ctx->num_sms * 8);
     dim_filter_kernel<<<dim3(std::max(gx_rows, 1), nj), tpb, 0, st>>>(da);
     CRYS_LAUNCHED("dim_filter_kernel");
     count_launch(ctx);
     if (any_ht) {  // linear-probing builds (hash_table.cpp:20-94) for sparse key domains
+      const int gx_cap = (int)std::min<int64_t>((max_cap + tpb - 1) / tpb, (int64_t)ctx->num_sms * 8);
       dim_init_kernel<<<dim3(std::max(gx_cap, 1), nj), tpb, 0, st>>>(da);
       CRYS_LAUNCHED("dim_init_kernel");
       dim_insert_kernel<<<dim3(std::max(gx_rows, 1), nj), tpb, 0, st>>>(da);
       CRYS_LAUNCHED("dim_insert_kernel");
       count_launch(ctx, 2);
     }
-  } else {
-    int64_t rows = 0;
-    for (int f = 0; f < 3; ++f) {
-      fa.fcol[f] = db->col("lineorder", plan.fact_filters[f].column, &rows);
-      CRYS_CHECK(rows == n, CRYS_ECONTRACT, "lineorder columns of different length");
-      fa.flo[f] = plan.fact_filters[f].lo;
-      fa.fhi[f] = plan.fact_filters[f].hi;
-    }
-  }
-  // aggregate columns (agg_fact_columns, ssb_plans.cpp:287-299)
-  int64_t rows = 0;
-  if (plan.agg == kAggExtPriceTimesDiscount) {
-    fa.agg_a = db->col("lineorder", "lo_extendedprice", &rows);
-    fa.agg_b = db->col("lineorder", "lo_discount", &rows);
-    fa.agg_b_is_f1 = plan.fact_filters.size() > 1 && plan.fact_filters[1].column == "lo_discount";
-  } else {
-    fa.agg_a = db->col("lineorder", "lo_revenue", &rows);
-    if (plan.agg == kAggRevenueMinusSupplyCost) fa.agg_b = db->col("lineorder", "lo_supplycost", &rows);
   }
 
-  const size_t smem_bytes = (size_t)cells * 12;
-  static const size_t smem_max = [] {
-    const char* e = getenv("CRYS_SMEM_AGG_MAX");  // tuning knob (bytes)
-    return e ? (size_t)atoll(e) : (size_t)64 * 1024;
-  }();
-  const bool smem = nj > 0 && smem_bytes <= smem_max;
-  // The join flights run the async-staged pipeline (its warp-tile shape is
-  // fixed; results are tile-invariant, test_ssb.cpp:251-261).  The register-
-  // tile Crystal kernels remain reachable for ablation with
-  // CRYS_SSB_JOIN_KERNEL=register (TileConfig then picks the instantiation).
-  static const bool register_tiles = [] {
-    const char* e = getenv("CRYS_SSB_JOIN_KERNEL");
-    return e && std::string(e) == "register";
-  }();
-  if (nj > 0 && !register_tiles) {
+  // ---- the fused lineorder pass
+  int64_t rows = 0;
+  if (nj) {
+    pa.n = n;
+    pa.meta = ws.meta.as<HtMeta>();
+    pa.cells = (int32_t)cells;
+    pa.g_sum = d_agg;
+    pa.g_cnt = d_agg + cells;
+    pa.surv = d_surv;
+    pa.err = d_err;
+    CRYS_CHECK(plan.agg != kAggExtPriceTimesDiscount, CRYS_ENOTBUILT, "join flights aggregate revenue");
+    pa.col[nj] = db->col("lineorder", "lo_revenue", &rows);
+    if (plan.agg == kAggRevenueMinusSupplyCost) pa.col[nj + 1] = db->col("lineorder", "lo_supplycost", &rows);
     timing_kernel_begin(ctx);
     if (nj == 3 && plan.agg == kAggRevenue)
-      launch_staged_cfg<3, kAggRevenue>(ctx, fa, smem, cells, n, plan.name);
+      launch_pipeline_cfg<3, 4>(ctx, pa, cells, plan.name);
     else if (nj == 4 && plan.agg == kAggRevenueMinusSupplyCost)
-      launch_staged_cfg<4, kAggRevenueMinusSupplyCost>(ctx, fa, smem, cells, n, plan.name);
+      launch_pipeline_cfg<4, 6>(ctx, pa, cells, plan.name);
     else
-      fail(CRYS_ENOTBUILT, "no staged pipeline for this plan shape");
+      fail(CRYS_ENOTBUILT, "no fused pipeline for this plan shape");
     timing_kernel_end(ctx);
     count_launch(ctx);
     return;
   }
-  Launch L = select_kernel(bt, ipt, nj, plan.agg, smem);
-  const size_t dyn = smem ? smem_bytes : 0;
-  const int nb = blocks_per_sm(ctx, L.fn, L.bt, dyn);
+  Flight1Args fa;
+  std::memset(&fa, 0, sizeof(fa));
+  fa.n = n;
+  fa.g_sum = d_agg;
+  fa.g_cnt = d_agg + cells;
+  fa.surv = d_surv;
+  for (int f = 0; f < 3; ++f) {
+    fa.fcol[f] = db->col("lineorder", plan.fact_filters[f].column, &rows);
+    CRYS_CHECK(rows == n, CRYS_ECONTRACT, "lineorder columns of different length");
+    fa.flo[f] = plan.fact_filters[f].lo;
+    fa.fhi[f] = plan.fact_filters[f].hi;
+  }
+  // aggregate columns (agg_fact_columns, ssb_plans.cpp:287-299)
+  fa.agg_a = db->col("lineorder", "lo_extendedprice", &rows);
+  fa.agg_b = db->col("lineorder", "lo_discount", &rows);
+  fa.agg_b_is_f1 = plan.fact_filters.size() > 1 && plan.fact_filters[1].column == "lo_discount";
+  F1Launch L = select_flight1();
+  const int nb = blocks_per_sm((const void*)L.fn, L.bt, 0);
   const int64_t ntiles = (n + (int64_t)L.bt * L.ipt - 1) / ((int64_t)L.bt * L.ipt);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)nb * ctx->num_sms));
   timing_kernel_begin(ctx);
-  L.fn<<<grid, L.bt, dyn, st>>>(fa);
+  L.fn<<<grid, L.bt, 0, st>>>(fa);
   CRYS_LAUNCHED(std::string("fused ") + plan.name + " bt=" + std::to_string(L.bt) + " ipt=" +
-                std::to_string(L.ipt) + " grid=" + std::to_string(grid) + " smem=" + std::to_string(dyn));
+                std::to_string(L.ipt) + " grid=" + std::to_string(grid));
   timing_kernel_end(ctx);
   count_launch(ctx);
 }
 
+void ssb_query_partial(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt,
+                       unsigned long long* d_agg, unsigned long long* d_surv, int32_t* d_err) {
+  enqueue_query(ctx, db, qid, bt, ipt, d_agg, d_surv, d_err, nullptr, 0, false);
+}
+
 static void finalize_impl(crys_ctx* ctx, int qid, const unsigned long long* d_agg,
-                          const unsigned long long* d_surv, const int32_t* d_err, ResultRows* out) {
+                          const unsigned long long* d_surv, const int32_t* d_err, ResultRows* out,
+                          bool hdr_zeroed) {
   const QueryPlan& plan = plan_for(qid);
   QueryWorkspace& ws = ws_of(ctx);
   cudaStream_t st = ctx->stream;
@@ -916,7 +701,7 @@ static void finalize_impl(crys_ctx* ctx, int qid, const unsigned long long* d_ag
   ws.result.reserve(sizeof(ResultHeader) + sizeof(RowOut) * (size_t)cells);
   ResultHeader* hdr = ws.result.as<ResultHeader>();
   RowOut* rows = reinterpret_cast<RowOut*>(hdr + 1);
-  CUDA_TRY(cudaMemsetAsync(hdr, 0, sizeof(ResultHeader), st));
+  if (!hdr_zeroed) CUDA_TRY(cudaMemsetAsync(hdr, 0, sizeof(ResultHeader), st));
   const int tpb = 256;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((cells + tpb - 1) / tpb, (int64_t)ctx->num_sms * 8));
   finalize_kernel<<<grid, tpb, 0, st>>>(d_agg, d_agg + cells, cells, plan.joins.empty() ? 1 : 0, hdr,
@@ -952,30 +737,29 @@ static void finalize_impl(crys_ctx* ctx, int qid, const unsigned long long* d_ag
   if (ht_err == 1) fail(CRYS_EBUILD, "HashTable: key equals empty sentinel");
   if (ht_err == 2) fail(CRYS_EBUILD, "HashTable: duplicate key");
   if (ht_err == 3) fail(CRYS_EBUILD, "HashTable: capacity overflow");
+  if (ht_err == 4) fail(CRYS_ECONTRACT, "dimension key outside its column statistics");
   if (out->err) fail(CRYS_ECONTRACT, "group value outside its declared domain");
 }
 
 void ssb_finalize_device(crys_ctx* ctx, int qid, const unsigned long long* d_agg,
                          ResultRows* out) {
   ws_of(ctx).meta.reserve(sizeof(HtMeta) * kMaxJoins);
-  finalize_impl(ctx, qid, d_agg, nullptr, nullptr, out);
+  finalize_impl(ctx, qid, d_agg, nullptr, nullptr, out, false);
 }
 
 void ssb_run_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt, ResultRows* out) {
   const QueryPlan& plan = plan_for(qid);
   QueryWorkspace& ws = ws_of(ctx);
-  cudaStream_t st = ctx->stream;
   const int64_t cells = plan.cells();
-  ws.agg.reserve(sizeof(unsigned long long) * 2 * (size_t)cells);
-  ws.counters.reserve(64);
+  ws.agg.reserve(sizeof(unsigned long long) * (2 * (size_t)cells + 5));
+  ws.result.reserve(sizeof(ResultHeader) + sizeof(RowOut) * (size_t)cells);
   timing_begin(ctx);
-  CUDA_TRY(cudaMemsetAsync(ws.agg.p, 0, sizeof(unsigned long long) * 2 * (size_t)cells, st));
-  CUDA_TRY(cudaMemsetAsync(ws.counters.p, 0, 64, st));
   auto* agg = ws.agg.as<unsigned long long>();
-  auto* surv = ws.counters.as<unsigned long long>();
+  auto* surv = agg + 2 * cells;
   auto* err = reinterpret_cast<int32_t*>(surv + 4);
-  ssb_query_partial(ctx, db, qid, bt, ipt, agg, surv, err);
-  finalize_impl(ctx, qid, agg, surv, err, out);
+  enqueue_query(ctx, db, qid, bt, ipt, agg, surv, err, ws.result.as<unsigned long long>(),
+                sizeof(ResultHeader) / 8, true);
+  finalize_impl(ctx, qid, agg, surv, err, out, true);
   timing_end(ctx);
 }
 

@@ -1,7 +1,11 @@
-"""Run the given queries once for warm-up and once more (the profiled launch)."""
-import os, sys
+"""Run the given SSB queries twice each (warm-up + the profiled launch).
+
+    SF=20 python tools/profile_query.py 3 6 10      (query ids, all_query_ids order)"""
+import os
+import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2003_01178_b200 import tq
+from paper_2003_01178_b200 import tq  # noqa: E402
+
 sf = int(os.environ.get("SF", "20"))
 bt, ipt = map(int, os.environ.get("TILE", "256x16").split("x"))
 db = tq.DeviceDatabase.generate(sf, 42)
