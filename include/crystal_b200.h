@@ -99,6 +99,16 @@ crys_status crys_db_download_column(const crys_db* db, const char* table, const 
                                     int32_t* h_out, int64_t rows);
 void crys_db_free(crys_db* db);
 
+/* Microbenchmark inputs generated in HBM, bit-identical to the reference CLI's
+ * host generators: d_out[i] = Rng(seed, stream).uniform_i32(index0 + i, lo, hi)
+ * (random_i32, tools/tq_main.cpp:147-152; rng.hpp:23-35).  Asynchronous. */
+crys_status crys_fill_uniform_i32(crys_ctx* ctx, int32_t* d_out, int64_t n, uint64_t seed,
+                                  uint64_t stream, int64_t index0, int32_t lo, int32_t hi);
+/* d_x1[i] = uniform_float(2i, lo, hi), d_x2[i] = uniform_float(2i+1, lo, hi) of
+ * Rng(seed, stream) (the project inputs, tools/tq_main.cpp:335-340). Asynchronous. */
+crys_status crys_fill_float_pairs(crys_ctx* ctx, float* d_x1, float* d_x2, int64_t n, uint64_t seed,
+                                  uint64_t stream, float lo, float hi);
+
 /* ------------------------------------------------------------ SSB queries
  * qid: 0..12 = q11 q12 q13 q21 q22 q23 q31 q32 q33 q34 q41 q42 q43 (all_query_ids,
  * ssb_plans.cpp:301-306).  bt/ipt: TileConfig (tile.hpp:24-36). */

@@ -40,6 +40,10 @@ SIGNATURES = [
     ("crys_synchronize", C.c_int, [_P]),
     ("crys_kernel_launches", C.c_int64, [_P]),
     ("crys_db_generate", C.c_int, [_P, C.c_int64, C.c_uint64, C.c_int64, C.c_int64, C.POINTER(_P)]),
+    ("crys_fill_uniform_i32", C.c_int, [_P, _P, C.c_int64, C.c_uint64, C.c_uint64, C.c_int64,
+                                        C.c_int32, C.c_int32]),
+    ("crys_fill_float_pairs", C.c_int, [_P, _P, _P, C.c_int64, C.c_uint64, C.c_uint64, C.c_float,
+                                        C.c_float]),
     ("crys_db_create", C.c_int, [_P, C.c_int64, C.c_uint64, C.POINTER(_P)]),
     ("crys_db_upload_column", C.c_int, [_P, C.c_char_p, C.c_char_p, _P, C.c_int64]),
     ("crys_db_column", C.c_int, [_P, C.c_char_p, C.c_char_p, C.POINTER(_P), _I64P]),

@@ -240,6 +240,24 @@ crys_status crys_db_generate(crys_ctx* ctx, int64_t sf, uint64_t seed, int64_t l
   });
 }
 
+crys_status crys_fill_uniform_i32(crys_ctx* ctx, int32_t* d_out, int64_t n, uint64_t seed,
+                                  uint64_t stream, int64_t index0, int32_t lo, int32_t hi) {
+  return guarded([&] {
+    bind(ctx);
+    CRYS_CHECK(n == 0 || d_out, CRYS_ECONFIG, "null output");
+    crys::fill_uniform_i32(ctx, d_out, n, seed, stream, index0, lo, hi);
+  });
+}
+
+crys_status crys_fill_float_pairs(crys_ctx* ctx, float* d_x1, float* d_x2, int64_t n, uint64_t seed,
+                                  uint64_t stream, float lo, float hi) {
+  return guarded([&] {
+    bind(ctx);
+    CRYS_CHECK(n == 0 || (d_x1 && d_x2), CRYS_ECONFIG, "null output");
+    crys::fill_float_pairs(ctx, d_x1, d_x2, n, seed, stream, lo, hi);
+  });
+}
+
 crys_status crys_db_create(crys_ctx* ctx, int64_t sf, uint64_t seed, crys_db** out) {
   return guarded([&] {
     bind(ctx);

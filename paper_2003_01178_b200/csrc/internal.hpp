@@ -180,6 +180,10 @@ void timing_end(crys_ctx* c);  // synchronises and fills kernel_ms/total_ms when
 
 // Entry points implemented in the .cu files.
 void ssb_generate(crys_ctx* ctx, crys_db* db);
+void fill_uniform_i32(crys_ctx* ctx, int32_t* out, int64_t n, uint64_t seed, uint64_t stream,
+                      int64_t index0, int32_t lo, int32_t hi);
+void fill_float_pairs(crys_ctx* ctx, float* x1, float* x2, int64_t n, uint64_t seed, uint64_t stream,
+                      float lo, float hi);
 void ssb_query_partial(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt,
                        unsigned long long* d_agg, unsigned long long* d_surv, int32_t* d_err);
 struct ResultRows {

@@ -68,6 +68,19 @@ __global__ void gen_part_kernel(int32_t* key, int32_t* brand, int32_t* cat, int3
   }
 }
 
+// uniform_float (rng.hpp:37-40): x1[i] = at(2i), x2[i] = at(2i+1) of one stream
+// (the project microbenchmark inputs, tools/tq_main.cpp:335-340).
+__global__ void gen_float_pairs_kernel(float* __restrict__ x1, float* __restrict__ x2, int64_t n,
+                                       uint64_t base, float lo, float hi) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double u1 = (double)(mix64(base + (uint64_t)(2 * i)) >> 11) * 0x1.0p-53;
+    const double u2 = (double)(mix64(base + (uint64_t)(2 * i + 1)) >> 11) * 0x1.0p-53;
+    x1[i] = (float)((double)lo + u1 * ((double)hi - (double)lo));
+    x2[i] = (float)((double)lo + u2 * ((double)hi - (double)lo));
+  }
+}
+
 bool is_leap(int y) { return y % 4 == 0 && (y % 100 != 0 || y % 400 == 0); }
 
 // make_date_table (ssb_gen.cpp:60-90): a 2556-day calendar from 1992-01-01.
@@ -111,6 +124,30 @@ int grid_for(crys_ctx* ctx, int64_t n) {
 }
 
 }  // namespace
+
+// random_i32 of the reference CLI (tools/tq_main.cpp:147-152):
+// out[i] = Rng(seed, stream).uniform_i32(index0 + i, lo, hi).
+void fill_uniform_i32(crys_ctx* ctx, int32_t* out, int64_t n, uint64_t seed, uint64_t stream,
+                      int64_t index0, int32_t lo, int32_t hi) {
+  CRYS_CHECK(n >= 0 && index0 >= 0, CRYS_ECONFIG, "bad length");
+  CRYS_CHECK(lo <= hi, CRYS_ECONFIG, "uniform_i32 requires lo <= hi");
+  if (n == 0) return;
+  const uint64_t range = (uint64_t)((int64_t)hi - (int64_t)lo + 1);
+  gen_uniform_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(out, index0, n, rng_base(seed, stream, 0, 0),
+                                                                lo, range, nullptr);
+  CRYS_LAUNCHED("gen_uniform_kernel");
+  count_launch(ctx);
+}
+
+void fill_float_pairs(crys_ctx* ctx, float* x1, float* x2, int64_t n, uint64_t seed, uint64_t stream,
+                      float lo, float hi) {
+  CRYS_CHECK(n >= 0, CRYS_ECONFIG, "bad length");
+  if (n == 0) return;
+  gen_float_pairs_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(x1, x2, n, rng_base(seed, stream, 0, 0),
+                                                                    lo, hi);
+  CRYS_LAUNCHED("gen_float_pairs_kernel");
+  count_launch(ctx);
+}
 
 void ssb_generate(crys_ctx* ctx, crys_db* db) {
   const int64_t sf = db->sf;

@@ -362,6 +362,26 @@ class DeviceDatabase:
             pass
 
 
+def random_i32(out, seed: int, stream: int, lo: int, hi: int, index0: int = 0) -> None:
+    """Fill a CUDA int32 tensor with the reference CLI's random_i32 stream
+    (tools/tq_main.cpp:147-152): out[i] = Rng(seed, stream).uniform_i32(index0+i, lo, hi)."""
+    p, n = _dev(out, "int32")
+    ctx = _ctx_for(out)
+    check(LIB.crys_fill_uniform_i32(ctx.h, C.c_void_p(p), n, int(seed), int(stream), int(index0),
+                                    int(lo), int(hi)))
+
+
+def project_inputs(x1, x2, seed: int, stream: int = 2, lo: float = -4.0, hi: float = 4.0) -> None:
+    """The project microbenchmark inputs (tools/tq_main.cpp:335-340), in HBM."""
+    p1, n1 = _dev(x1, "float32")
+    p2, n2 = _dev(x2, "float32")
+    if n1 != n2:
+        raise ConfigError("project inputs: length mismatch")
+    ctx = _ctx_for(x1)
+    check(LIB.crys_fill_float_pairs(ctx.h, C.c_void_p(p1), C.c_void_p(p2), n1, int(seed), int(stream),
+                                    float(lo), float(hi)))
+
+
 def generate_ssb(sf: int, seed: int = 42, ctx: Optional[Context] = None) -> DeviceDatabase:
     return DeviceDatabase.generate(sf, seed, ctx=ctx)
 

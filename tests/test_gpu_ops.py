@@ -294,3 +294,30 @@ def test_sorts_2e28(env):
     assert np.array_equal(km, kc)
     assert np.array_equal(kh[pm], km)
     assert np.array_equal(np.bincount(pm, minlength=n), np.ones(n, np.int64))
+
+
+# ------------------------------------------------------------------ input generators
+
+@pytest.mark.parametrize("n,stream,lo,hi,index0", [(1, 1, 0, (1 << 20) - 1, 0), (100_003, 5, 1, 512, 7),
+                                                   (1 << 20, 6, -(2 ** 31) // 2, (2 ** 31 - 1) // 2, 0),
+                                                   (4097, 3, -(2 ** 31), 2 ** 31 - 1, 0)])
+def test_fill_uniform_i32_matches_reference_stream(env, n, stream, lo, hi, index0):
+    # random_i32 of the reference CLI (tools/tq_main.cpp:147-152) generated in HBM
+    torch, tq, orc = env
+    x = torch.empty(n + index0, dtype=torch.int32, device="cuda")
+    tq.random_i32(x, 42, stream, lo, hi)
+    exp = orc.random_i32(n + index0, 42, stream, lo, hi)
+    assert np.array_equal(x.cpu().numpy(), exp)
+    y = torch.empty(n, dtype=torch.int32, device="cuda")
+    tq.random_i32(y, 42, stream, lo, hi, index0=index0)
+    assert np.array_equal(y.cpu().numpy(), exp[index0:])
+
+
+def test_project_inputs_match_reference_stream(env):
+    torch, tq, orc = env
+    n = 100_001
+    x1 = torch.empty(n, dtype=torch.float32, device="cuda")
+    x2 = torch.empty_like(x1)
+    tq.project_inputs(x1, x2, 42)
+    e1, e2 = orc.project_inputs(n, 42)
+    assert np.array_equal(x1.cpu().numpy(), e1) and np.array_equal(x2.cpu().numpy(), e2)
