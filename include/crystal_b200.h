@@ -75,6 +75,14 @@ crys_status crys_synchronize(crys_ctx* ctx);
 /* Number of kernels this ctx launched since creation (telemetry for bench). */
 int64_t crys_kernel_launches(const crys_ctx* ctx);
 
+/* Device memory for host code that has no CUDA headers (the C++ drop-in layer
+ * under dropin/): allocations are 256 B aligned with 256 B of slack. Copies are
+ * synchronous with respect to the host. */
+crys_status crys_device_alloc(crys_ctx* ctx, size_t bytes, void** d_out);
+void crys_device_free(crys_ctx* ctx, void* d_ptr);
+crys_status crys_copy_to_device(crys_ctx* ctx, void* d_dst, const void* h_src, size_t bytes);
+crys_status crys_copy_to_host(crys_ctx* ctx, void* h_dst, const void* d_src, size_t bytes);
+
 /* ------------------------------------------------------------ database
  * An HBM-resident SSB database (columnar int32).  Lineorder may be a row-range
  * SHARD [lo_begin, lo_end) of the full fact table; dimensions are always whole
@@ -176,6 +184,12 @@ crys_status crys_ht_download(const crys_ht* ht, int32_t* h_keys, int32_t* h_payl
 int64_t crys_ht_capacity(const crys_ht* ht);
 void crys_ht_free(crys_ht* ht);
 
+/* A device table from existing slot arrays (a host-built tq::HashTable, whose
+ * slot_keys()/slot_payloads() are exposed at hash_table.hpp:53-54): capacity
+ * a power of two >= 2, empty slots hold INT32_MIN. */
+crys_status crys_ht_upload(crys_ctx* ctx, const int32_t* h_keys, const int32_t* h_payloads,
+                           int64_t capacity, crys_ht** out);
+
 /* Replaces join_probe_{scalar,prefetch,tile} (join.hpp:17-32, join.cpp:53-96):
  * *checksum = sum over hits of (build payload + probe payload), int64. */
 crys_status crys_join_probe_sum(crys_ctx* ctx, const int32_t* d_keys, const int32_t* d_payloads,
@@ -186,6 +200,18 @@ crys_status crys_join_probe_sum(crys_ctx* ctx, const int32_t* d_keys, const int3
  * (== std::stable_sort by key).  MSB: keys ascending, pairs preserved. */
 crys_status crys_sort_pairs(crys_ctx* ctx, int32_t* d_keys, int32_t* d_payloads, int64_t n,
                             int algo, int bits_per_pass);
+
+/* Replaces radix_histogram (radix.hpp:77-78, radix.cpp:33-53): h_counts =
+ * int64[num_owners][2^num_bits], owner o = input chunk [o*chunk, (o+1)*chunk),
+ * chunk = max(1, ceil(n / num_owners)); digit = radix_digit (radix.hpp:44-47). */
+crys_status crys_radix_histogram(crys_ctx* ctx, const int32_t* d_keys, int64_t n, int start_bit,
+                                 int num_bits, int64_t num_owners, int64_t* h_counts);
+/* Replaces radix_shuffle with a stable pass (radix.hpp:80-83, radix.cpp:75-136):
+ * d_out_* = the input stably partitioned by digit (what per-owner cursors over
+ * column-major offsets produce for ANY owner count).  Out-of-place. */
+crys_status crys_radix_partition(crys_ctx* ctx, const int32_t* d_keys, const int32_t* d_payloads,
+                                 int64_t n, int start_bit, int num_bits, int32_t* d_out_keys,
+                                 int32_t* d_out_payloads);
 
 /* ------------------------------------------------------------ timing hooks
  * Device-timed (CUDA events on the ctx stream) duration of the last call's

@@ -40,6 +40,10 @@ SIGNATURES = [
     ("crys_synchronize", C.c_int, [_P]),
     ("crys_kernel_launches", C.c_int64, [_P]),
     ("crys_db_generate", C.c_int, [_P, C.c_int64, C.c_uint64, C.c_int64, C.c_int64, C.POINTER(_P)]),
+    ("crys_device_alloc", C.c_int, [_P, C.c_size_t, C.POINTER(_P)]),
+    ("crys_device_free", None, [_P, _P]),
+    ("crys_copy_to_device", C.c_int, [_P, _P, _P, C.c_size_t]),
+    ("crys_copy_to_host", C.c_int, [_P, _P, _P, C.c_size_t]),
     ("crys_fill_uniform_i32", C.c_int, [_P, _P, C.c_int64, C.c_uint64, C.c_uint64, C.c_int64,
                                         C.c_int32, C.c_int32]),
     ("crys_fill_float_pairs", C.c_int, [_P, _P, _P, C.c_int64, C.c_uint64, C.c_uint64, C.c_float,
@@ -60,11 +64,14 @@ SIGNATURES = [
     ("crys_project_f32", C.c_int, [_P, _P, _P, C.c_int64, C.c_float, C.c_float, _P, C.c_int,
                                    C.c_int, C.c_int]),
     ("crys_ht_build", C.c_int, [_P, _P, _P, C.c_int64, C.c_int64, C.POINTER(_P)]),
+    ("crys_ht_upload", C.c_int, [_P, _P, _P, C.c_int64, C.POINTER(_P)]),
     ("crys_ht_download", C.c_int, [_P, _P, _P]),
     ("crys_ht_capacity", C.c_int64, [_P]),
     ("crys_ht_free", None, [_P]),
     ("crys_join_probe_sum", C.c_int, [_P, _P, _P, C.c_int64, _P, C.c_int, C.c_int, _I64P]),
     ("crys_sort_pairs", C.c_int, [_P, _P, _P, C.c_int64, C.c_int, C.c_int]),
+    ("crys_radix_histogram", C.c_int, [_P, _P, C.c_int64, C.c_int, C.c_int, C.c_int64, _P]),
+    ("crys_radix_partition", C.c_int, [_P, _P, _P, C.c_int64, C.c_int, C.c_int, _P, _P]),
     ("crys_last_timing", C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     ("crys_enable_timing", C.c_int, [_P, C.c_int]),
 ]

@@ -208,11 +208,72 @@ crys_status crys_enable_timing(crys_ctx* ctx, int enable) {
   });
 }
 
+crys_status crys_radix_histogram(crys_ctx* ctx, const int32_t* d_keys, int64_t n, int start_bit,
+                                 int num_bits, int64_t num_owners, int64_t* h_counts) {
+  return guarded([&] {
+    bind(ctx);
+    CRYS_CHECK(h_counts && n >= 0 && (n == 0 || d_keys), CRYS_ECONFIG, "bad argument");
+    crys::radix_owner_histogram(ctx, d_keys, n, start_bit, num_bits, num_owners, h_counts);
+  });
+}
+
+crys_status crys_radix_partition(crys_ctx* ctx, const int32_t* d_keys, const int32_t* d_payloads,
+                                 int64_t n, int start_bit, int num_bits, int32_t* d_out_keys,
+                                 int32_t* d_out_payloads) {
+  return guarded([&] {
+    bind(ctx);
+    CRYS_CHECK(n >= 0 && (n == 0 || (d_keys && d_payloads && d_out_keys && d_out_payloads)),
+               CRYS_ECONFIG, "bad argument");
+    crys::timing_begin(ctx);
+    crys::radix_partition_pass(ctx, d_keys, d_payloads, d_out_keys, d_out_payloads, n, start_bit, num_bits);
+    crys::timing_end(ctx);
+  });
+}
+
 crys_status crys_last_timing(const crys_ctx* ctx, double* kernel_ms, double* total_ms) {
   return guarded([&] {
     CRYS_CHECK(ctx != nullptr, CRYS_ECONFIG, "null context");
     if (kernel_ms) *kernel_ms = ctx->kernel_ms;
     if (total_ms) *total_ms = ctx->total_ms;
+  });
+}
+
+// ---------------------------------------------------------------- device memory
+
+crys_status crys_device_alloc(crys_ctx* ctx, size_t bytes, void** d_out) {
+  return guarded([&] {
+    bind(ctx);
+    CRYS_CHECK(d_out != nullptr, CRYS_ECONFIG, "null output");
+    void* p = nullptr;
+    CUDA_TRY(cudaMalloc(&p, bytes + 256));
+    *d_out = p;
+  });
+}
+
+void crys_device_free(crys_ctx* ctx, void* d_ptr) {
+  if (!ctx || !d_ptr) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  cudaFree(d_ptr);
+}
+
+crys_status crys_copy_to_device(crys_ctx* ctx, void* d_dst, const void* h_src, size_t bytes) {
+  return guarded([&] {
+    bind(ctx);
+    if (bytes == 0) return;
+    CRYS_CHECK(d_dst && h_src, CRYS_ECONFIG, "null argument");
+    CUDA_TRY(cudaMemcpyAsync(d_dst, h_src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+crys_status crys_copy_to_host(crys_ctx* ctx, void* h_dst, const void* d_src, size_t bytes) {
+  return guarded([&] {
+    bind(ctx);
+    if (bytes == 0) return;
+    CRYS_CHECK(h_dst && d_src, CRYS_ECONFIG, "null argument");
+    CUDA_TRY(cudaMemcpyAsync(h_dst, d_src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   });
 }
 
@@ -497,6 +558,40 @@ crys_status crys_ht_build(crys_ctx* ctx, const int32_t* d_keys, const int32_t* d
     try {
       ht->slots.reserve(sizeof(int2) * (size_t)capacity);
       crys::ht_build(ctx, ht, d_keys, d_payloads, n);
+    } catch (...) {
+      delete ht;
+      throw;
+    }
+    *out = ht;
+  });
+}
+
+crys_status crys_ht_upload(crys_ctx* ctx, const int32_t* h_keys, const int32_t* h_payloads,
+                           int64_t capacity, crys_ht** out) {
+  return guarded([&] {
+    bind(ctx);
+    CRYS_CHECK(out != nullptr, CRYS_ECONFIG, "null output handle");
+    CRYS_CHECK(capacity >= 2 && (capacity & (capacity - 1)) == 0 && capacity <= (1LL << 31),
+               CRYS_ECONFIG, "HashTable: capacity must be a power of two >= 2");
+    CRYS_CHECK(h_keys && h_payloads, CRYS_ECONFIG, "null argument");
+    std::vector<int2> v((size_t)capacity);
+    int64_t size = 0;
+    for (size_t i = 0; i < v.size(); ++i) {
+      v[i] = make_int2(h_keys[i], h_payloads[i]);
+      size += h_keys[i] != crys::kEmptyKey;
+    }
+    auto* ht = new crys_ht();
+    ht->ctx = ctx;
+    ht->capacity = capacity;
+    int lg = 0;
+    while ((1LL << lg) < capacity) ++lg;
+    ht->shift = 32 - lg;
+    ht->size = size;
+    try {
+      ht->slots.reserve(sizeof(int2) * (size_t)capacity);
+      CUDA_TRY(cudaMemcpyAsync(ht->slots.p, v.data(), sizeof(int2) * v.size(), cudaMemcpyHostToDevice,
+                               ctx->stream));
+      CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     } catch (...) {
       delete ht;
       throw;

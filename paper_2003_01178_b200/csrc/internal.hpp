@@ -208,5 +208,9 @@ int64_t join_probe_sum(crys_ctx* ctx, const int32_t* d_keys, const int32_t* d_pa
                        const crys_ht* ht);
 void sort_pairs(crys_ctx* ctx, int32_t* d_keys, int32_t* d_payloads, int64_t n, int algo,
                 int bits_per_pass);
+void radix_owner_histogram(crys_ctx* ctx, const int32_t* d_keys, int64_t n, int start, int bits,
+                           int64_t num_owners, int64_t* h_counts);
+void radix_partition_pass(crys_ctx* ctx, const int32_t* sk, const int32_t* sp, int32_t* dk, int32_t* dp,
+                          int64_t n, int start, int bits);
 
 }  // namespace crys

@@ -254,6 +254,31 @@ __global__ void __launch_bounds__(kLocalBT) local_sort_kernel(int32_t* keys, int
   }
 }
 
+// radix_histogram (radix.cpp:33-53): counts[owner][digit], owner = the
+// contiguous chunk [o*chunk, (o+1)*chunk).  Per tile a shared histogram for
+// each owner the tile overlaps, flushed with 64-bit atomics.
+constexpr int kHistTile = 8192;
+__global__ void __launch_bounds__(256) owner_hist_kernel(const int32_t* __restrict__ keys, int64_t n,
+                                                         int64_t chunk, int start, int bits,
+                                                         unsigned long long* counts) {
+  __shared__ uint32_t h[256];
+  const int D = 1 << bits;
+  const uint32_t mask = (uint32_t)D - 1;
+  for (int64_t t0 = (int64_t)blockIdx.x * kHistTile; t0 < n; t0 += (int64_t)gridDim.x * kHistTile) {
+    const int64_t t1 = min(n, t0 + kHistTile);
+    for (int64_t o = t0 / chunk; o * chunk < t1; ++o) {
+      const int64_t b = max(t0, o * chunk), e = min(t1, (o + 1) * chunk);
+      for (int d = threadIdx.x; d < D; d += blockDim.x) h[d] = 0;
+      __syncthreads();
+      for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) atomicAdd(&h[digit_of(keys[i], start, mask)], 1u);
+      __syncthreads();
+      for (int d = threadIdx.x; d < D; d += blockDim.x)
+        if (h[d]) atomicAdd(&counts[o * D + d], (unsigned long long)h[d]);
+      __syncthreads();
+    }
+  }
+}
+
 __global__ void copy_pairs_kernel(const int32_t* ks, const int32_t* ps, int32_t* kd, int32_t* pd,
                                   const SegLocal* segs) {
   const SegLocal s = segs[blockIdx.y];
@@ -445,6 +470,47 @@ void msb_sort(crys_ctx* ctx, SortWorkspace& ws, int32_t* keys, int32_t* pays, in
 }
 
 }  // namespace
+
+void radix_owner_histogram(crys_ctx* ctx, const int32_t* d_keys, int64_t n, int start, int bits,
+                           int64_t num_owners, int64_t* h_counts) {
+  CRYS_CHECK(bits >= 1 && bits <= 8 && start >= 0 && start + bits <= 32, CRYS_ECONFIG,
+             "RadixPass: bit range exceeds 32-bit keys");
+  CRYS_CHECK(num_owners >= 1, CRYS_ECONFIG, "radix_histogram: need at least one owner");
+  cudaStream_t st = ctx->stream;
+  if (!ctx->sws) ctx->sws.reset(new SortWorkspace());
+  SortWorkspace& ws = *ctx->sws;
+  const int D = 1 << bits;
+  int64_t chunk = (n + num_owners - 1) / num_owners;
+  if (chunk == 0) chunk = 1;
+  const size_t cells = (size_t)num_owners * D;
+  ws.hist.reserve(sizeof(unsigned long long) * cells);
+  CUDA_TRY(cudaMemsetAsync(ws.hist.p, 0, sizeof(unsigned long long) * cells, st));
+  if (n > 0) {
+    const int grid = (int)std::min<int64_t>((n + kHistTile - 1) / kHistTile, (int64_t)ctx->num_sms * 8);
+    owner_hist_kernel<<<grid, 256, 0, st>>>(d_keys, n, chunk, start, bits, ws.hist.as<unsigned long long>());
+    CRYS_LAUNCHED("owner_hist_kernel");
+    count_launch(ctx);
+  }
+  CUDA_TRY(cudaMemcpyAsync(h_counts, ws.hist.p, sizeof(int64_t) * cells, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+}
+
+// One stable partition pass (radix_shuffle with pass.stable, radix.cpp:75-136):
+// the output of per-owner cursors over column-major offsets is exactly the
+// stable partition by digit, independent of the owner count.
+void radix_partition_pass(crys_ctx* ctx, const int32_t* sk, const int32_t* sp, int32_t* dk, int32_t* dp,
+                          int64_t n, int start, int bits) {
+  CRYS_CHECK(bits >= 1 && bits <= 8 && start >= 0 && start + bits <= 32, CRYS_ECONFIG,
+             "RadixPass: bit range exceeds 32-bit keys");
+  if (n == 0) return;
+  CRYS_CHECK(n < (1LL << 32), CRYS_ENOTBUILT, "partition supports fewer than 2^32 pairs");
+  if (!ctx->sws) ctx->sws.reset(new SortWorkspace());
+  std::vector<SegLocal> one{{0, n}};
+  timing_kernel_begin(ctx);
+  radix_pass(ctx, *ctx->sws, sk, sp, dk, dp, one, start, bits, nullptr);
+  timing_kernel_end(ctx);
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+}
 
 void sort_pairs(crys_ctx* ctx, int32_t* d_keys, int32_t* d_payloads, int64_t n, int algo,
                 int bits_per_pass) {

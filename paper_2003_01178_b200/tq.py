@@ -257,14 +257,41 @@ class ResultRow:
     sum: int
 
 
-@dataclass
 class QueryResult:
-    """ssb_queries.hpp:52-62: rows sorted by group (lexicographic)."""
-    group_labels: List[str] = field(default_factory=list)
-    rows: List[ResultRow] = field(default_factory=list)
+    """ssb_queries.hpp:52-62: rows sorted by group (lexicographic).
+
+    Backed by two arrays straight from the C ABI (``groups`` int32[n, arity],
+    ``sums`` int64[n]); ``rows`` materialises ResultRow objects on first use."""
+
+    def __init__(self, group_labels=None, rows=None, groups=None, sums=None):
+        self.group_labels = list(group_labels or [])
+        if rows is not None:
+            self._rows = list(rows)
+            self.groups = np.array([r.group for r in self._rows], np.int32).reshape(len(self._rows), -1)
+            self.sums = np.array([r.sum for r in self._rows], np.int64)
+        else:
+            self._rows = None
+            self.groups = groups if groups is not None else np.zeros((0, len(self.group_labels)), np.int32)
+            self.sums = sums if sums is not None else np.zeros(0, np.int64)
+
+    def __len__(self) -> int:
+        return len(self.sums)
+
+    @property
+    def rows(self) -> List[ResultRow]:
+        if self._rows is None:
+            self._rows = [ResultRow(tuple(int(x) for x in g), int(v)) for g, v in
+                          zip(self.groups.tolist(), self.sums.tolist())]
+        return self._rows
+
+    @rows.setter
+    def rows(self, value) -> None:
+        self._rows = list(value)
 
     def as_tuples(self) -> List[Tuple[Tuple[int, ...], int]]:
-        return [(tuple(r.group), int(r.sum)) for r in self.rows]
+        if self._rows is not None:
+            return [(tuple(r.group), int(r.sum)) for r in self._rows]
+        return [(tuple(g), v) for g, v in zip(self.groups.tolist(), self.sums.tolist())]
 
 
 @dataclass
@@ -389,8 +416,18 @@ def generate_ssb(sf: int, seed: int = 42, ctx: Optional[Context] = None) -> Devi
 def _rows_from_buffers(qid, groups, sums, n) -> QueryResult:
     labels = _GROUP_LABELS[int(qid)]
     ng = len(labels)
-    rows = [ResultRow(tuple(int(x) for x in groups[3 * i:3 * i + ng]), int(sums[i])) for i in range(n)]
-    return QueryResult(list(labels), rows)
+    g = np.ascontiguousarray(groups[:3 * n].reshape(n, 3)[:, :ng]) if n else np.zeros((0, ng), np.int32)
+    return QueryResult(list(labels), groups=g, sums=np.array(sums[:n], np.int64))
+
+
+_SHAPES: Dict[int, Tuple[int, int, int]] = {}
+
+
+def _shape(qid: int) -> Tuple[int, int, int]:
+    sh = _SHAPES.get(qid)
+    if sh is None:
+        sh = _SHAPES[qid] = query_shape(qid)
+    return sh
 
 
 def run_query(db, qid, config: TileConfig = TileConfig(), workers: int = 1,
@@ -404,10 +441,10 @@ def run_query(db, qid, config: TileConfig = TileConfig(), workers: int = 1,
     if workers < 1:
         raise ConfigError("run_query: workers must be >= 1")
     qid = int(qid)
-    cells, ng, nj = query_shape(qid)
+    cells, ng, nj = _shape(qid)
     maxr = max(cells, 1)
-    groups = np.zeros(3 * maxr, np.int32)
-    sums = np.zeros(maxr, np.int64)
+    groups = np.empty(3 * maxr, np.int32)  # untouched pages cost nothing; only n rows are written
+    sums = np.empty(maxr, np.int64)
     surv = np.zeros(4, np.int64)
     n = C.c_int64()
     if isinstance(db, DeviceDatabase):
