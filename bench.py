@@ -48,6 +48,23 @@ def fact_bytes(q, rows):
     return 4 * FACT_COLS[q] * rows
 
 
+def ncu_traffic():
+    """DRAM traffic of the 13 fused lineorder launches from the committed
+    `ncu --set full` capture (profiles/*_suite_traffic.json, newest round):
+    mean dram__bytes_read.sum + dram__bytes_write.sum per launch."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_suite_traffic.json")))
+    if not files:
+        return None, None
+    with open(files[-1]) as f:
+        d = json.load(f)
+    L = d["launches"]
+    if len(L) != 13:
+        return None, None
+    per = [x["dram_read"] + x["dram_write"] for x in L]
+    return sum(per) / 13.0, os.path.relpath(files[-1], ROOT)
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -314,60 +331,89 @@ def run_ours(args, rank, world):
             line["fused_kernel_ms"] = dict(zip(QUERY_NAMES, [round(x, 4) for x in kern_ms]))
             alg = sum(fact_bytes(q, rows_total) for q in range(13))
             achieved = alg / (sum(kern_ms) * 1e-3) / 1e9
+            traffic, tsrc = ncu_traffic()
             line["roofline"] = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
                                 "unit": "GB/s", "frac": round(achieved / hbm, 4),
-                                "traffic": None, "peak_kind": peak_kind,
-                                "kernel": "ssb_flight1_kernel / ssb_join_kernel (fused lineorder pass)",
+                                "traffic": round(traffic) if traffic else None,
+                                "traffic_source": tsrc,
+                                "algorithmic_bytes_per_launch": round(alg / 13),
+                                "peak_kind": peak_kind,
+                                "kernel": "ssb_flight1_kernel / ssb_pipeline_kernel (fused lineorder pass)",
                                 "algorithmic_bytes": "4 B x referenced fact columns x lineorder rows "
                                                      "(16 B/row q1-q3, 24 B/row q4), summed over the 13 launches"}
         out = line
     return out, sh, sf
 
 
+def suite_upload_order():
+    """(table, column) of every column the 13 plans read, in first-use order,
+    so the suite's first queries overlap the upload of later queries' columns."""
+    order = []
+    for q in range(13):
+        for t, cols in host_columns_needed(q).items():
+            for c in cols:
+                if (t, c) not in order:
+                    order.append((t, c))
+    # dimension columns are tiny: put each query's before its fact columns
+    return order
+
+
 def e2e_host(args, sh, sf):
-    """Same metric through the C ABI with HOST (pinned) columns: every query
-    copies its referenced columns H2D and its result D2H inside the timed region."""
+    """Same metric through the C ABI with HOST (pinned) columns.  Each step is
+    what a user holding a host-resident `SsbDatabase` does: the columns the
+    suite reads are copied H2D (crys_db_upload_host: one DMA per column on a
+    copy stream, per-column ready events) and the 13 queries run as their
+    columns land, each returning its rows D2H (crys_run_query).  Every step
+    re-copies every column; nothing is cached across steps."""
     import torch
     from paper_2003_01178_b200 import tq
     cfg = tq.TileConfig(args.bt, args.ipt)
+    order = suite_upload_order()
     host = {}
-    for t, cols in [("lineorder", tq.LO_COLS)] + list(tq.DIM_COLS.items()):
-        host[t] = {}
-        for c in cols:
-            a = sh.db.download(t, c)
-            pt = torch.empty(len(a), dtype=torch.int32, pin_memory=True)
-            pt.numpy()[:] = a
-            host[t][c] = pt.numpy()
-    h2d = 0
-    for q in range(13):
-        for t, cols in host_columns_needed(q).items():
-            for c in set(cols):
-                h2d += 4 * len(host[t][c])
+    for t, c in order:
+        a = sh.db.download(t, c)
+        pt = torch.empty(len(a), dtype=torch.int32, pin_memory=True)
+        pt.numpy()[:] = a
+        host.setdefault(t, {})[c] = pt.numpy()
+    h2d = sum(4 * len(host[t][c]) for t, c in order)
     d2h = 0
     for q in range(13):
         cells = tq.query_shape(q)[0]
         d2h += 64 + 16 * min(cells, 2048)
     ctx = sh.ctx
-    for _ in range(1):
+    staging = tq.DeviceDatabase.from_host({}, ctx=ctx, sf=sf, seed=42)
+    ctx.bind_torch_stream()
+
+    def step():
+        staging.upload_host(host, order)
+        out = None
         for q in range(13):
-            tq.run_query(host, q, cfg, ctx=ctx)
+            out = tq.run_query(staging, q, cfg)
+        return out
+
+    for _ in range(2):
+        step()
     torch.cuda.synchronize()
-    steps = max(1, min(args.steps, 3))
+    steps = max(1, min(args.steps, 5))
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    ctx.bind_torch_stream()
+    w0 = time.perf_counter()
     e0.record()
     for _ in range(steps):
-        for q in range(13):
-            tq.run_query(host, q, cfg, ctx=ctx)
+        step()
     e1.record()
     torch.cuda.synchronize()
+    wall = (time.perf_counter() - w0) * 1e3 / steps
     ms_step = e0.elapsed_time(e1) / steps
+    staging.free()
     rows = 6_000_000 * sf
     total = sum(fact_bytes(q, rows) for q in range(13))
     return {"value": round(total / (ms_step * 1e-3) / 1e9, 3), "unit": "GB/s",
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "ms_per_step": round(ms_step, 3), "steps": steps}
+            "ms_per_step": round(ms_step, 3), "wall_ms_per_step": round(wall, 3), "steps": steps,
+            "h2d_gbs": round(h2d / (ms_step * 1e-3) / 1e9, 2),
+            "path": "crys_db_upload_host (pinned host columns, one H2D per referenced column per "
+                    "step, copy stream + per-column events) + 13 x crys_run_query (rows D2H)"}
 
 
 def main():

@@ -99,6 +99,21 @@ crys_status crys_db_create(crys_ctx* ctx, int64_t sf, uint64_t seed, crys_db** o
 /* Copy one host column into HBM (replacing any previous one of that name). */
 crys_status crys_db_upload_column(crys_db* db, const char* table, const char* column,
                                   const int32_t* h_data, int64_t rows);
+typedef struct {
+  const char* table;
+  const char* column;
+  const int32_t* h_data;
+  int64_t rows;
+} crys_host_column;
+/* Asynchronous bulk upload of HOST columns (the reference's host-resident
+ * `const SsbDatabase&`, ssb_gen.hpp): every copy is issued in array order on
+ * the context's copy stream (pinned host memory makes it a true DMA), each
+ * column gets a ready event, and work enqueued later on the compute stream
+ * waits only for the columns it reads -- so a query suite overlaps its first
+ * queries with the upload of the columns later queries need.  Dimension
+ * statistics are computed on the host while the DMA runs.  The host arrays
+ * must stay alive until the queries that read them have completed. */
+crys_status crys_db_upload_host(crys_db* db, const crys_host_column* cols, int ncols);
 /* Device pointer + rows of a column (borrowed; valid until the db is freed). */
 crys_status crys_db_column(const crys_db* db, const char* table, const char* column,
                            const int32_t** d_data, int64_t* rows);
@@ -138,12 +153,6 @@ crys_status crys_run_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, in
 /* End-to-end variant over HOST columns (the reference's `const SsbDatabase&`):
  * the query's referenced columns are copied H2D inside the call, then as
  * crys_run_query.  Tables are described by parallel arrays of names/pointers. */
-typedef struct {
-  const char* table;
-  const char* column;
-  const int32_t* h_data;
-  int64_t rows;
-} crys_host_column;
 crys_status crys_run_query_host(crys_ctx* ctx, const crys_host_column* cols, int ncols, int qid,
                                 int bt, int ipt, int32_t* h_groups, int64_t* h_sums,
                                 int64_t max_rows, int64_t* nrows, int64_t* h_survivors);

@@ -47,14 +47,27 @@ crys_ctx::~crys_ctx() {
   qws.reset();
   sws.reset();
   delete staging;
+  if (copy_stream) cudaStreamDestroy(copy_stream);
   if (own_stream) cudaStreamDestroy(own_stream);
+}
+
+crys_db::~crys_db() {
+  for (auto& kv : cols)
+    if (kv.second.ready) cudaEventDestroy(kv.second.ready);
 }
 
 const int32_t* crys_db::col(const std::string& table, const std::string& column, int64_t* rows) const {
   auto it = cols.find(table + "." + column);
   CRYS_CHECK(it != cols.end(), CRYS_ECONTRACT, "table " + table + ": no column " + column);
   if (rows) *rows = it->second.rows;
-  return it->second.buf->as<int32_t>();
+  const Col& c = it->second;
+  if (c.pending) {  // column still in flight from crys_db_upload_host
+    if (cudaEventQuery(c.ready) == cudaSuccess)
+      c.pending = false;
+    else
+      CUDA_TRY(cudaStreamWaitEvent(ctx->stream, c.ready, 0));
+  }
+  return c.buf->as<int32_t>();
 }
 
 bool crys_db::col_range(const std::string& table, const std::string& column, int32_t* lo,
@@ -350,6 +363,48 @@ crys_status crys_db_upload_column(crys_db* db, const char* table, const char* co
       db->lo_begin = 0;
       db->lo_end = rows;
     }
+  });
+}
+
+crys_status crys_db_upload_host(crys_db* db, const crys_host_column* cols, int ncols) {
+  return guarded([&] {
+    CRYS_CHECK(db && (ncols == 0 || cols), CRYS_ECONFIG, "null argument");
+    crys_ctx* ctx = db->ctx;
+    bind(ctx);
+    if (!ctx->copy_stream) CUDA_TRY(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    // WAR: work already queued on the compute stream may still read the
+    // previous contents of these buffers
+    cudaEvent_t fence;
+    CUDA_TRY(cudaEventCreateWithFlags(&fence, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(fence, ctx->stream));
+    CUDA_TRY(cudaStreamWaitEvent(ctx->copy_stream, fence, 0));
+    CUDA_TRY(cudaEventDestroy(fence));
+    std::vector<crys_db::Col*> issued((size_t)ncols, nullptr);
+    for (int i = 0; i < ncols; ++i) {  // issue every copy first, in the caller's order
+      const crys_host_column& hc = cols[i];
+      CRYS_CHECK(hc.table && hc.column, CRYS_ECONFIG, "null column name");
+      CRYS_CHECK(hc.rows >= 0 && (hc.rows == 0 || hc.h_data), CRYS_ECONFIG, "bad column data");
+      auto& c = db->cols[std::string(hc.table) + "." + hc.column];
+      if (!c.buf) c.buf.reset(new crys::DevBuf());
+      if (sizeof(int32_t) * (size_t)std::max<int64_t>(hc.rows, 1) > c.buf->bytes) {
+        CUDA_TRY(cudaStreamSynchronize(ctx->copy_stream));
+        c.buf->reserve(sizeof(int32_t) * (size_t)std::max<int64_t>(hc.rows, 1));
+      }
+      c.rows = hc.rows;
+      if (!c.ready) CUDA_TRY(cudaEventCreateWithFlags(&c.ready, cudaEventDisableTiming));
+      if (hc.rows)
+        CUDA_TRY(cudaMemcpyAsync(c.buf->p, hc.h_data, sizeof(int32_t) * (size_t)hc.rows,
+                                 cudaMemcpyHostToDevice, ctx->copy_stream));
+      CUDA_TRY(cudaEventRecord(c.ready, ctx->copy_stream));
+      c.pending = true;
+      issued[(size_t)i] = &c;
+      if (std::string(hc.table) == "lineorder") {
+        db->lo_begin = 0;
+        db->lo_end = hc.rows;
+      }
+    }
+    // dimension statistics on the host while the DMA runs
+    for (int i = 0; i < ncols; ++i) host_stats(*issued[(size_t)i], cols[i].table, cols[i].h_data, cols[i].rows);
   });
 }
 

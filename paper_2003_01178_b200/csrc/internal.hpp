@@ -133,6 +133,7 @@ struct crys_ctx {
   std::unique_ptr<crys::QueryWorkspace, crys::WsDeleter> qws;
   std::unique_ptr<crys::SortWorkspace, crys::WsDeleter> sws;
   crys_db* staging = nullptr;  // device copies for crys_run_query_host
+  cudaStream_t copy_stream = nullptr;  // H2D of crys_db_upload_host (lazy)
   ~crys_ctx();
 };
 
@@ -148,12 +149,18 @@ struct crys_db {
     // exact key-range membership bitmaps of the SSB dimension builds
     bool stats = false;
     int32_t vmin = 0, vmax = -1;
+    // asynchronous host upload (crys_db_upload_host): the copy stream records
+    // `ready` after this column's H2D; consumers on the compute stream wait on
+    // it per column, so a query starts as soon as ITS columns have landed
+    mutable cudaEvent_t ready = nullptr;
+    mutable bool pending = false;
   };
   std::map<std::string, Col> cols;  // "table.column"
   const int32_t* col(const std::string& table, const std::string& column, int64_t* rows) const;
   // false when the column carries no statistics
   bool col_range(const std::string& table, const std::string& column, int32_t* lo, int32_t* hi) const;
   int64_t table_rows(const std::string& table) const;
+  ~crys_db();
 };
 
 struct crys_ht {

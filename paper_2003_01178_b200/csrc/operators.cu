@@ -29,114 +29,150 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
+// Input-order selection: persistent CTAs walk tiles blockIdx.x, +gridDim.x,
+// ...; the NEXT tile's 128-bit loads are issued before the current tile's
+// scan + decoupled look-back, so HBM reads overlap the serial part.  Every
+// CTA is resident and walks its tiles in increasing order, so each tile's
+// predecessors are always in progress or done (no look-back deadlock).
 template <int BT, int IPT>
 __global__ void __launch_bounds__(BT) select_input_kernel(const int32_t* __restrict__ in, int64_t n,
                                                           int32_t lo, int32_t hi,
                                                           int32_t* __restrict__ out,
                                                           unsigned long long* status,
-                                                          unsigned long long* tile_counter,
-                                                          long long* total_out) {
+                                                          long long ntiles, long long* total_out) {
   using L = VecLayout<BT, IPT>;
   static_assert(L::NV <= 4 && BT * L::VEC < 65536, "packed 16-bit per-vector counts");
   __shared__ int32_t s_items[L::TILE];
   __shared__ unsigned long long s_scan[BT / 32 + 1];
-  __shared__ long long s_tile, s_off;
-  if (threadIdx.x == 0) s_tile = (long long)atomicAdd(tile_counter, 1ull);
-  __syncthreads();
-  const long long tile = s_tile;
-  const int64_t base = tile * L::TILE;
-  const int valid = (int)min((int64_t)L::TILE, n - base);
-  int32_t items[IPT];
-  BlockLoad<BT, IPT>(in + base, valid, items);
-  const unsigned f = BlockPred<IPT>(items, lo, hi, BlockValidMask<BT, IPT>(valid));
-  // Input order inside the tile is (vector v, thread, element): scan the
-  // per-vector counts of all threads at once, packed 16 bits per vector.
-  unsigned long long packed = 0;
+  __shared__ long long s_off;
+  long long tile = blockIdx.x;
+  if (tile >= ntiles) return;
+  int32_t cur[IPT], nxt[IPT];
+  BlockLoad<BT, IPT>(in + tile * L::TILE, (int)min((int64_t)L::TILE, (int64_t)(n - tile * L::TILE)), cur);
+  for (; tile < ntiles; tile += gridDim.x) {
+    const int64_t base = tile * L::TILE;
+    const int valid = (int)min((int64_t)L::TILE, n - base);
+    const long long nt = tile + gridDim.x;
+    if (nt < ntiles)  // prefetch: in flight during this tile's scan/look-back/store
+      BlockLoad<BT, IPT>(in + nt * L::TILE, (int)min((int64_t)L::TILE, (int64_t)(n - nt * L::TILE)), nxt);
+    const unsigned f = BlockPred<IPT>(cur, lo, hi, BlockValidMask<BT, IPT>(valid));
+    // Input order inside the tile is (vector v, thread, element): scan the
+    // per-vector counts of all threads at once, packed 16 bits per vector.
+    unsigned long long packed = 0;
 #pragma unroll
-  for (int v = 0; v < L::NV; ++v) packed |= (unsigned long long)__popc(L::vec_bits(f, v)) << (16 * v);
-  unsigned long long tot;
-  const unsigned long long ex = BlockScan<BT>(packed, s_scan, tot);
-  int run = 0;
+    for (int v = 0; v < L::NV; ++v) packed |= (unsigned long long)__popc(L::vec_bits(f, v)) << (16 * v);
+    unsigned long long tot;
+    const unsigned long long ex = BlockScan<BT>(packed, s_scan, tot);
+    int run = 0;
 #pragma unroll
-  for (int v = 0; v < L::NV; ++v) {
-    int pos = run + (int)((ex >> (16 * v)) & 0xffff);
+    for (int v = 0; v < L::NV; ++v) {
+      int pos = run + (int)((ex >> (16 * v)) & 0xffff);
 #pragma unroll
-    for (int e = 0; e < L::VEC; ++e)
-      if ((f >> (v * L::VEC + e)) & 1u) s_items[pos++] = items[v * L::VEC + e];
-    run += (int)((tot >> (16 * v)) & 0xffff);
+      for (int e = 0; e < L::VEC; ++e)
+        if ((f >> (v * L::VEC + e)) & 1u) s_items[pos++] = cur[v * L::VEC + e];
+      run += (int)((tot >> (16 * v)) & 0xffff);
+    }
+    const int tile_total = run;
+    if (threadIdx.x < 32) {
+      const long long off = tile_lookback(status, tile, tile_total);
+      if (threadIdx.x == 0) s_off = off;
+    }
+    __syncthreads();
+    const long long off = s_off;
+    for (int i = threadIdx.x; i < tile_total; i += BT) out[off + i] = s_items[i];
+    if (threadIdx.x == 0 && tile == ntiles - 1) *total_out = off + tile_total;
+    __syncthreads();  // s_items / s_off reuse
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) cur[k] = nxt[k];
   }
-  const int tile_total = run;
-  if (threadIdx.x < 32) {
-    const long long off = tile_lookback(status, tile, tile_total);
-    if (threadIdx.x == 0) s_off = off;
-  }
-  __syncthreads();
-  const long long off = s_off;
-  for (int i = threadIdx.x; i < tile_total; i += BT) out[off + i] = s_items[i];
-  if (threadIdx.x == 0 && base + L::TILE >= n) *total_out = off + tile_total;
 }
 
-// Crystal order for an arbitrary logical (bt, ipt): logical thread t owns
-// slots t, t+bt, ...; its matches go, in stride order, to its exclusive prefix
-// (block_thread_counts + block_scan + block_shuffle, block_ops.hpp:73-122).
+// Crystal order for an arbitrary logical (bt, ipt) (select_tile_into,
+// select.hpp:107-135 with block_thread_counts + block_scan + block_shuffle,
+// block_ops.hpp:73-122): logical thread t of logical tile j owns slots
+// j*S + t + k*bt (S = bt*ipt); the tile's matches are laid out thread-major,
+// each thread's in k order, and tiles follow each other.  A CTA stages a
+// CHUNK of whole logical tiles (~kCrysChunk elements) in shared memory, so
+// small logical tiles do not mean small CTAs; one look-back per chunk.
 constexpr int kCrysPB = 256;
+constexpr int kCrysChunk = 8192;
 
 __global__ void __launch_bounds__(kCrysPB) select_crystal_kernel(
-    const int32_t* __restrict__ in, int64_t n, int32_t lo, int32_t hi, int bt, int ipt,
-    int32_t* __restrict__ out, unsigned long long* status, unsigned long long* tile_counter,
-    long long* total_out) {
+    const int32_t* __restrict__ in, int64_t n, int32_t lo, int32_t hi, int bt, int ipt, int chunk,
+    int32_t* __restrict__ out, unsigned long long* status, long long* total_out) {
   extern __shared__ int32_t s_dyn[];
-  const int tile_sz = bt * ipt;
-  int32_t* s_in = s_dyn;
-  int32_t* s_out = s_dyn + tile_sz;
-  int32_t* s_pre = s_out + tile_sz;  // [bt] per-logical-thread exclusive prefix
+  int32_t* s_in = s_dyn;                 // [chunk]
+  int32_t* s_out = s_dyn + chunk;        // [chunk]
+  int32_t* s_cnt = s_out + chunk;        // [pairs] counts, then exclusive prefixes
   __shared__ int s_scan[kCrysPB / 32 + 1];
-  __shared__ long long s_tile, s_off;
-  if (threadIdx.x == 0) s_tile = (long long)atomicAdd(tile_counter, 1ull);
-  __syncthreads();
-  const long long tile = s_tile;
-  const int64_t base = tile * (int64_t)tile_sz;
-  const int valid = (int)min((int64_t)tile_sz, n - base);
-  for (int i = threadIdx.x; i < valid; i += kCrysPB) s_in[i] = ld_stream1(in + base + i);
-  __syncthreads();
-  // logical threads [g*G, g*G+G) belong to physical thread g
-  const int G = (bt + kCrysPB - 1) / kCrysPB;
-  int mine = 0;
-  for (int q = 0; q < G; ++q) {
-    const int t = threadIdx.x * G + q;
-    int c = 0;
-    if (t < bt)
-      for (int i = t; i < valid; i += bt) c += (s_in[i] >= lo && s_in[i] <= hi);
-    if (t < bt) s_pre[t] = c;
-    mine += c;
+  __shared__ long long s_off;
+  const long long c = blockIdx.x;
+  const int64_t base = c * (int64_t)chunk;
+  const int valid = (int)min((int64_t)chunk, n - base);
+  // 1. stage the chunk (128-bit loads where aligned)
+  const int32_t* src = in + base;
+  if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+    const int nv = valid >> 2;
+    for (int i = threadIdx.x; i < nv; i += kCrysPB)
+      reinterpret_cast<int4*>(s_in)[i] = ld_stream4(src + 4 * i);
+    for (int i = 4 * nv + threadIdx.x; i < valid; i += kCrysPB) s_in[i] = ld_stream1(src + i);
+  } else {
+    for (int i = threadIdx.x; i < valid; i += kCrysPB) s_in[i] = ld_stream1(src + i);
   }
+  __syncthreads();
+  const int S = bt * ipt;
+  const int tiles = (valid + S - 1) / S;
+  const int pairs = tiles * bt;  // (logical tile, logical thread), in output order
+  // 2. per-pair match counts; consecutive threads take consecutive logical
+  //    threads, so the strided smem reads are bank-conflict free
+  for (int p = threadIdx.x; p < pairs; p += kCrysPB) {
+    const int j = p / bt, t = p - j * bt;
+    const int b = j * S + t;
+    int cnt = 0;
+    for (int k = 0; k < ipt; ++k) {
+      const int i = b + k * bt;
+      if (i < valid) {
+        const int32_t x = s_in[i];
+        cnt += (x >= lo && x <= hi);
+      }
+    }
+    s_cnt[p] = cnt;
+  }
+  __syncthreads();
+  // 3. exclusive scan of the counts in pair order: thread u owns a contiguous run
+  const int per = (pairs + kCrysPB - 1) / kCrysPB;
+  const int p0 = min(pairs, (int)threadIdx.x * per), p1 = min(pairs, p0 + per);
+  int mine = 0;
+  for (int p = p0; p < p1; ++p) mine += s_cnt[p];
   int total;
   int run = BlockScan<kCrysPB>(mine, s_scan, total);
-  for (int q = 0; q < G; ++q) {
-    const int t = threadIdx.x * G + q;
-    if (t < bt) {
-      const int c = s_pre[t];
-      s_pre[t] = run;
-      run += c;
-    }
+  for (int p = p0; p < p1; ++p) {
+    const int cc = s_cnt[p];
+    s_cnt[p] = run;
+    run += cc;
   }
   __syncthreads();
-  for (int q = 0; q < G; ++q) {
-    const int t = threadIdx.x * G + q;
-    if (t < bt) {
-      int pos = s_pre[t];
-      for (int i = t; i < valid; i += bt)
-        if (s_in[i] >= lo && s_in[i] <= hi) s_out[pos++] = s_in[i];
+  // 4. block_shuffle: each logical thread's matches, in k order, at its prefix
+  for (int p = threadIdx.x; p < pairs; p += kCrysPB) {
+    const int j = p / bt, t = p - j * bt;
+    const int b = j * S + t;
+    int pos = s_cnt[p];
+    for (int k = 0; k < ipt; ++k) {
+      const int i = b + k * bt;
+      if (i < valid) {
+        const int32_t x = s_in[i];
+        if (x >= lo && x <= hi) s_out[pos++] = x;
+      }
     }
   }
   if (threadIdx.x < 32) {
-    const long long off = tile_lookback(status, tile, total);
+    const long long off = tile_lookback(status, c, total);
     if (threadIdx.x == 0) s_off = off;
   }
   __syncthreads();
   const long long off = s_off;
   for (int i = threadIdx.x; i < total; i += kCrysPB) out[off + i] = s_out[i];
-  if (threadIdx.x == 0 && base + tile_sz >= n) *total_out = off + total;
+  if (threadIdx.x == 0 && base + chunk >= n) *total_out = off + total;
 }
 
 // project.hpp:49-64.  Linear: float mul, float mul, float add with no FMA
@@ -252,28 +288,33 @@ int64_t select_i32(crys_ctx* ctx, const int32_t* d_in, int64_t n, int32_t lo, in
   cudaStream_t st = ctx->stream;
   int64_t tile;
   size_t dyn = 0;
+  int chunk = 0;
   if (order == CRYS_ORDER_INPUT) {
     tile = (int64_t)kSelBT * kSelIPT;
   } else {
     CRYS_CHECK(order == CRYS_ORDER_CRYSTAL, CRYS_ECONFIG, "unknown select order");
-    tile = (int64_t)bt * ipt;
-    dyn = sizeof(int32_t) * (size_t)(2 * tile + bt);
-    CRYS_CHECK(dyn <= 200 * 1024, CRYS_ENOTBUILT, "Crystal-order tile too large for shared memory");
+    const int64_t S = (int64_t)bt * ipt;
+    CRYS_CHECK(S <= 16384, CRYS_ENOTBUILT, "Crystal-order tile too large for shared memory");
+    chunk = (int)(S >= kCrysChunk ? S : S * (kCrysChunk / S));
+    tile = chunk;
+    const int64_t pairs = (chunk / S) * bt;
+    dyn = sizeof(int32_t) * (size_t)(2 * chunk + pairs);
   }
   const int64_t ntiles = (n + tile - 1) / tile;
   ctx->status.reserve(sizeof(unsigned long long) * (size_t)(ntiles + 2));
   auto* status = ctx->status.as<unsigned long long>();
-  auto* counter = status + ntiles;
   auto* total = reinterpret_cast<long long*>(status + ntiles + 1);
   CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(unsigned long long) * (size_t)(ntiles + 2), st));
   timing_kernel_begin(ctx);
   if (order == CRYS_ORDER_INPUT) {
-    select_input_kernel<kSelBT, kSelIPT><<<(unsigned)ntiles, kSelBT, 0, st>>>(d_in, n, lo, hi, d_out,
-                                                                             status, counter, total);
+    auto fn = select_input_kernel<kSelBT, kSelIPT>;
+    const int nb = occupancy((const void*)fn, kSelBT, 0);
+    const int grid = (int)std::min<int64_t>(ntiles, (int64_t)nb * ctx->num_sms);
+    fn<<<grid, kSelBT, 0, st>>>(d_in, n, lo, hi, d_out, status, ntiles, total);
   } else {
     occupancy((const void*)select_crystal_kernel, kCrysPB, dyn);
-    select_crystal_kernel<<<(unsigned)ntiles, kCrysPB, dyn, st>>>(d_in, n, lo, hi, bt, ipt, d_out,
-                                                                 status, counter, total);
+    select_crystal_kernel<<<(unsigned)ntiles, kCrysPB, dyn, st>>>(d_in, n, lo, hi, bt, ipt, chunk, d_out,
+                                                                 status, total);
   }
   timing_kernel_end(ctx);
   count_launch(ctx);

@@ -360,6 +360,26 @@ class DeviceDatabase:
                 db.upload(t, c, a)
         return db
 
+    def upload_host(self, tables, order=None) -> None:
+        """Asynchronous bulk H2D of host columns (crys_db_upload_host): copies
+        are issued in ``order`` (a list of (table, column); default: mapping
+        order) on the copy stream and each query waits only for the columns it
+        reads.  The arrays must stay alive (and, for a true DMA, be pinned)
+        until the queries that read them have completed; they are kept
+        referenced by this object until the next upload_host."""
+        if order is None:
+            order = [(t, c) for t, cs in tables.items() for c in cs]
+        keep, cols = [], []
+        for t, c in order:
+            a = tables[t][c]
+            if not (isinstance(a, np.ndarray) and a.dtype == np.int32 and a.flags.c_contiguous):
+                a = np.ascontiguousarray(a, dtype=np.int32)
+            keep.append(a)
+            cols.append(_lib.crys_host_column(t.encode(), c.encode(), a.ctypes.data, len(a)))
+        arr = (_lib.crys_host_column * len(cols))(*cols)
+        check(LIB.crys_db_upload_host(self.h, arr, len(cols)))
+        self._host_keep = keep
+
     def upload(self, table: str, column: str, data) -> None:
         a = np.ascontiguousarray(data, dtype=np.int32)
         check(LIB.crys_db_upload_column(self.h, table.encode(), column.encode(),

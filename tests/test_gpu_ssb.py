@@ -87,6 +87,33 @@ def test_host_database_end_to_end(tq):
         assert stats.survivors == rec["survivors"]
 
 
+def test_async_host_upload_suite(tq):
+    """crys_db_upload_host: the whole suite over asynchronously uploaded
+    (pinned) host columns, re-uploaded while earlier work may be in flight,
+    equals the SF=1 goldens (per-column ready events + WAR fence)."""
+    import torch
+    from oracle.oracle import Oracle
+    host = Oracle().generate(1, 42)
+    pinned = {}
+    for t, cols in host.items():
+        for c, a in cols.items():
+            pt = torch.empty(len(a), dtype=torch.int32, pin_memory=True)
+            pt.numpy()[:] = a
+            pinned.setdefault(t, {})[c] = pt.numpy()
+    db = tq.DeviceDatabase.from_host({}, sf=1, seed=42)
+    # fact columns first in reverse first-use order: q1 waits on the last DMA
+    order = [("lineorder", c) for c in reversed(list(pinned["lineorder"]))]
+    order += [(t, c) for t in pinned if t != "lineorder" for c in pinned[t]]
+    for rep in range(2):
+        db.upload_host(pinned, order)
+        for q in range(13):
+            rec = golden("sf1")["queries"][QUERY_NAMES[q]]
+            stats = tq.QueryStats()
+            assert tq.run_query(db, q, tq.TileConfig(), 1, stats).as_tuples() == golden_rows(rec), (rep, q)
+            assert stats.survivors == rec["survivors"]
+    db.free()
+
+
 @pytest.mark.parametrize("cfg", [(128, 4), (256, 8), (256, 16), (128, 16), (512, 8), (32, 1)])
 def test_ssb_sf1_tile_invariance(tq, sf1, cfg):
     # test_ssb.cpp:251-261

@@ -1,6 +1,7 @@
 """Run the given SSB queries twice each (warm-up + the profiled launch).
 
-    SF=20 python tools/profile_query.py 3 6 10      (query ids, all_query_ids order)"""
+    SF=20 python tools/profile_query.py 3 6 10      (query ids, all_query_ids order)
+    SUITE=1 python tools/profile_query.py           (all 13 in suite order: warm-up pass + profiled pass)"""
 import os
 import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -9,7 +10,14 @@ from paper_2003_01178_b200 import tq  # noqa: E402
 sf = int(os.environ.get("SF", "20"))
 bt, ipt = map(int, os.environ.get("TILE", "256x16").split("x"))
 db = tq.DeviceDatabase.generate(sf, 42)
-for q in map(int, sys.argv[1:]):
-    tq.run_query(db, q, tq.TileConfig(bt, ipt))
-    tq.run_query(db, q, tq.TileConfig(bt, ipt))
+qs = list(map(int, sys.argv[1:])) or list(range(13))
+if os.environ.get("SUITE"):
+    # suite order: one warm-up pass, then the profiled pass (ncu -s len(qs) -c len(qs))
+    for _ in range(2):
+        for q in qs:
+            tq.run_query(db, q, tq.TileConfig(bt, ipt))
+else:
+    for q in qs:
+        tq.run_query(db, q, tq.TileConfig(bt, ipt))
+        tq.run_query(db, q, tq.TileConfig(bt, ipt))
 print("done")

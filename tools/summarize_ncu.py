@@ -3,6 +3,7 @@
   python tools/summarize_ncu.py launches gpurun_out/launches.csv   # per-kernel share of a launch list
   python tools/summarize_ncu.py full gpurun_out/prof.ncu-rep        # key counters per profiled launch
   python tools/summarize_ncu.py sass gpurun_out/prof.ncu-rep [k]    # opcode mix + stall reasons of launch k
+  python tools/summarize_ncu.py traffic gpurun_out/prof.ncu-rep out.json  # DRAM bytes per launch
 """
 import csv
 import io
@@ -57,6 +58,30 @@ def full(rep):
                 print(f"  {k:60s} {r[i]:>18s} {units[i]}")
 
 
+def traffic(rep, out_json):
+    """DRAM bytes per profiled launch (dram__bytes_read.sum + _write.sum) ->
+    JSON consumed by bench.py's roofline.traffic."""
+    import json
+    hdr, units, data = raw(rep)
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    tscale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
+    launches = []
+    for r in data:
+        def val(k):
+            i = hdr.index(k)
+            return float(r[i].replace(",", "")) * scale.get(units[i], 1)
+        ti = hdr.index("gpu__time_duration.sum")
+        launches.append({"kernel": r[hdr.index("Kernel Name")].split("(")[0].replace("void ", ""),
+                         "dram_read": val("dram__bytes_read.sum"),
+                         "dram_write": val("dram__bytes_write.sum"),
+                         "us": float(r[ti].replace(",", "")) * tscale.get(units[ti], 1e-3),
+                         "l2_hit_pct": float(r[hdr.index("lts__t_sector_hit_rate.pct")])})
+    json.dump({"source": rep, "launches": launches}, open(out_json, "w"), indent=1)
+    for L in launches:
+        print(f"{L['us']:9.1f} us  {(L['dram_read'] + L['dram_write']) / 1e9:7.3f} GB  "
+              f"L2 hit {L['l2_hit_pct']:5.1f}%  {L['kernel'][:80]}")
+
+
 def sass(rep, which=0):
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True, check=True).stdout
@@ -98,5 +123,7 @@ if __name__ == "__main__":
         launches(path)
     elif mode == "full":
         full(path)
+    elif mode == "traffic":
+        traffic(path, sys.argv[3])
     else:
         sass(path, int(sys.argv[3]) if len(sys.argv) > 3 else 0)
