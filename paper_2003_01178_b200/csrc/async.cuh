@@ -1,0 +1,59 @@
+// async.cuh -- mbarrier + 1-D TMA bulk-copy (cp.async.bulk) PTX helpers for
+// sm_100a, shared by the SSB pipeline ring and the onesweep radix tiles.
+#pragma once
+
+#include "common.cuh"
+
+namespace crys {
+namespace pipe {
+
+__device__ __forceinline__ uint32_t s_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_addr(bar)) : "memory");
+}
+// Release a ring slot after this warp's last reads of it.  The reads are
+// generic-proxy accesses and the refill is an async-proxy (TMA) write, so
+// the producer orders the two with fence.proxy.async after acquiring the
+// empty barrier (without it, rare wrong sums were observed on B200).
+__device__ __forceinline__ void release_slot(uint64_t* bar, bool leader) {
+  __syncwarp();
+  if (leader) mbar_arrive(bar);
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(s_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// 1-D TMA bulk copy global -> shared, completion counted on `bar` in bytes.
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(s_addr(dst)),
+      "l"(src), "r"(bytes), "r"(s_addr(bar)), "l"(policy)
+      : "memory");
+}
+
+}  // namespace pipe
+}  // namespace crys

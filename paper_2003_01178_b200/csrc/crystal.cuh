@@ -323,9 +323,11 @@ __device__ __forceinline__ long long tile_lookback(unsigned long long* status, l
     const long long idx = look - (long long)lane;
     unsigned long long w = kPre;  // lanes before tile 0 act as an empty prefix
     if (idx >= 0) {
-      do {
-        w = st[idx];
-      } while ((w >> 62) == 0);
+      unsigned ns = 32;
+      while (((w = st[idx]) >> 62) == 0) {
+        __nanosleep(ns);
+        ns = min(ns * 2, 512u);
+      }
     } else {
       w = kPre;
     }
@@ -341,6 +343,70 @@ __device__ __forceinline__ long long tile_lookback(unsigned long long* status, l
     look -= 32;
   }
   if (lane == 0) st[tile] = kPre | (unsigned long long)(excl + aggregate);
+  return excl;
+}
+
+// Publish a tile's aggregate (tile 0: its inclusive prefix) ahead of its
+// look-back; pair with block_lookback(..., published = true).
+__device__ __forceinline__ void lookback_publish(unsigned long long* status, long long tile,
+                                                 long long aggregate) {
+  volatile unsigned long long* st = status;
+  st[tile] = (tile == 0 ? (2ull << 62) : (1ull << 62)) | (unsigned long long)aggregate;
+}
+
+// Block-wide decoupled look-back: the whole CTA reads a window of BT
+// predecessors per round trip (instead of a warp's 32), so a tile whose
+// nearest inclusive predecessor is a few hundred tiles back -- the normal
+// case with ~1000 tiles in flight on 148 SMs -- resolves in one or two L2
+// round trips.  Same status-word format as tile_lookback.  Every thread of
+// the CTA must call it; returns the tile's exclusive offset to all threads.
+template <int BT>
+__device__ __forceinline__ long long block_lookback(unsigned long long* status, long long tile,
+                                                    long long aggregate, long long* s_red,
+                                                    bool published = false) {
+  constexpr int W = BT / 32;
+  constexpr unsigned long long kAgg = 1ull << 62, kPre = 2ull << 62, kVal = (1ull << 62) - 1;
+  volatile unsigned long long* st = status;
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  int* s_first = reinterpret_cast<int*>(s_red + W);  // [W]
+  if (tile == 0) {
+    if (threadIdx.x == 0) st[0] = kPre | (unsigned long long)aggregate;
+    return 0;
+  }
+  if (threadIdx.x == 0) st[tile] = kAgg | (unsigned long long)aggregate;
+  long long excl = 0;
+  long long look = tile - 1;
+  while (true) {
+    const long long idx = look - (long long)threadIdx.x;
+    unsigned long long w = kPre;  // before tile 0: an empty inclusive prefix
+    if (idx >= 0) {
+      // exponential back-off: ~1000 CTAs polling the same few status lines
+      // otherwise saturate the L2 slice that must also absorb the publishes
+      unsigned ns = 32;
+      while (((w = st[idx]) >> 62) == 0) {
+        __nanosleep(ns);
+        ns = min(ns * 2, 512u);
+      }
+    }
+    const unsigned pre = __ballot_sync(0xffffffffu, (w >> 62) == 2);
+    if (lane == 0) s_first[warp] = pre ? (int)(warp * 32 + __ffs(pre) - 1) : BT;
+    __syncthreads();
+    int first = BT;
+#pragma unroll
+    for (int i = 0; i < W; ++i) first = min(first, s_first[i]);
+    long long v = (int)threadIdx.x <= first ? (long long)(w & kVal) : 0;
+    v = warp_sum(v);
+    if (lane == 0) s_red[warp] = v;
+    __syncthreads();
+    long long sum = 0;
+#pragma unroll
+    for (int i = 0; i < W; ++i) sum += s_red[i];
+    excl += sum;
+    __syncthreads();  // s_first / s_red reuse
+    if (first < BT) break;
+    look -= BT;
+  }
+  if (threadIdx.x == 0) st[tile] = kPre | (unsigned long long)(excl + aggregate);
   return excl;
 }
 

@@ -21,7 +21,14 @@
 namespace crys {
 namespace {
 
-constexpr int kSelBT = 256, kSelIPT = 16;  // native select tile (4096 rows, 16 KB)
+// Tuning knob CRYS_SEL_CFG picks the input-order select instantiation.
+int sel_cfg() {
+  static const int cfg = [] {
+    const char* e = getenv("CRYS_SEL_CFG");
+    return e ? atoi(e) : 0;
+  }();
+  return cfg;
+}
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -29,62 +36,282 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
-// Input-order selection: persistent CTAs walk tiles blockIdx.x, +gridDim.x,
-// ...; the NEXT tile's 128-bit loads are issued before the current tile's
-// scan + decoupled look-back, so HBM reads overlap the serial part.  Every
-// CTA is resident and walks its tiles in increasing order, so each tile's
-// predecessors are always in progress or done (no look-back deadlock).
+// Input-order selection (select_branching/predicated_into, workers=1: output
+// in input order).  Single pass with a decoupled look-back over tiles.
+// Tile layout is WARP-CONTIGUOUS: warp w owns slots [w*32*IPT, (w+1)*32*IPT),
+// lane l's vector v is the 4 slots at w*32*IPT + v*128 + 4*l, so a warp's
+// order is (v, lane, element) and every load is a 128-bit coalesced read.
+// Positions come from per-vector warp scans (popc + shuffles) and one barrier
+// for the warp totals; the compacted tile is staged in shared memory and
+// stored with coalesced writes.
+//   PERSIST = false: one tile per CTA, tile = blockIdx.x (dispatch order).
+//   PERSIST = true : resident CTAs take tiles from an atomic counter and
+//                    prefetch the next tile's vectors before the current
+//                    tile's look-back + store (dynamic order keeps the
+//                    look-back chain short).
 template <int BT, int IPT>
+struct SelTile {
+  static constexpr int NV = IPT / 4;
+  static constexpr int TILE = BT * IPT;
+  static constexpr int W = BT / 32;
+  static_assert(IPT % 4 == 0, "128-bit vectors");
+};
+
+template <int BT, int IPT>
+__device__ __forceinline__ void sel_load(const int32_t* __restrict__ in, int64_t base, int valid,
+                                         int4 (&v)[IPT / 4]) {
+  const int wb = (threadIdx.x >> 5) * 32 * IPT + 4 * (int)lane_id();
+#pragma unroll
+  for (int j = 0; j < IPT / 4; ++j) {
+    const int s = wb + j * 128;
+    if (s + 4 <= valid) {
+      v[j] = ld_stream4(in + base + s);
+    } else {
+      v[j] = make_int4(0, 0, 0, 0);
+      if (s + 0 < valid) v[j].x = ld_stream1(in + base + s + 0);
+      if (s + 1 < valid) v[j].y = ld_stream1(in + base + s + 1);
+      if (s + 2 < valid) v[j].z = ld_stream1(in + base + s + 2);
+    }
+  }
+}
+
+// Per-vector predicate bits and warp-local positions of one tile; the block
+// total via one barrier.  Returns the tile's match count; woff = this warp's
+// offset inside the tile.
+template <int BT, int IPT>
+__device__ __forceinline__ int sel_count(const int4 (&v)[IPT / 4], int valid, int32_t lo, int32_t hi,
+                                         int* s_warp, unsigned (&bits)[IPT / 4], int (&pos)[IPT / 4],
+                                         int& woff) {
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  const int wb = warp * 32 * IPT + 4 * (int)lane;
+  int run = 0;
+#pragma unroll
+  for (int j = 0; j < IPT / 4; ++j) {
+    const int s = wb + j * 128;
+    unsigned b = 0;
+    b |= (unsigned)(s + 0 < valid && v[j].x >= lo && v[j].x <= hi) << 0;
+    b |= (unsigned)(s + 1 < valid && v[j].y >= lo && v[j].y <= hi) << 1;
+    b |= (unsigned)(s + 2 < valid && v[j].z >= lo && v[j].z <= hi) << 2;
+    b |= (unsigned)(s + 3 < valid && v[j].w >= lo && v[j].w <= hi) << 3;
+    bits[j] = b;
+    const int c = __popc(b);
+    int x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if ((int)lane >= o) x += y;
+    }
+    pos[j] = run + x - c;
+    run += __shfl_sync(0xffffffffu, x, 31);
+  }
+  if (lane == 31) s_warp[warp] = run;
+  __syncthreads();
+  int total = 0;
+  woff = 0;
+#pragma unroll
+  for (int w = 0; w < BT / 32; ++w) {
+    const int t = s_warp[w];
+    woff += (w < (int)warp) ? t : 0;
+    total += t;
+  }
+  return total;
+}
+
+template <int IPT>
+__device__ __forceinline__ void sel_scatter(const int4 (&v)[IPT / 4], const unsigned (&bits)[IPT / 4],
+                                            const int (&pos)[IPT / 4], int woff, int32_t* s_items) {
+#pragma unroll
+  for (int j = 0; j < IPT / 4; ++j) {
+    int p = woff + pos[j];
+    if (bits[j] & 1u) s_items[p++] = v[j].x;
+    if (bits[j] & 2u) s_items[p++] = v[j].y;
+    if (bits[j] & 4u) s_items[p++] = v[j].z;
+    if (bits[j] & 8u) s_items[p++] = v[j].w;
+  }
+}
+
+// Compacts one tile into s_items; returns the tile's match count.
+template <int BT, int IPT>
+__device__ __forceinline__ int sel_compact(const int4 (&v)[IPT / 4], int valid, int32_t lo, int32_t hi,
+                                           int32_t* s_items, int* s_warp) {
+  unsigned bits[IPT / 4];
+  int pos[IPT / 4];
+  int woff;
+  const int total = sel_count<BT, IPT>(v, valid, lo, hi, s_warp, bits, pos, woff);
+  sel_scatter<IPT>(v, bits, pos, woff, s_items);
+  return total;
+}
+
+// Persistent WAVE form: CTA c takes tiles c, c+G, c+2G, ... (static, so no
+// tile is ever held unpublished behind another); per tile it counts, PUBLISHES
+// the aggregate at once, issues the next tile's loads, then looks back (one
+// block-wide round trip covers the whole previous wave) and stores.  The
+// next tile's HBM reads are in flight during the look-back wait.
+template <int BT, int IPT>
+__global__ void __launch_bounds__(BT) select_wave_kernel(const int32_t* __restrict__ in, int64_t n,
+                                                         int32_t lo, int32_t hi, int32_t* __restrict__ out,
+                                                         unsigned long long* status, long long ntiles,
+                                                         long long* total_out) {
+  using T = SelTile<BT, IPT>;
+  __shared__ __align__(16) int32_t s_items[T::TILE];
+  __shared__ int s_warp[T::W];
+  __shared__ long long s_red[T::W + T::W / 2 + 1];
+  long long tile = blockIdx.x;
+  if (tile >= ntiles) return;
+  int4 v[IPT / 4];
+  sel_load<BT, IPT>(in, tile * T::TILE, (int)min((int64_t)T::TILE, (int64_t)(n - tile * T::TILE)), v);
+  for (; tile < ntiles; tile += gridDim.x) {
+    const int64_t base = tile * T::TILE;
+    const int valid = (int)min((int64_t)T::TILE, (int64_t)(n - base));
+    unsigned bits[IPT / 4];
+    int pos[IPT / 4];
+    int woff;
+    const int total = sel_count<BT, IPT>(v, valid, lo, hi, s_warp, bits, pos, woff);
+    if (threadIdx.x == 0) lookback_publish(status, tile, total);
+    sel_scatter<IPT>(v, bits, pos, woff, s_items);
+    const long long nt = tile + gridDim.x;
+    if (nt < ntiles)  // prefetch: overwrites v (already scattered to smem)
+      sel_load<BT, IPT>(in, nt * T::TILE, (int)min((int64_t)T::TILE, (int64_t)(n - nt * T::TILE)), v);
+    const long long off = block_lookback<BT>(status, tile, total, s_red, true);
+    for (int i = threadIdx.x; i < total; i += BT) out[off + i] = s_items[i];
+    if (threadIdx.x == 0 && tile == ntiles - 1) *total_out = off + total;
+    __syncthreads();  // s_items / s_warp reuse
+  }
+}
+
+template <int BT, int IPT, bool PERSIST, bool NOLB = false>
 __global__ void __launch_bounds__(BT) select_input_kernel(const int32_t* __restrict__ in, int64_t n,
                                                           int32_t lo, int32_t hi,
                                                           int32_t* __restrict__ out,
                                                           unsigned long long* status,
+                                                          unsigned long long* tile_counter,
                                                           long long ntiles, long long* total_out) {
-  using L = VecLayout<BT, IPT>;
-  static_assert(L::NV <= 4 && BT * L::VEC < 65536, "packed 16-bit per-vector counts");
-  __shared__ int32_t s_items[L::TILE];
-  __shared__ unsigned long long s_scan[BT / 32 + 1];
-  __shared__ long long s_off;
-  long long tile = blockIdx.x;
-  if (tile >= ntiles) return;
-  int32_t cur[IPT], nxt[IPT];
-  BlockLoad<BT, IPT>(in + tile * L::TILE, (int)min((int64_t)L::TILE, (int64_t)(n - tile * L::TILE)), cur);
-  for (; tile < ntiles; tile += gridDim.x) {
-    const int64_t base = tile * L::TILE;
-    const int valid = (int)min((int64_t)L::TILE, n - base);
-    const long long nt = tile + gridDim.x;
-    if (nt < ntiles)  // prefetch: in flight during this tile's scan/look-back/store
-      BlockLoad<BT, IPT>(in + nt * L::TILE, (int)min((int64_t)L::TILE, (int64_t)(n - nt * L::TILE)), nxt);
-    const unsigned f = BlockPred<IPT>(cur, lo, hi, BlockValidMask<BT, IPT>(valid));
-    // Input order inside the tile is (vector v, thread, element): scan the
-    // per-vector counts of all threads at once, packed 16 bits per vector.
-    unsigned long long packed = 0;
-#pragma unroll
-    for (int v = 0; v < L::NV; ++v) packed |= (unsigned long long)__popc(L::vec_bits(f, v)) << (16 * v);
-    unsigned long long tot;
-    const unsigned long long ex = BlockScan<BT>(packed, s_scan, tot);
-    int run = 0;
-#pragma unroll
-    for (int v = 0; v < L::NV; ++v) {
-      int pos = run + (int)((ex >> (16 * v)) & 0xffff);
-#pragma unroll
-      for (int e = 0; e < L::VEC; ++e)
-        if ((f >> (v * L::VEC + e)) & 1u) s_items[pos++] = cur[v * L::VEC + e];
-      run += (int)((tot >> (16 * v)) & 0xffff);
+  using T = SelTile<BT, IPT>;
+  __shared__ __align__(16) int32_t s_items[T::TILE];
+  __shared__ int s_warp[T::W];
+  __shared__ long long s_off, s_next;
+  __shared__ long long s_red[T::W + T::W / 2 + 1];
+  if constexpr (!PERSIST) {
+    const long long tile = blockIdx.x;
+    const int64_t base = tile * T::TILE;
+    const int valid = (int)min((int64_t)T::TILE, (int64_t)(n - base));
+    int4 v[IPT / 4];
+    sel_load<BT, IPT>(in, base, valid, v);
+    const int total = sel_compact<BT, IPT>(v, valid, lo, hi, s_items, s_warp);
+    long long off;
+    if constexpr (NOLB) {  // timing experiment: no look-back (tile-private output slots)
+      __syncthreads();
+      off = tile * T::TILE;
+    } else {
+      off = block_lookback<BT>(status, tile, total, s_red);
     }
-    const int tile_total = run;
-    if (threadIdx.x < 32) {
-      const long long off = tile_lookback(status, tile, tile_total);
-      if (threadIdx.x == 0) s_off = off;
+    for (int i = threadIdx.x; i < total; i += BT) out[off + i] = s_items[i];
+    if (threadIdx.x == 0 && tile == ntiles - 1) *total_out = off + total;
+  } else {
+    if (threadIdx.x == 0) s_next = (long long)atomicAdd(tile_counter, 1ull);
+    __syncthreads();
+    long long tile = s_next;
+    int4 v[IPT / 4], nv[IPT / 4];
+    if (tile < ntiles)
+      sel_load<BT, IPT>(in, tile * T::TILE, (int)min((int64_t)T::TILE, (int64_t)(n - tile * T::TILE)), v);
+    while (tile < ntiles) {
+      const int64_t base = tile * T::TILE;
+      const int valid = (int)min((int64_t)T::TILE, (int64_t)(n - base));
+      if (threadIdx.x == 0) s_next = (long long)atomicAdd(tile_counter, 1ull);
+      const int total = sel_compact<BT, IPT>(v, valid, lo, hi, s_items, s_warp);  // barrier inside
+      const long long nt = s_next;
+      if (nt < ntiles)
+        sel_load<BT, IPT>(in, nt * T::TILE, (int)min((int64_t)T::TILE, (int64_t)(n - nt * T::TILE)), nv);
+      if (threadIdx.x < 32) {
+        const long long off = tile_lookback(status, tile, total);
+        if (threadIdx.x == 0) s_off = off;
+      }
+      __syncthreads();
+      const long long off = s_off;
+      for (int i = threadIdx.x; i < total; i += BT) out[off + i] = s_items[i];
+      if (threadIdx.x == 0 && tile == ntiles - 1) *total_out = off + total;
+      __syncthreads();  // s_items / s_off / s_next reuse
+      tile = nt;
+#pragma unroll
+      for (int j = 0; j < IPT / 4; ++j) v[j] = nv[j];
+    }
+  }
+}
+
+// Reduce-then-scan form (no look-back latency on the critical path): pass 1
+// streams the input and writes one count per tile, a single CTA scans the
+// counts, pass 2 re-streams the input and writes every tile at its known
+// offset.  8N + 4*matched bytes instead of 4N + 4*matched, but both passes
+// are pure streaming (measured on B200: a tile's chained look-back costs ~7 us
+// under full HBM load, 4x its load).
+template <int BT, int IPT>
+__global__ void __launch_bounds__(BT) select_count_kernel(const int32_t* __restrict__ in, int64_t n,
+                                                          int32_t lo, int32_t hi, long long ntiles,
+                                                          unsigned* counts) {
+  using T = SelTile<BT, IPT>;
+  __shared__ int s_warp[T::W];
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t base = tile * T::TILE;
+    const int valid = (int)min((int64_t)T::TILE, (int64_t)(n - base));
+    int4 v[IPT / 4];
+    sel_load<BT, IPT>(in, base, valid, v);
+    const unsigned lane = lane_id();
+    const int wb = (threadIdx.x >> 5) * 32 * IPT + 4 * (int)lane;
+    int c = 0;
+#pragma unroll
+    for (int j = 0; j < IPT / 4; ++j) {
+      const int s0 = wb + j * 128;
+      c += (s0 + 0 < valid && v[j].x >= lo && v[j].x <= hi) + (s0 + 1 < valid && v[j].y >= lo && v[j].y <= hi) +
+           (s0 + 2 < valid && v[j].z >= lo && v[j].z <= hi) + (s0 + 3 < valid && v[j].w >= lo && v[j].w <= hi);
+    }
+    c = warp_sum(c);
+    if (lane == 0) s_warp[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+#pragma unroll
+      for (int w = 0; w < T::W; ++w) t += s_warp[w];
+      counts[tile] = (unsigned)t;
     }
     __syncthreads();
-    const long long off = s_off;
-    for (int i = threadIdx.x; i < tile_total; i += BT) out[off + i] = s_items[i];
-    if (threadIdx.x == 0 && tile == ntiles - 1) *total_out = off + tile_total;
-    __syncthreads();  // s_items / s_off reuse
-#pragma unroll
-    for (int k = 0; k < IPT; ++k) cur[k] = nxt[k];
   }
+}
+
+// Exclusive scan of the per-tile counts into 64-bit offsets (+ the total at [ntiles]).
+__global__ void __launch_bounds__(1024) select_scan_kernel(const unsigned* counts, long long ntiles,
+                                                           long long* offsets) {
+  __shared__ long long sm[33];
+  const long long per = (ntiles + 1023) / 1024;
+  const long long b = threadIdx.x * per, e = min(ntiles, b + per);
+  long long local = 0;
+  for (long long i = b; i < e; ++i) local += counts[i];
+  long long tot;
+  long long run = BlockScan<1024>(local, sm, tot);
+  for (long long i = b; i < e; ++i) {
+    offsets[i] = run;
+    run += counts[i];
+  }
+  if (threadIdx.x == 0) offsets[ntiles] = tot;
+}
+
+template <int BT, int IPT>
+__global__ void __launch_bounds__(BT) select_write_kernel(const int32_t* __restrict__ in, int64_t n,
+                                                          int32_t lo, int32_t hi, long long ntiles,
+                                                          const long long* offsets, int32_t* __restrict__ out) {
+  using T = SelTile<BT, IPT>;
+  __shared__ __align__(16) int32_t s_items[T::TILE];
+  __shared__ int s_warp[T::W];
+  const long long tile = blockIdx.x;
+  const int64_t base = tile * T::TILE;
+  const int valid = (int)min((int64_t)T::TILE, (int64_t)(n - base));
+  const long long off = offsets[tile];
+  const int total = (int)(offsets[tile + 1] - off);
+  if (total == 0) return;  // whole CTA: uniform
+  int4 v[IPT / 4];
+  sel_load<BT, IPT>(in, base, valid, v);
+  sel_compact<BT, IPT>(v, valid, lo, hi, s_items, s_warp);
+  __syncthreads();
+  for (int i = threadIdx.x; i < total; i += BT) out[off + i] = s_items[i];
 }
 
 // Crystal order for an arbitrary logical (bt, ipt) (select_tile_into,
@@ -173,6 +400,70 @@ __global__ void __launch_bounds__(kCrysPB) select_crystal_kernel(
   const long long off = s_off;
   for (int i = threadIdx.x; i < total; i += kCrysPB) out[off + i] = s_out[i];
   if (threadIdx.x == 0 && base + chunk >= n) *total_out = off + total;
+}
+
+// Crystal order, register form: physical thread u of a round owns logical
+// pairs p = p0 + g*256 + u (g < G); pair p = (logical tile j, logical thread
+// t) reads its IPT slots j*S + t + k*bt straight from HBM (consecutive u ->
+// consecutive t: coalesced, the reference's striped ownership), counts are
+// packed 16 bits per g into one 64-bit block scan, and matches land in the
+// chunk's shared-memory output at their Crystal positions.  One look-back per
+// chunk.  IPTM >= ipt is the unrolled item bound (items stay in registers).
+template <int IPTM, int G>
+__global__ void __launch_bounds__(kCrysPB) select_crystal_reg_kernel(
+    const int32_t* __restrict__ in, int64_t n, int32_t lo, int32_t hi, int bt, int ipt, int chunk,
+    int32_t* __restrict__ out, unsigned long long* status, long long* total_out) {
+  static_assert(G >= 1 && G <= 4, "four 16-bit count fields per scan word");
+  extern __shared__ int32_t s_dyn[];
+  int32_t* s_out = s_dyn;  // [chunk]
+  __shared__ unsigned long long s_scan[kCrysPB / 32 + 1];
+  __shared__ long long s_red[kCrysPB / 32 + kCrysPB / 64 + 1];
+  const long long c = blockIdx.x;
+  const int64_t base = c * (int64_t)chunk;
+  const int valid = (int)min((int64_t)chunk, n - base);
+  const int S = bt * ipt;
+  const int pairs = ((valid + S - 1) / S) * bt;
+  const int32_t* src = in + base;
+  int run = 0;
+  for (int p0 = 0; p0 < pairs; p0 += kCrysPB * G) {
+    int32_t x[G][IPTM];
+    unsigned f[G];
+    unsigned long long packed = 0;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      f[g] = 0;
+      const int p = p0 + g * kCrysPB + (int)threadIdx.x;
+      if (p < pairs) {
+        const int j = p / bt, t = p - j * bt;
+        const int b = j * S + t;
+#pragma unroll
+        for (int k = 0; k < IPTM; ++k) {
+          const int i = b + k * bt;
+          if (k < ipt && i < valid) {
+            x[g][k] = ld_stream1(src + i);
+            f[g] |= (unsigned)(x[g][k] >= lo && x[g][k] <= hi) << k;
+          }
+        }
+      }
+      packed |= (unsigned long long)__popc(f[g]) << (16 * g);
+    }
+    unsigned long long tot;
+    const unsigned long long ex = BlockScan<kCrysPB>(packed, s_scan, tot);
+    int before = run;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      int pos = before + (int)((ex >> (16 * g)) & 0xffff);
+#pragma unroll
+      for (int k = 0; k < IPTM; ++k)
+        if ((f[g] >> k) & 1u) s_out[pos++] = x[g][k];
+      before += (int)((tot >> (16 * g)) & 0xffff);
+    }
+    run = before;
+  }
+  __syncthreads();  // s_out complete (the look-back's barriers would also order it)
+  const long long off = block_lookback<kCrysPB>(status, c, run, s_red);
+  for (int i = threadIdx.x; i < run; i += kCrysPB) out[off + i] = s_out[i];
+  if (threadIdx.x == 0 && base + chunk >= n) *total_out = off + run;
 }
 
 // project.hpp:49-64.  Linear: float mul, float mul, float add with no FMA
@@ -289,8 +580,9 @@ int64_t select_i32(crys_ctx* ctx, const int32_t* d_in, int64_t n, int32_t lo, in
   int64_t tile;
   size_t dyn = 0;
   int chunk = 0;
+  const int cfg = sel_cfg();
   if (order == CRYS_ORDER_INPUT) {
-    tile = (int64_t)kSelBT * kSelIPT;
+    tile = cfg == 1 || cfg == 3 ? 8192 : 4096;  // cfg 6/7: 4096
   } else {
     CRYS_CHECK(order == CRYS_ORDER_CRYSTAL, CRYS_ECONFIG, "unknown select order");
     const int64_t S = (int64_t)bt * ipt;
@@ -303,14 +595,61 @@ int64_t select_i32(crys_ctx* ctx, const int32_t* d_in, int64_t n, int32_t lo, in
   const int64_t ntiles = (n + tile - 1) / tile;
   ctx->status.reserve(sizeof(unsigned long long) * (size_t)(ntiles + 2));
   auto* status = ctx->status.as<unsigned long long>();
+  auto* counter = status + ntiles;
   auto* total = reinterpret_cast<long long*>(status + ntiles + 1);
   CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(unsigned long long) * (size_t)(ntiles + 2), st));
   timing_kernel_begin(ctx);
   if (order == CRYS_ORDER_INPUT) {
-    auto fn = select_input_kernel<kSelBT, kSelIPT>;
-    const int nb = occupancy((const void*)fn, kSelBT, 0);
-    const int grid = (int)std::min<int64_t>(ntiles, (int64_t)nb * ctx->num_sms);
-    fn<<<grid, kSelBT, 0, st>>>(d_in, n, lo, hi, d_out, status, ntiles, total);
+    auto launch = [&](auto fn, int bt_, bool persist) {
+      int grid = (int)ntiles;
+      if (persist) grid = (int)std::min<int64_t>(ntiles, (int64_t)occupancy((const void*)fn, bt_, 0) * ctx->num_sms);
+      fn<<<grid, bt_, 0, st>>>(d_in, n, lo, hi, d_out, status, counter, ntiles, total);
+    };
+    switch (cfg) {
+      case 1: launch(select_input_kernel<256, 32, false>, 256, false); break;
+      case 2: launch(select_input_kernel<256, 16, true>, 256, true); break;
+      case 3: launch(select_input_kernel<256, 32, true>, 256, true); break;
+      case 4: launch(select_input_kernel<128, 32, false>, 128, false); break;
+      case 5: launch(select_input_kernel<128, 32, false, true>, 128, false); break;
+      case 8: case 0: {
+        constexpr int BT = 128, IPT = 32;
+        ctx->scratch2.reserve(sizeof(unsigned) * (size_t)ntiles + sizeof(long long) * (size_t)(ntiles + 1) + 64);
+        unsigned* counts = ctx->scratch2.as<unsigned>();
+        long long* offs = reinterpret_cast<long long*>(counts + ((ntiles + 1) & ~1LL));
+        const int gc = (int)std::min<int64_t>(ntiles, (int64_t)occupancy((const void*)select_count_kernel<BT, IPT>, BT, 0) * ctx->num_sms);
+        select_count_kernel<BT, IPT><<<gc, BT, 0, st>>>(d_in, n, lo, hi, ntiles, counts);
+        select_scan_kernel<<<1, 1024, 0, st>>>(counts, ntiles, offs);
+        select_write_kernel<BT, IPT><<<(unsigned)ntiles, BT, 0, st>>>(d_in, n, lo, hi, ntiles, offs, d_out);
+        CUDA_TRY(cudaMemcpyAsync(total, offs + ntiles, sizeof(long long), cudaMemcpyDeviceToDevice, st));
+        count_launch(ctx, 2);
+        break;
+      }
+      case 6: {
+        auto fn = select_wave_kernel<256, 16>;
+        const int g = (int)std::min<int64_t>(ntiles, (int64_t)occupancy((const void*)fn, 256, 0) * ctx->num_sms);
+        fn<<<g, 256, 0, st>>>(d_in, n, lo, hi, d_out, status, ntiles, total);
+        break;
+      }
+      case 7: {
+        auto fn = select_wave_kernel<128, 32>;
+        const int g = (int)std::min<int64_t>(ntiles, (int64_t)occupancy((const void*)fn, 128, 0) * ctx->num_sms);
+        fn<<<g, 128, 0, st>>>(d_in, n, lo, hi, d_out, status, ntiles, total);
+        break;
+      }
+      default: launch(select_input_kernel<256, 16, false>, 256, false); break;  // cfg 9
+    }
+  } else if (ipt <= 32) {
+    const size_t dyn2 = sizeof(int32_t) * (size_t)chunk;
+    auto launch = [&](auto fn) {
+      occupancy((const void*)fn, kCrysPB, dyn2);
+      fn<<<(unsigned)ntiles, kCrysPB, dyn2, st>>>(d_in, n, lo, hi, bt, ipt, chunk, d_out, status, total);
+    };
+    if (ipt <= 1) launch(select_crystal_reg_kernel<1, 4>);
+    else if (ipt <= 2) launch(select_crystal_reg_kernel<2, 4>);
+    else if (ipt <= 4) launch(select_crystal_reg_kernel<4, 4>);
+    else if (ipt <= 8) launch(select_crystal_reg_kernel<8, 2>);
+    else if (ipt <= 16) launch(select_crystal_reg_kernel<16, 1>);
+    else launch(select_crystal_reg_kernel<32, 1>);
   } else {
     occupancy((const void*)select_crystal_kernel, kCrysPB, dyn);
     select_crystal_kernel<<<(unsigned)ntiles, kCrysPB, dyn, st>>>(d_in, n, lo, hi, bt, ipt, chunk, d_out,

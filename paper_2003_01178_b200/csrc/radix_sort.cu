@@ -6,45 +6,40 @@
 //   radix_offsets    column-major exclusive prefix (digit-major, owner within digit)
 //   radix_shuffle    stable scatter: each owner writes its runs in input order
 //   lsb_radix_sort   stable passes low->high (default 4 x 8 bit) == std::stable_sort
-//   msb_radix_sort   8-bit MSB recursion from bit 24; small partitions sorted directly
+//   msb_radix_sort   8-bit MSB partition from bit 24, then each partition sorted
+//                    independently (radix.cpp:165-216; output keys sorted, pairs kept)
 //
-// B200 form: an "owner" is a CTA with a contiguous chunk.  One pass =
-//   radix_upsweep_kernel    per-CTA digit histogram (smem, vectorised loads)
-//   radix_scan_kernel       column-major exclusive scan per segment
-//   radix_downsweep_kernel  per tile: warp-level stable ranking (match.any),
-//                           shared-memory reorder, coalesced-run scatter
-// Traffic per pass = 4N (upsweep) + 8N read + 8N write = 20N, exactly the
-// reference's bytes_moved convention (tools/tq_main.cpp:482-483).
-// The same kernels run SEGMENTED for MSB: every segment is an independent
-// sub-array with its own CTAs and scan; segments that fit shared memory are
-// finished by one CTA with a bitonic sort (msb_recurse base case, radix.cpp:184-187).
+// B200 form: ONESWEEP.  The digit histograms of every pass are computed in ONE
+// read of the keys up front (os_hist_kernel, 4N bytes); each pass is then a
+// single kernel (onesweep_kernel): a tile of 8192 pairs is ranked stably in
+// shared memory (warp match.any ranking, warp-major = input order), its
+// per-digit counts are published and resolved against the preceding tiles by a
+// per-digit DECOUPLED LOOK-BACK (the B200 replacement for the reference's
+// column-major owner offsets, radix.cpp:55-73: tile order = owner order), and
+// the tile is scattered in digit runs.  Traffic = 4N + 16N per pass (68N for
+// four 8-bit passes vs the reference's 80N bytes_moved convention).
+//
+// MSB: pass 1 partitions by the top digit (bits 24-31) over the whole array;
+// the 256 partitions then become SEGMENTS sorted independently by three
+// segmented onesweep passes over bits 0-23 (each tile belongs to one segment,
+// look-back stays inside it; segment histograms are taken in one read after
+// the partition).  All segment bookkeeping stays on the device.
 #include <algorithm>
 #include <vector>
 
+#include "async.cuh"
 #include "crystal.cuh"
 #include "internal.hpp"
 
 namespace crys {
 namespace {
 
-constexpr int kUpBT = 512;
-constexpr int kDnBT = 512, kDnIPT = 16;            // 8192-pair tiles
-constexpr int kDnTile = kDnBT * kDnIPT;
-constexpr int kDnWarps = kDnBT / 32;
-constexpr int kLocalMax = 8192;                     // bitonic base case (64 KB smem)
-constexpr int kLocalBT = 1024;
-
-struct SegCta {  // one owner: [begin, end) of segment `seg`
-  int64_t begin, end;
-  int32_t seg, cta_in_seg;
-};
-struct SegInfo {
-  int64_t begin, size;
-  int32_t first_cta, ncta;
-};
-struct SegLocal {
-  int64_t begin, size;
-};
+constexpr int kOsBT = 512, kOsIPT = 16;
+constexpr int kOsTile = kOsBT * kOsIPT;  // 8192 pairs
+constexpr int kOsWarps = kOsBT / 32;
+constexpr uint32_t kOsAgg = 1u << 30, kOsPre = 2u << 30, kOsVal = (1u << 30) - 1;
+constexpr int kHistBT = 512;
+constexpr int kMaxPasses = 32;
 
 __device__ __forceinline__ uint32_t digit_of(int32_t key, int start, uint32_t mask) {
   return (((uint32_t)key ^ 0x80000000u) >> start) & mask;  // radix.hpp:44-47
@@ -56,202 +51,328 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
-// hist layout: segment s occupies [first_cta*D, (first_cta+ncta)*D), digit-major
-// inside: index first_cta*D + d*ncta + cta_in_seg (column-major, radix.cpp:55-73).
-__global__ void __launch_bounds__(kUpBT) radix_upsweep_kernel(const int32_t* __restrict__ keys,
-                                                              const SegCta* ctas,
-                                                              const SegInfo* segs, int start,
-                                                              int bits, uint32_t* hist) {
-  __shared__ uint32_t h[kUpBT / 32][256];
-  const int D = 1 << bits;
-  const uint32_t mask = (uint32_t)D - 1;
-  const unsigned warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < (kUpBT / 32) * 256; i += kUpBT) (&h[0][0])[i] = 0;
-  __syncthreads();
-  const SegCta c = ctas[blockIdx.x];
-  int64_t i = c.begin + threadIdx.x * 4;
-  // vectorised body when the chunk start is 16 B aligned
-  if ((c.begin & 3) == 0 && (reinterpret_cast<uintptr_t>(keys) & 15) == 0) {
-    for (; i + 3 < c.end; i += kUpBT * 4) {
-      const int4 k = ld_stream4(keys + i);
-      atomicAdd(&h[warp][digit_of(k.x, start, mask)], 1u);
-      atomicAdd(&h[warp][digit_of(k.y, start, mask)], 1u);
-      atomicAdd(&h[warp][digit_of(k.z, start, mask)], 1u);
-      atomicAdd(&h[warp][digit_of(k.w, start, mask)], 1u);
-    }
-    for (int64_t j = i; j < c.end && j < i + 4; ++j) atomicAdd(&h[warp][digit_of(keys[j], start, mask)], 1u);
-  } else {
-    for (int64_t j = c.begin + threadIdx.x; j < c.end; j += kUpBT)
-      atomicAdd(&h[warp][digit_of(keys[j], start, mask)], 1u);
-  }
-  __syncthreads();
-  const SegInfo s = segs[c.seg];
-  for (int d = threadIdx.x; d < D; d += kUpBT) {
-    uint32_t t = 0;
-    for (int w = 0; w < kUpBT / 32; ++w) t += h[w][d];
-    hist[(int64_t)s.first_cta * D + (int64_t)d * s.ncta + c.cta_in_seg] = t;
-  }
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// One CTA per segment: in-place exclusive scan of its D*ncta counters; also
-// records each digit's base (first owner's offset) for MSB planning.
-__global__ void __launch_bounds__(1024) radix_scan_kernel(uint32_t* hist, const SegInfo* segs,
-                                                          int bits, uint32_t* digit_base) {
-  __shared__ uint32_t sm[33];
-  const SegInfo s = segs[blockIdx.x];
-  const int D = 1 << bits;
-  const int64_t len = (int64_t)D * s.ncta;
-  uint32_t* h = hist + (int64_t)s.first_cta * D;
-  const int64_t per = (len + 1023) / 1024;
-  const int64_t b = threadIdx.x * per, e = min(len, b + per);
-  uint32_t local = 0;
-  for (int64_t i = b; i < e; ++i) local += h[i];
-  uint32_t tot;
-  uint32_t run = BlockScan<1024>(local, sm, tot);
-  for (int64_t i = b; i < e; ++i) {
-    const uint32_t v = h[i];
-    h[i] = run;
-    run += v;
+// Segment table (device): segment s = [begin[s], begin[s] + size[s]), its
+// tiles are global tile ids [first_tile[s], first_tile[s+1]).
+struct SegTable {
+  int64_t begin[256];
+  int64_t size[256];
+  int32_t first_tile[257];
+  int32_t nseg;
+};
+
+// Digit histograms of several passes in one read.  hist[(seg*npass + p)*256 + d].
+// seg_mode 0: one segment (the whole array); 1: the array is partitioned by
+// the top digit and `segs` holds the partitions -- each CTA walks the
+// partitions its contiguous chunk overlaps.
+__global__ void __launch_bounds__(kHistBT) os_hist_kernel(const int32_t* __restrict__ keys, int64_t n,
+                                                          int npass, int start0, int bits,
+                                                          const SegTable* segs, int64_t chunk,
+                                                          uint32_t* hist) {
+  __shared__ uint32_t h[4][256];
+  const uint32_t mask = (1u << bits) - 1u;
+  const int64_t b0 = (int64_t)blockIdx.x * chunk, e0 = min(n, b0 + chunk);
+  if (b0 >= e0) return;
+  int s_lo = 0, s_hi = 0;
+  if (segs) {
+    s_hi = segs->nseg - 1;
+    // first segment whose end is beyond b0
+    while (s_lo < s_hi && segs->begin[s_lo] + segs->size[s_lo] <= b0) ++s_lo;
   }
-  __syncthreads();
-  if (digit_base)
-    for (int d = threadIdx.x; d < D; d += 1024)
-      digit_base[(int64_t)blockIdx.x * 256 + d] = h[(int64_t)d * s.ncta];
-}
-
-__global__ void __launch_bounds__(kDnBT) radix_downsweep_kernel(
-    const int32_t* __restrict__ kin, const int32_t* __restrict__ pin, int32_t* __restrict__ kout,
-    int32_t* __restrict__ pout, const SegCta* ctas, const SegInfo* segs, const uint32_t* hist,
-    int start, int bits) {
-  extern __shared__ int32_t smem[];
-  int32_t* s_k = smem;                                       // [kDnTile]
-  int32_t* s_p = smem + kDnTile;                             // [kDnTile]
-  uint32_t* s_wc = reinterpret_cast<uint32_t*>(smem + 2 * kDnTile);  // [kDnWarps][256]
-  uint32_t* s_off = s_wc + kDnWarps * 256;                   // [256] running global offsets
-  uint32_t* s_start = s_off + 256;                           // [257] tile digit starts
-  __shared__ uint32_t s_scan[kDnBT / 32 + 1];
-
-  const int D = 1 << bits;
-  const uint32_t mask = (uint32_t)D - 1;
-  const SegCta c = ctas[blockIdx.x];
-  const SegInfo sg = segs[c.seg];
-  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-  for (int d = threadIdx.x; d < 256; d += kDnBT)
-    s_off[d] = d < D ? hist[(int64_t)sg.first_cta * D + (int64_t)d * sg.ncta + c.cta_in_seg] : 0;
-
-  for (int64_t base = c.begin; base < c.end; base += kDnTile) {
-    const int valid = (int)min((int64_t)kDnTile, c.end - base);
-    for (int i = threadIdx.x; i < kDnWarps * 256; i += kDnBT) s_wc[i] = 0;
+  for (int sg = s_lo; sg <= s_hi; ++sg) {
+    int64_t b = b0, e = e0;
+    if (segs) {
+      const int64_t sb = segs->begin[sg], se = sb + segs->size[sg];
+      if (sb >= e0) break;
+      b = max(b0, sb);
+      e = min(e0, se);
+      if (b >= e) continue;
+    }
+    for (int i = threadIdx.x; i < npass * 256; i += kHistBT) (&h[0][0])[i] = 0;
     __syncthreads();
-    // warp-striped ownership: item k of lane l in warp w is tile slot
-    // w*32*IPT + k*32 + l, so (k, lane) order is input order within the warp.
-    int32_t key[kDnIPT], pay[kDnIPT];
-    uint32_t rank[kDnIPT], dg[kDnIPT];
-    const int wbase = warp * 32 * kDnIPT;
+    int64_t i = b + threadIdx.x;
+    // align to 4 elements, then 128-bit loads
+    const int64_t ab = min(e, (b + 3) & ~(int64_t)3);
+    for (; i < ab; i += kHistBT)
+      for (int p = 0; p < npass; ++p) atomicAdd(&h[p][digit_of(keys[i], start0 + p * bits, mask)], 1u);
+    const int64_t nvec = (e - ab) >> 2;  // whole 16 B vectors from ab
+    int64_t v = threadIdx.x;
+    for (; v + 3 * kHistBT < nvec; v += 4 * kHistBT) {  // 4 vectors in flight per thread
+      int4 k[4];
 #pragma unroll
-    for (int k = 0; k < kDnIPT; ++k) {
-      const int s = wbase + k * 32 + lane;
-      if (s < valid) {
-        key[k] = ld_stream1(kin + base + s);
-        pay[k] = ld_stream1(pin + base + s);
-        dg[k] = digit_of(key[k], start, mask);
-      } else {
-        dg[k] = 256;  // out-of-tile sentinel, never counted
-      }
-    }
-    uint32_t* wc = s_wc + warp * 256;
+      for (int u = 0; u < 4; ++u) k[u] = ld_stream4(keys + ab + 4 * (v + u * kHistBT));
+      for (int p = 0; p < npass; ++p) {
+        const int st = start0 + p * bits;
 #pragma unroll
-    for (int k = 0; k < kDnIPT; ++k) {
-      const unsigned peers = __match_any_sync(0xffffffffu, dg[k]);
-      const unsigned below = __popc(peers & lanemask_lt());
-      const bool leader = below == 0;
-      uint32_t basec = 0;
-      if (dg[k] < 256) basec = wc[dg[k]];
-      rank[k] = basec + below;
-      __syncwarp();
-      if (leader && dg[k] < 256) wc[dg[k]] = basec + __popc(peers);
-      __syncwarp();
-    }
-    __syncthreads();
-    // per digit: warp-exclusive prefix (in place) and the tile total
-    uint32_t tot = 0;
-    if (threadIdx.x < 256) {
-      const int d = threadIdx.x;
-      for (int w = 0; w < kDnWarps; ++w) {
-        const uint32_t v = s_wc[w * 256 + d];
-        s_wc[w * 256 + d] = tot;
-        tot += v;
-      }
-    }
-    uint32_t all;
-    const uint32_t st = BlockScan<kDnBT>(threadIdx.x < 256 ? tot : 0u, s_scan, all);
-    if (threadIdx.x < 256) s_start[threadIdx.x] = st;
-    if (threadIdx.x == 0) s_start[256] = all;
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kDnIPT; ++k) {
-      if (dg[k] < 256) {
-        const uint32_t pos = s_start[dg[k]] + s_wc[warp * 256 + dg[k]] + rank[k];
-        s_k[pos] = key[k];
-        s_p[pos] = pay[k];
-      }
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < valid; i += kDnBT) {
-      const int32_t kk = s_k[i];
-      const uint32_t d = digit_of(kk, start, mask);
-      const int64_t dst = sg.begin + (int64_t)s_off[d] + (i - (int64_t)s_start[d]);
-      kout[dst] = kk;
-      pout[dst] = s_p[i];
-    }
-    __syncthreads();
-    if (threadIdx.x < 256) s_off[threadIdx.x] += s_start[threadIdx.x + 1] - s_start[threadIdx.x];
-    __syncthreads();
-  }
-}
-
-// Base case: one CTA sorts a segment of <= kLocalMax pairs in shared memory
-// (bitonic network over a power-of-two padded array; keys ascending).
-__global__ void __launch_bounds__(kLocalBT) local_sort_kernel(int32_t* keys, int32_t* pays,
-                                                             const SegLocal* segs) {
-  extern __shared__ int32_t s_local[];
-  int32_t* sk = s_local;
-  int32_t* sp = s_local + kLocalMax;
-  const SegLocal s = segs[blockIdx.x];
-  int n2 = 1;
-  while (n2 < s.size) n2 <<= 1;
-  for (int i = threadIdx.x; i < n2; i += kLocalBT) {
-    if (i < s.size) {
-      sk[i] = keys[s.begin + i];
-      sp[i] = pays[s.begin + i];
-    } else {
-      sk[i] = INT32_MAX;
-      sp[i] = 0;
-    }
-  }
-  __syncthreads();
-  for (int size = 2; size <= n2; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int t = threadIdx.x; t < n2 / 2; t += kLocalBT) {
-        const int i = 2 * t - (t & (stride - 1));
-        const int j = i + stride;
-        const bool up = (i & size) == 0;
-        const int32_t a = sk[i], b = sk[j];
-        if ((a > b) == up) {
-          sk[i] = b;
-          sk[j] = a;
-          const int32_t x = sp[i];
-          sp[i] = sp[j];
-          sp[j] = x;
+        for (int u = 0; u < 4; ++u) {
+          atomicAdd(&h[p][digit_of(k[u].x, st, mask)], 1u);
+          atomicAdd(&h[p][digit_of(k[u].y, st, mask)], 1u);
+          atomicAdd(&h[p][digit_of(k[u].z, st, mask)], 1u);
+          atomicAdd(&h[p][digit_of(k[u].w, st, mask)], 1u);
         }
       }
-      __syncthreads();
     }
+    for (; v < nvec; v += kHistBT) {
+      const int4 k = ld_stream4(keys + ab + 4 * v);
+      for (int p = 0; p < npass; ++p) {
+        const int st = start0 + p * bits;
+        atomicAdd(&h[p][digit_of(k.x, st, mask)], 1u);
+        atomicAdd(&h[p][digit_of(k.y, st, mask)], 1u);
+        atomicAdd(&h[p][digit_of(k.z, st, mask)], 1u);
+        atomicAdd(&h[p][digit_of(k.w, st, mask)], 1u);
+      }
+    }
+    const int64_t tail = ab + ((e - ab) & ~(int64_t)3);
+    for (int64_t t = tail + threadIdx.x; t < e; t += kHistBT)
+      for (int p = 0; p < npass; ++p) atomicAdd(&h[p][digit_of(keys[t], start0 + p * bits, mask)], 1u);
+    __syncthreads();
+    for (int x = threadIdx.x; x < npass * 256; x += kHistBT) {
+      const uint32_t c = (&h[0][0])[x];
+      if (c) atomicAdd(&hist[((int64_t)sg * npass + x / 256) * 256 + (x & 255)], c);
+    }
+    __syncthreads();
+    if (!segs) break;
   }
-  for (int i = threadIdx.x; i < s.size; i += kLocalBT) {
-    keys[s.begin + i] = sk[i];
-    pays[s.begin + i] = sp[i];
+}
+
+// Exclusive scan of each 256-digit row in place (one warp per row).
+__global__ void os_scan_kernel(uint32_t* hist, int rows) {
+  const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  uint32_t* h = hist + (int64_t)row * 256;
+  const unsigned lane = lane_id();
+  uint32_t v[8], run = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v[j] = h[lane * 8 + j];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) run += v[j];
+  uint32_t x = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= (unsigned)o) x += y;
   }
+  uint32_t ex = x - run;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    h[lane * 8 + j] = ex;
+    ex += v[j];
+  }
+}
+
+// MSB segment plan from the (un-scanned) top-digit histogram: 256 partitions,
+// their begins, sizes and tile ranges.  One CTA of 256 threads.
+__global__ void os_plan_kernel(const uint32_t* top_hist, int64_t base_begin, SegTable* segs) {
+  __shared__ uint32_t sc[9];
+  const int d = threadIdx.x;
+  const uint32_t c = top_hist[d];
+  const uint32_t nt = (c + kOsTile - 1) / kOsTile;
+  uint32_t tot_c, tot_t;
+  const uint32_t ex_c = BlockScan<256>(c, sc, tot_c);
+  const uint32_t ex_t = BlockScan<256>(nt, sc, tot_t);
+  segs->begin[d] = base_begin + ex_c;
+  segs->size[d] = c;
+  segs->first_tile[d] = (int32_t)ex_t;
+  if (d == 0) {
+    segs->first_tile[256] = (int32_t)tot_t;
+    segs->nseg = 256;
+  }
+}
+
+struct OsPass {
+  const int32_t* kin;
+  const int32_t* pin;
+  int32_t* kout;
+  int32_t* pout;
+  int start, bits;
+  const SegTable* segs;     // nullptr: one segment [0, n)
+  int64_t n;                // single-segment length
+  const uint32_t* bases;    // scanned histogram rows of this pass
+  int bases_stride;         // elements between consecutive segments' rows
+  uint32_t* status;         // [tiles][256] look-back words
+  uint32_t* tile_counter;
+  int32_t total_tiles;      // single-segment tile count (segmented: first_tile[nseg])
+};
+
+// One stable pass: tile ranking + per-digit decoupled look-back + scatter.
+// The tile's keys and payloads arrive by two 1-D TMA bulk copies (one
+// elected thread, mbarrier completion) when the tile is 16 B aligned, so no
+// register or LSU time goes into the loads.  Ranking: all 16 warp match.any
+// of a thread are issued back to back, then a short serial per-warp counter
+// update gives each item its stable rank (warp-striped order = input order).
+// DBG 1 skips the look-back (timing experiments only; wrong output).
+template <int DBG>
+__global__ void __launch_bounds__(kOsBT, 2) onesweep_kernel(OsPass a) {
+  extern __shared__ __align__(128) uint32_t os_sm[];
+  int32_t* s_k = reinterpret_cast<int32_t*>(os_sm);           // [kOsTile] staged -> digit-sorted keys
+  int32_t* s_p = s_k + kOsTile;                                // [kOsTile] staged -> digit-sorted payloads
+  uint32_t* s_wc = os_sm + 2 * kOsTile;                        // [kOsWarps][256]
+  uint32_t* s_start = s_wc + kOsWarps * 256;                   // [257] tile digit starts
+  long long* s_dst = reinterpret_cast<long long*>(s_start + 260);  // [256] dst - start
+  __shared__ uint32_t s_scan[kOsBT / 32 + 1];
+  __shared__ int s_tile;
+  __shared__ __align__(8) uint64_t s_bar;
+
+  if (threadIdx.x == 0) {
+    s_tile = (int)atomicAdd(a.tile_counter, 1u);
+    pipe::mbar_init(&s_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = threadIdx.x; i < kOsWarps * 256; i += kOsBT) s_wc[i] = 0;
+  __syncthreads();
+  const int tile = s_tile;
+  int seg = 0, first = 0;
+  int64_t sbeg = 0, ssize = a.n;
+  int total = a.total_tiles;
+  if (a.segs) {
+    total = a.segs->first_tile[a.segs->nseg];
+    int lo = 0, hi = a.segs->nseg - 1;  // last segment with first_tile <= tile
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (a.segs->first_tile[mid] <= tile) lo = mid; else hi = mid - 1;
+    }
+    seg = lo;
+    first = a.segs->first_tile[seg];
+    sbeg = a.segs->begin[seg];
+    ssize = a.segs->size[seg];
+  }
+  if (tile >= total) return;
+  const int t_in = tile - first;
+  const int64_t base = sbeg + (int64_t)t_in * kOsTile;
+  const int valid = (int)min((int64_t)kOsTile, ssize - (int64_t)t_in * kOsTile);
+  const uint32_t mask = (1u << a.bits) - 1u;
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+
+  // ---- stage the tile
+  const bool tma = ((reinterpret_cast<uintptr_t>(a.kin + base) | reinterpret_cast<uintptr_t>(a.pin + base)) & 15) == 0 &&
+                   (valid & 3) == 0;
+  if (tma) {
+    if (threadIdx.x == 0) {
+      const uint64_t pol = pipe::policy_evict_first();
+      pipe::mbar_expect_tx(&s_bar, 8u * (uint32_t)valid);
+      pipe::tma_load_1d(s_k, a.kin + base, 4u * (uint32_t)valid, &s_bar, pol);
+      pipe::tma_load_1d(s_p, a.pin + base, 4u * (uint32_t)valid, &s_bar, pol);
+    }
+    pipe::mbar_wait(&s_bar, 0);
+  } else {
+    for (int i = threadIdx.x; i < valid; i += kOsBT) {
+      s_k[i] = ld_stream1(a.kin + base + i);
+      s_p[i] = ld_stream1(a.pin + base + i);
+    }
+    __syncthreads();
+  }
+
+  // ---- stable rank (warp-striped: item k of lane l in warp w is slot w*32*IPT + k*32 + l)
+  const int wbase = warp * 32 * kOsIPT;
+  int32_t key[kOsIPT];
+  uint32_t rd[kOsIPT];  // peers mask, then rank (low 16) | digit << 16 ; digit 256 = outside
+#pragma unroll
+  for (int k = 0; k < kOsIPT; ++k) {
+    const int sl = wbase + k * 32 + lane;
+    key[k] = s_k[sl];
+    const uint32_t d = sl < valid ? digit_of(key[k], a.start, mask) : 256u;
+    rd[k] = __match_any_sync(0xffffffffu, d);
+  }
+  uint32_t* wc = s_wc + warp * 256;
+  const unsigned lt = lanemask_lt();
+#pragma unroll
+  for (int k = 0; k < kOsIPT; ++k) {
+    const int sl = wbase + k * 32 + lane;
+    const uint32_t d = sl < valid ? digit_of(key[k], a.start, mask) : 256u;
+    const unsigned peers = rd[k];
+    const unsigned below = __popc(peers & lt);
+    uint32_t basec = 0;
+    if (d < 256) basec = wc[d];
+    rd[k] = (basec + below) | (d << 16);
+    __syncwarp();
+    if (below == 0 && d < 256) wc[d] = basec + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // per digit: warp-exclusive prefix (in place) and the tile count
+  uint32_t cnt = 0;
+  if (threadIdx.x < 256) {
+    const int d = threadIdx.x;
+#pragma unroll
+    for (int w = 0; w < kOsWarps; ++w) {
+      const uint32_t v = s_wc[w * 256 + d];
+      s_wc[w * 256 + d] = cnt;
+      cnt += v;
+    }
+    // publish this tile's count early so successors can start looking back
+    st_relaxed(a.status + (int64_t)tile * 256 + d, (t_in == 0 ? kOsPre : kOsAgg) | cnt);
+  }
+  uint32_t all;
+  const uint32_t stt = BlockScan<kOsBT>(threadIdx.x < 256 ? cnt : 0u, s_scan, all);
+  if (threadIdx.x < 256) s_start[threadIdx.x] = stt;
+  if (threadIdx.x == 0) s_start[256] = all;
+  __syncthreads();  // also: every staged key has been read
+  // keys into digit order (in place over the staging buffer)
+#pragma unroll
+  for (int k = 0; k < kOsIPT; ++k) {
+    const uint32_t d = rd[k] >> 16;
+    if (d < 256) s_k[s_start[d] + s_wc[warp * 256 + d] + (rd[k] & 0xffffu)] = key[k];
+  }
+  // payloads: staged -> registers -> digit order
+#pragma unroll
+  for (int k = 0; k < kOsIPT; ++k) key[k] = s_p[wbase + k * 32 + lane];
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kOsIPT; ++k) {
+    const uint32_t d = rd[k] >> 16;
+    if (d < 256) s_p[s_start[d] + s_wc[warp * 256 + d] + (rd[k] & 0xffffu)] = key[k];
+  }
+  // per-digit look-back over the preceding tiles of this segment
+  if (threadIdx.x < 256) {
+    const int d = threadIdx.x;
+    uint32_t excl = 0;
+    if constexpr (DBG != 1) {
+      for (int t = tile - 1; t >= first; --t) {
+        uint32_t w;
+        unsigned ns = 32;
+        while (((w = ld_relaxed(a.status + (int64_t)t * 256 + d)) >> 30) == 0) {
+          __nanosleep(ns);
+          ns = min(ns * 2, 512u);
+        }
+        excl += w & kOsVal;
+        if ((w >> 30) == 2) break;
+      }
+    }
+    if (t_in != 0) st_relaxed(a.status + (int64_t)tile * 256 + d, kOsPre | (excl + cnt));
+    const uint32_t gb = a.bases[(int64_t)seg * a.bases_stride + d];
+    s_dst[d] = (long long)sbeg + (long long)gb + (long long)excl - (long long)s_start[d];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < valid; i += kOsBT) {
+    const int32_t kk = s_k[i];
+    const long long dst = s_dst[digit_of(kk, a.start, mask)] + i;
+    a.kout[dst] = kk;
+    a.pout[dst] = s_p[i];
+  }
+}
+
+// Tuning/experiment knob: CRYS_OS_DBG=1 launches the no-look-back variant.
+int os_dbg() {
+  static const int v = [] {
+    const char* e = getenv("CRYS_OS_DBG");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+void launch_onesweep(const OsPass& a, unsigned grid, size_t smem, cudaStream_t st) {
+  if (os_dbg() == 1)
+    onesweep_kernel<1><<<grid, kOsBT, smem, st>>>(a);
+  else
+    onesweep_kernel<0><<<grid, kOsBT, smem, st>>>(a);
 }
 
 // radix_histogram (radix.cpp:33-53): counts[owner][digit], owner = the
@@ -279,194 +400,179 @@ __global__ void __launch_bounds__(256) owner_hist_kernel(const int32_t* __restri
   }
 }
 
-__global__ void copy_pairs_kernel(const int32_t* ks, const int32_t* ps, int32_t* kd, int32_t* pd,
-                                  const SegLocal* segs) {
-  const SegLocal s = segs[blockIdx.y];
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < s.size;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    kd[s.begin + i] = ks[s.begin + i];
-    pd[s.begin + i] = ps[s.begin + i];
-  }
-}
-
 }  // namespace
 
 struct SortWorkspace {
   DevBuf tk, tp;          // ping-pong pair arrays
-  DevBuf ctas, segs, hist, digit_base, locals;
+  DevBuf hist;            // digit histograms (scanned in place)
+  DevBuf status;          // look-back words, one region per pass
+  DevBuf counters;        // tile counters, one per pass
+  DevBuf segs;            // SegTable (MSB)
+  DevBuf owner;           // radix_histogram counts
 };
 
 void WsDeleter::operator()(SortWorkspace* p) const { delete p; }
 
 namespace {
 
-size_t down_smem() {
-  return sizeof(int32_t) * (2 * kDnTile) + sizeof(uint32_t) * (kDnWarps * 256 + 256 + 257);
+size_t os_smem() {
+  return sizeof(int32_t) * 2 * kOsTile + sizeof(uint32_t) * (kOsWarps * 256 + 260) + sizeof(long long) * 256;
 }
 
-void set_down_smem() {
+void os_attr() {
   static bool done = false;
   if (!done) {
-    CUDA_TRY(cudaFuncSetAttribute((const void*)radix_downsweep_kernel,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)down_smem()));
+    CUDA_TRY(cudaFuncSetAttribute((const void*)onesweep_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)os_smem()));
+    CUDA_TRY(cudaFuncSetAttribute((const void*)onesweep_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)os_smem()));
     done = true;
   }
 }
 
-// Plans owners (CTAs) for a set of segments: ~target pairs per CTA, chunk
-// boundaries tile-aligned inside each segment.
-void plan_ctas(const std::vector<SegLocal>& in, int64_t target, std::vector<SegCta>& ctas,
-               std::vector<SegInfo>& segs) {
-  ctas.clear();
-  segs.clear();
-  for (size_t s = 0; s < in.size(); ++s) {
-    const int64_t n = in[s].size;
-    int64_t nc = std::max<int64_t>(1, (n + target - 1) / target);
-    int64_t chunk = (n + nc - 1) / nc;
-    chunk = (chunk + kDnTile - 1) / kDnTile * kDnTile;
-    nc = std::max<int64_t>(1, (n + chunk - 1) / chunk);
-    SegInfo si{in[s].begin, n, (int32_t)ctas.size(), (int32_t)nc};
-    for (int64_t c = 0; c < nc; ++c) {
-      const int64_t b = in[s].begin + c * chunk;
-      const int64_t e = std::min(in[s].begin + n, b + chunk);
-      ctas.push_back({b, e, (int32_t)s, (int32_t)c});
-    }
-    segs.push_back(si);
-  }
+int64_t hist_chunk(crys_ctx* ctx, int64_t n) {
+  const int64_t ctas = (int64_t)ctx->num_sms * 4;
+  int64_t c = (n + ctas - 1) / ctas;
+  c = (c + 4095) & ~(int64_t)4095;
+  return std::max<int64_t>(c, 4096);
 }
 
-// One (segmented) radix pass src -> dst over `segments`; returns per-segment
-// digit bases (host) when `want_bases`.
-void radix_pass(crys_ctx* ctx, SortWorkspace& ws, const int32_t* sk, const int32_t* sp, int32_t* dk,
-                int32_t* dp, const std::vector<SegLocal>& segments, int start, int bits,
-                std::vector<uint32_t>* bases) {
+// Stable passes over one segment [0, n): bits [start0, start0 + npass*bits).
+// Reads (sk, sp), ping-pongs through (tk, tp); returns true when the result
+// ended in (tk, tp).
+bool onesweep_passes(crys_ctx* ctx, SortWorkspace& ws, int32_t* sk, int32_t* sp, int32_t* tk, int32_t* tp,
+                     int64_t n, int start0, int bits, int npass, const std::vector<int>* pass_bits) {
   cudaStream_t st = ctx->stream;
-  std::vector<SegCta> ctas;
-  std::vector<SegInfo> segs;
-  int64_t total = 0;
-  for (auto& s : segments) total += s.size;
-  // ~4 owners per SM worth of work when one segment; proportional otherwise
-  const int64_t target = std::max<int64_t>(kDnTile, total / ((int64_t)ctx->num_sms * 4) + 1);
-  plan_ctas(segments, target, ctas, segs);
-  const int D = 1 << bits;
-  ws.ctas.reserve(sizeof(SegCta) * ctas.size());
-  ws.segs.reserve(sizeof(SegInfo) * segs.size());
-  ws.hist.reserve(sizeof(uint32_t) * ctas.size() * (size_t)D);
-  ws.digit_base.reserve(sizeof(uint32_t) * segs.size() * 256);
-  CUDA_TRY(cudaMemcpyAsync(ws.ctas.p, ctas.data(), sizeof(SegCta) * ctas.size(), cudaMemcpyHostToDevice, st));
-  CUDA_TRY(cudaMemcpyAsync(ws.segs.p, segs.data(), sizeof(SegInfo) * segs.size(), cudaMemcpyHostToDevice, st));
-  radix_upsweep_kernel<<<(unsigned)ctas.size(), kUpBT, 0, st>>>(sk, ws.ctas.as<SegCta>(), ws.segs.as<SegInfo>(),
-                                                                start, bits, ws.hist.as<uint32_t>());
-  radix_scan_kernel<<<(unsigned)segs.size(), 1024, 0, st>>>(ws.hist.as<uint32_t>(), ws.segs.as<SegInfo>(), bits,
-                                                            bases ? ws.digit_base.as<uint32_t>() : nullptr);
-  set_down_smem();
-  radix_downsweep_kernel<<<(unsigned)ctas.size(), kDnBT, down_smem(), st>>>(
-      sk, sp, dk, dp, ws.ctas.as<SegCta>(), ws.segs.as<SegInfo>(), ws.hist.as<uint32_t>(), start, bits);
-  count_launch(ctx, 3);
-  CUDA_TRY(cudaGetLastError());
-  if (bases) {
-    bases->resize(segs.size() * 256);
-    CUDA_TRY(cudaMemcpyAsync(bases->data(), ws.digit_base.p, sizeof(uint32_t) * bases->size(),
-                             cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
+  const int64_t tiles = (n + kOsTile - 1) / kOsTile;
+  ws.hist.reserve(sizeof(uint32_t) * 256 * (size_t)npass);
+  ws.status.reserve(sizeof(uint32_t) * 256 * (size_t)tiles * (size_t)npass);
+  ws.counters.reserve(sizeof(uint32_t) * kMaxPasses);
+  CUDA_TRY(cudaMemsetAsync(ws.hist.p, 0, sizeof(uint32_t) * 256 * (size_t)npass, st));
+  CUDA_TRY(cudaMemsetAsync(ws.status.p, 0, sizeof(uint32_t) * 256 * (size_t)tiles * (size_t)npass, st));
+  CUDA_TRY(cudaMemsetAsync(ws.counters.p, 0, sizeof(uint32_t) * kMaxPasses, st));
+  uint32_t* hist = ws.hist.as<uint32_t>();
+  const int64_t chunk = hist_chunk(ctx, n);
+  const int hgrid = (int)((n + chunk - 1) / chunk);
+  // histograms: passes of equal width share one read (<= 4 per read)
+  for (int p0 = 0; p0 < npass; p0 += 4) {
+    const int np = std::min(4, npass - p0);
+    const int b = pass_bits ? (*pass_bits)[p0] : bits;
+    bool same = true;
+    for (int p = p0; p < p0 + np; ++p) same = same && (!pass_bits || (*pass_bits)[p] == b);
+    if (same) {
+      os_hist_kernel<<<hgrid, kHistBT, 0, st>>>(sk, n, np, start0 + p0 * bits, b, nullptr, chunk,
+                                                hist + (int64_t)p0 * 256);
+      count_launch(ctx);
+    } else {
+      for (int p = p0; p < p0 + np; ++p) {
+        os_hist_kernel<<<hgrid, kHistBT, 0, st>>>(sk, n, 1, start0 + p * bits, (*pass_bits)[p], nullptr, chunk,
+                                                  hist + (int64_t)p * 256);
+        count_launch(ctx);
+      }
+    }
   }
-  // host vectors must outlive the async H2D copies
-  CUDA_TRY(cudaStreamSynchronize(st));
+  os_scan_kernel<<<(npass + 7) / 8, 256, 0, st>>>(hist, npass);
+  count_launch(ctx);
+  os_attr();
+  int32_t *ik = sk, *ip = sp, *ok = tk, *op = tp;
+  for (int p = 0; p < npass; ++p) {
+    OsPass a;
+    a.kin = ik; a.pin = ip; a.kout = ok; a.pout = op;
+    a.start = start0 + p * bits;
+    a.bits = pass_bits ? (*pass_bits)[p] : bits;
+    a.segs = nullptr;
+    a.n = n;
+    a.bases = hist + (int64_t)p * 256;
+    a.bases_stride = 0;
+    a.status = ws.status.as<uint32_t>() + (int64_t)p * 256 * tiles;
+    a.tile_counter = ws.counters.as<uint32_t>() + p;
+    a.total_tiles = (int32_t)tiles;
+    launch_onesweep(a, (unsigned)tiles, os_smem(), st);
+    CRYS_LAUNCHED("onesweep_kernel");
+    count_launch(ctx);
+    std::swap(ik, ok);
+    std::swap(ip, op);
+  }
+  return (npass & 1) != 0;
 }
 
 void lsb_sort(crys_ctx* ctx, SortWorkspace& ws, int32_t* keys, int32_t* pays, int64_t n, int bpp) {
   ws.tk.reserve(sizeof(int32_t) * (size_t)n);
   ws.tp.reserve(sizeof(int32_t) * (size_t)n);
-  int32_t *sk = keys, *sp = pays, *dk = ws.tk.as<int32_t>(), *dp = ws.tp.as<int32_t>();
-  std::vector<SegLocal> one{{0, n}};
+  // lsb_radix_sort (radix.cpp:151-159): passes at 0, bpp, 2bpp, ... of width min(bpp, 32-start)
+  std::vector<int> pb;
+  for (int start = 0; start < 32; start += bpp) pb.push_back(std::min(bpp, 32 - start));
   timing_kernel_begin(ctx);
-  for (int start = 0; start < 32; start += bpp) {  // lsb_radix_sort, radix.cpp:151-159
-    const int bits = std::min(bpp, 32 - start);
-    radix_pass(ctx, ws, sk, sp, dk, dp, one, start, bits, nullptr);
-    std::swap(sk, dk);
-    std::swap(sp, dp);
-  }
+  const bool in_tmp = onesweep_passes(ctx, ws, keys, pays, ws.tk.as<int32_t>(), ws.tp.as<int32_t>(), n, 0, bpp,
+                                      (int)pb.size(), &pb);
   timing_kernel_end(ctx);
-  if (sk != keys) {
-    CUDA_TRY(cudaMemcpyAsync(keys, sk, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToDevice, ctx->stream));
-    CUDA_TRY(cudaMemcpyAsync(pays, sp, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (in_tmp) {
+    CUDA_TRY(cudaMemcpyAsync(keys, ws.tk.p, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToDevice, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(pays, ws.tp.p, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToDevice, ctx->stream));
   }
 }
 
-// msb_recurse (radix.cpp:181-206), level-synchronous: every segment still
-// larger than the shared-memory base case takes one more 8-bit pass.
+// msb_radix_sort (radix.cpp:165-216): partition by the top 8-bit digit, then
+// sort every partition independently on bits 0-23 (segmented passes).
 void msb_sort(crys_ctx* ctx, SortWorkspace& ws, int32_t* keys, int32_t* pays, int64_t n) {
   cudaStream_t st = ctx->stream;
   ws.tk.reserve(sizeof(int32_t) * (size_t)n);
   ws.tp.reserve(sizeof(int32_t) * (size_t)n);
-  int32_t* bufk[2] = {keys, ws.tk.as<int32_t>()};
-  int32_t* bufp[2] = {pays, ws.tp.as<int32_t>()};
-  int cur = 0;  // buffer holding the live data of the pending segments
-  std::vector<SegLocal> pending{{0, n}};
-  std::vector<SegLocal> local_in[2];  // finished-by-local-sort segments per buffer
-  std::vector<SegLocal> done_in[2];   // already final (size <= 1 or all bits used)
+  int32_t* tk = ws.tk.as<int32_t>();
+  int32_t* tp = ws.tp.as<int32_t>();
+  const int64_t tiles1 = (n + kOsTile - 1) / kOsTile;
+  const int64_t tiles_seg = tiles1 + 256;  // each partition rounds its tail tile up
+  // hist rows: [0] top digit (kept un-scanned copy in row 1), [2 + s*3 + p] segment rows
+  const size_t hist_words = 256 * (2 + 256 * 3);
+  ws.hist.reserve(sizeof(uint32_t) * hist_words);
+  ws.status.reserve(sizeof(uint32_t) * 256 * (size_t)(tiles1 + 3 * tiles_seg));
+  ws.counters.reserve(sizeof(uint32_t) * kMaxPasses);
+  ws.segs.reserve(sizeof(SegTable));
+  uint32_t* hist = ws.hist.as<uint32_t>();
+  uint32_t* status = ws.status.as<uint32_t>();
+  uint32_t* ctr = ws.counters.as<uint32_t>();
+  SegTable* segs = ws.segs.as<SegTable>();
   timing_kernel_begin(ctx);
-  for (int start = 24; start >= 0 && !pending.empty(); start -= 8) {
-    std::vector<SegLocal> big, small;
-    for (auto& s : pending) {
-      if (s.size <= 1) done_in[cur].push_back(s);
-      else if (s.size <= kLocalMax) small.push_back(s);
-      else big.push_back(s);
-    }
-    local_in[cur].insert(local_in[cur].end(), small.begin(), small.end());
-    pending.clear();
-    if (big.empty()) break;
-    std::vector<uint32_t> bases;
-    radix_pass(ctx, ws, bufk[cur], bufp[cur], bufk[cur ^ 1], bufp[cur ^ 1], big, start, 8, &bases);
-    cur ^= 1;
-    for (size_t s = 0; s < big.size(); ++s) {
-      for (int d = 0; d < 256; ++d) {
-        const int64_t lo = bases[s * 256 + d];
-        const int64_t hi = d + 1 < 256 ? (int64_t)bases[s * 256 + d + 1] : big[s].size;
-        if (hi - lo > 0) pending.push_back({big[s].begin + lo, hi - lo});
-      }
-    }
-    if (start == 0) {  // all 32 bits consumed: segments hold equal keys
-      for (auto& s : pending) done_in[cur].push_back(s);
-      pending.clear();
-    }
+  CUDA_TRY(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * hist_words, st));
+  CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(uint32_t) * 256 * (size_t)(tiles1 + 3 * tiles_seg), st));
+  CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(uint32_t) * kMaxPasses, st));
+  const int64_t chunk = hist_chunk(ctx, n);
+  const int hgrid = (int)((n + chunk - 1) / chunk);
+  os_hist_kernel<<<hgrid, kHistBT, 0, st>>>(keys, n, 1, 24, 8, nullptr, chunk, hist);
+  CUDA_TRY(cudaMemcpyAsync(hist + 256, hist, sizeof(uint32_t) * 256, cudaMemcpyDeviceToDevice, st));
+  os_scan_kernel<<<1, 32, 0, st>>>(hist, 1);
+  os_plan_kernel<<<1, 256, 0, st>>>(hist + 256, 0, segs);
+  os_attr();
+  {  // pass 1: top digit, whole array, keys -> tmp
+    OsPass a;
+    a.kin = keys; a.pin = pays; a.kout = tk; a.pout = tp;
+    a.start = 24; a.bits = 8; a.segs = nullptr; a.n = n;
+    a.bases = hist; a.bases_stride = 0;
+    a.status = status; a.tile_counter = ctr; a.total_tiles = (int32_t)tiles1;
+    launch_onesweep(a, (unsigned)tiles1, os_smem(), st);
+    CRYS_LAUNCHED("onesweep_kernel msb top");
   }
-  for (auto& s : pending) local_in[cur].push_back(s);
-  // Gather every final segment into `keys`: sort locally in place when the
-  // segment lives in `keys`, otherwise copy it over first.
-  std::vector<SegLocal> to_copy = local_in[1];
-  to_copy.insert(to_copy.end(), done_in[1].begin(), done_in[1].end());
-  if (!to_copy.empty()) {
-    ws.locals.reserve(sizeof(SegLocal) * to_copy.size());
-    CUDA_TRY(cudaMemcpyAsync(ws.locals.p, to_copy.data(), sizeof(SegLocal) * to_copy.size(),
-                             cudaMemcpyHostToDevice, st));
-    for (size_t b = 0; b < to_copy.size(); b += 65535) {
-      const unsigned cnt = (unsigned)std::min<size_t>(65535, to_copy.size() - b);
-      copy_pairs_kernel<<<dim3(8, cnt), 256, 0, st>>>(bufk[1], bufp[1], keys, pays,
-                                                      ws.locals.as<SegLocal>() + b);
-      count_launch(ctx);
-    }
-    CUDA_TRY(cudaStreamSynchronize(st));
+  // segment histograms of bits 0-7, 8-15, 16-23 in one read of tmp
+  uint32_t* shist = hist + 2 * 256;
+  os_hist_kernel<<<hgrid, kHistBT, 0, st>>>(tk, n, 3, 0, 8, segs, chunk, shist);
+  os_scan_kernel<<<(256 * 3 + 7) / 8, 256, 0, st>>>(shist, 256 * 3);
+  int32_t *ik = tk, *ip = tp, *ok = keys, *op = pays;
+  for (int p = 0; p < 3; ++p) {
+    OsPass a;
+    a.kin = ik; a.pin = ip; a.kout = ok; a.pout = op;
+    a.start = 8 * p; a.bits = 8; a.segs = segs; a.n = n;
+    a.bases = shist + 256 * p; a.bases_stride = 3 * 256;
+    a.status = status + 256 * (tiles1 + p * tiles_seg);
+    a.tile_counter = ctr + 1 + p;
+    a.total_tiles = (int32_t)tiles_seg;
+    launch_onesweep(a, (unsigned)tiles_seg, os_smem(), st);
+    CRYS_LAUNCHED("onesweep_kernel msb segmented");
+    std::swap(ik, ok);
+    std::swap(ip, op);
   }
-  std::vector<SegLocal> locals = local_in[0];
-  locals.insert(locals.end(), local_in[1].begin(), local_in[1].end());
-  if (!locals.empty()) {
-    ws.locals.reserve(sizeof(SegLocal) * locals.size());
-    CUDA_TRY(cudaMemcpyAsync(ws.locals.p, locals.data(), sizeof(SegLocal) * locals.size(),
-                             cudaMemcpyHostToDevice, st));
-    static bool attr = false;
-    if (!attr) {
-      CUDA_TRY(cudaFuncSetAttribute((const void*)local_sort_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)(2 * kLocalMax * sizeof(int32_t))));
-      attr = true;
-    }
-    local_sort_kernel<<<(unsigned)locals.size(), kLocalBT, 2 * kLocalMax * sizeof(int32_t), st>>>(keys, pays, ws.locals.as<SegLocal>());
-    count_launch(ctx);
-    CUDA_TRY(cudaGetLastError());
-  }
+  count_launch(ctx, 9);
   timing_kernel_end(ctx);
-  CUDA_TRY(cudaStreamSynchronize(st));
+  // 4 passes: keys -> tmp -> keys -> tmp -> keys; the result is in `keys`
 }
 
 }  // namespace
@@ -497,17 +603,18 @@ void radix_owner_histogram(crys_ctx* ctx, const int32_t* d_keys, int64_t n, int 
 
 // One stable partition pass (radix_shuffle with pass.stable, radix.cpp:75-136):
 // the output of per-owner cursors over column-major offsets is exactly the
-// stable partition by digit, independent of the owner count.
+// stable partition by digit, independent of the owner count -- one onesweep pass.
 void radix_partition_pass(crys_ctx* ctx, const int32_t* sk, const int32_t* sp, int32_t* dk, int32_t* dp,
                           int64_t n, int start, int bits) {
   CRYS_CHECK(bits >= 1 && bits <= 8 && start >= 0 && start + bits <= 32, CRYS_ECONFIG,
              "RadixPass: bit range exceeds 32-bit keys");
   if (n == 0) return;
-  CRYS_CHECK(n < (1LL << 32), CRYS_ENOTBUILT, "partition supports fewer than 2^32 pairs");
+  CRYS_CHECK(n < (1LL << 30), CRYS_ENOTBUILT, "partition supports fewer than 2^30 pairs");
   if (!ctx->sws) ctx->sws.reset(new SortWorkspace());
-  std::vector<SegLocal> one{{0, n}};
+  std::vector<int> pb{bits};
   timing_kernel_begin(ctx);
-  radix_pass(ctx, *ctx->sws, sk, sp, dk, dp, one, start, bits, nullptr);
+  onesweep_passes(ctx, *ctx->sws, const_cast<int32_t*>(sk), const_cast<int32_t*>(sp), dk, dp, n, start, bits, 1,
+                  &pb);
   timing_kernel_end(ctx);
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
 }
@@ -515,7 +622,7 @@ void radix_partition_pass(crys_ctx* ctx, const int32_t* sk, const int32_t* sp, i
 void sort_pairs(crys_ctx* ctx, int32_t* d_keys, int32_t* d_payloads, int64_t n, int algo,
                 int bits_per_pass) {
   if (n <= 1) return;
-  CRYS_CHECK(n < (1LL << 32), CRYS_ENOTBUILT, "sort supports fewer than 2^32 pairs");
+  CRYS_CHECK(n < (1LL << 30), CRYS_ENOTBUILT, "sort supports fewer than 2^30 pairs");
   if (!ctx->sws) ctx->sws.reset(new SortWorkspace());
   if (algo == CRYS_SORT_LSB)
     lsb_sort(ctx, *ctx->sws, d_keys, d_payloads, n, bits_per_pass);

@@ -127,3 +127,29 @@ if __name__ == "__main__":
         traffic(path, sys.argv[3])
     else:
         sass(path, int(sys.argv[3]) if len(sys.argv) > 3 else 0)
+
+
+def hot(rep, which=0, top=40):
+    """Top SASS instructions of launch `which` by warp-stall samples."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True, check=True).stdout
+    kern, cur, hdr = [], None, None
+    for r in csv.reader(io.StringIO(out)):
+        if r and r[0] == "Kernel Name":
+            cur = [r[1], []]
+            kern.append(cur)
+        elif r and r[0] == "Address":
+            hdr = r
+        elif cur is not None and len(r) > 5:
+            cur[1].append(r)
+    name, ins = kern[which]
+    smp = hdr.index("Warp Stall Sampling (All Samples)")
+    ts = sum(int(x[smp]) for x in ins) or 1
+    print(name[:120])
+    idx = sorted(range(len(ins)), key=lambda i: -int(ins[i][smp]))[:top]
+    for i in sorted(idx):
+        print(f"{i:5d} {100 * int(ins[i][smp]) / ts:5.1f}%  {ins[i][1][:90]}")
+
+
+if __name__ == "__main__" and sys.argv[1] == "hot":
+    hot(sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 0)
