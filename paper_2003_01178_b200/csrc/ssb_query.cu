@@ -161,6 +161,13 @@ __global__ void dim_filter_kernel(const DimBuildArgs a) {
   const DimBuildDesc& d = a.d[blockIdx.y];
   HtMeta* m = a.meta + blockIdx.y;
   const unsigned lane = lane_id();
+  // build size: per-warp atomics only where the compaction needs positions
+  // (kTabHash); direct tables count in shared memory, one global add per CTA
+  // (a per-warp add to one address serialised ~30 us on the 1 M-row part table)
+  __shared__ int s_count;
+  if (threadIdx.x == 0) s_count = 0;
+  __syncthreads();
+  const bool hashed = d.kind == kTabHash;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < d.rows;
        base += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = base + threadIdx.x;
@@ -177,8 +184,12 @@ __global__ void dim_filter_kernel(const DimBuildArgs a) {
     if (bal == 0) continue;
     const int leader = __ffs(bal) - 1;
     int pos0 = 0;
-    if ((int)lane == leader) pos0 = atomicAdd(&m->count, __popc(bal));  // build size
-    pos0 = __shfl_sync(0xffffffffu, pos0, leader);
+    if (hashed) {
+      if ((int)lane == leader) pos0 = atomicAdd(&m->count, __popc(bal));
+      pos0 = __shfl_sync(0xffffffffu, pos0, leader);
+    } else if ((int)lane == leader) {
+      atomicAdd(&s_count, __popc(bal));
+    }
     if (!pass) continue;
     const int32_t key = d.key[row];
     const int32_t dig = digit_of(d, d.payload ? d.payload[row] : 0);
@@ -202,6 +213,8 @@ __global__ void dim_filter_kernel(const DimBuildArgs a) {
     }
     if (!ok) atomicCAS(&m->err, 0, 2);  // duplicate key (BuildError)
   }
+  __syncthreads();
+  if (threadIdx.x == 0 && !hashed && s_count) atomicAdd(&m->count, s_count);
 }
 
 __global__ void dim_init_kernel(const DimBuildArgs a) {
