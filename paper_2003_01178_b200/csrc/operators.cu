@@ -15,6 +15,7 @@
 #include <map>
 #include <mutex>
 
+#include "async.cuh"
 #include "crystal.cuh"
 #include "internal.hpp"
 
@@ -555,6 +556,130 @@ __global__ void __launch_bounds__(BT) join_probe_kernel(const int32_t* __restric
   }
 }
 
+// join_probe_tile as a streaming pipeline (the SSB join ring specialised to
+// one join and a checksum): one persistent CTA per SM; warp W (producer)
+// streams the probe keys and payloads through a STAGES-deep shared-memory
+// ring with 1-D TMA bulk copies; consumer warps own R rows of a stage, issue
+// all of a lane's first-slot probes (shared-memory copy of the table when it
+// fits, else L2/HBM) before resolving any, walk collisions with every
+// pending item's next slot in flight, and accumulate hits in 64 bits.
+constexpr int kJW = 16;          // consumer warps
+constexpr int kJTile = 4096;     // rows per stage (R = 256 per warp, 8 per lane)
+constexpr int kJR = kJTile / kJW;
+
+template <int STAGES, bool SMEM>
+__global__ void __launch_bounds__((kJW + 1) * 32, 1) join_ring_kernel(
+    const int32_t* __restrict__ keys, const int32_t* __restrict__ pays, int64_t n,
+    const int2* __restrict__ gslots, uint32_t mask, int shift, unsigned long long* out) {
+  constexpr int IT = kJR / 32;  // rows per lane per stage
+  extern __shared__ __align__(128) unsigned char smem[];
+  int32_t* ring = reinterpret_cast<int32_t*>(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)STAGES * 2 * kJTile * 4);
+  uint64_t* empty = full + STAGES;
+  int2* s_slots = reinterpret_cast<int2*>(empty + STAGES);
+  __shared__ long long red[kJW];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = (n + kJTile - 1) / kJTile;
+  const int my_tiles = ntiles > blockIdx.x ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      pipe::mbar_init(full + s, 1);
+      pipe::mbar_init(empty + s, kJW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint64_t policy = 0;
+  auto issue = [&](int it) {
+    const int s = it % STAGES;
+    const int64_t base = (blockIdx.x + (int64_t)it * gridDim.x) * (int64_t)kJTile;
+    const int64_t rows = min((int64_t)kJTile, n - base);
+    const uint32_t bytes = (uint32_t)(rows * 4);  // host guarantees 16 B multiples
+    pipe::mbar_expect_tx(full + s, 2 * bytes);
+    pipe::tma_load_1d(ring + (size_t)s * 2 * kJTile, keys + base, bytes, full + s, policy);
+    pipe::tma_load_1d(ring + (size_t)s * 2 * kJTile + kJTile, pays + base, bytes, full + s, policy);
+  };
+  if (warp == kJW && lane == 0) {
+    policy = pipe::policy_evict_first();
+    for (int it = 0; it < my_tiles && it < STAGES; ++it) issue(it);
+  }
+  if constexpr (SMEM) {
+    const int cap = (int)mask + 1;
+    for (int i = threadIdx.x; i < cap; i += blockDim.x) s_slots[i] = __ldg(gslots + i);
+  }
+  __syncthreads();
+  const int2* slots = SMEM ? s_slots : gslots;
+  long long sum = 0;
+  if (warp == kJW) {
+    if (lane == 0) {
+      for (int it = STAGES; it < my_tiles; ++it) {
+        const int s = it % STAGES;
+        pipe::mbar_wait(empty + s, (uint32_t)(((it / STAGES) - 1) & 1));
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(it);
+      }
+    }
+  } else {
+    int64_t row0 = (int64_t)blockIdx.x * kJTile + warp * kJR;
+    const int64_t step = (int64_t)gridDim.x * kJTile;
+    for (int it = 0; it < my_tiles; ++it, row0 += step) {
+      const int s = it % STAGES;
+      const int64_t left = n - row0;
+      const int valid = left >= kJR ? kJR : (left > 0 ? (int)left : 0);
+      pipe::mbar_wait(full + s, (uint32_t)((it / STAGES) & 1));
+      const int32_t* sk = ring + (size_t)s * 2 * kJTile + warp * kJR;
+      const int32_t* sp = sk + kJTile;
+      int32_t k[IT], p[IT];
+#pragma unroll
+      for (int v = 0; v < IT / 4; ++v) {
+        const int4 a = reinterpret_cast<const int4*>(sk)[v * 32 + lane];
+        const int4 b = reinterpret_cast<const int4*>(sp)[v * 32 + lane];
+        k[v * 4 + 0] = a.x; k[v * 4 + 1] = a.y; k[v * 4 + 2] = a.z; k[v * 4 + 3] = a.w;
+        p[v * 4 + 0] = b.x; p[v * 4 + 1] = b.y; p[v * 4 + 2] = b.z; p[v * 4 + 3] = b.w;
+      }
+      pipe::release_slot(empty + s, lane == 0);  // keys/payloads are in registers now
+      uint32_t sl[IT];
+      int2 e[IT];
+      unsigned pending = 0;
+#pragma unroll
+      for (int i = 0; i < IT; ++i) {
+        const int row = (i / 4) * 128 + lane * 4 + (i & 3);
+        if (row < valid && k[i] != kEmptyKey) {  // INT32_MIN is unstorable: always a miss
+          pending |= 1u << i;
+          sl[i] = ht_slot_of(k[i], shift);
+          e[i] = SMEM ? slots[sl[i]] : __ldg(slots + sl[i]);
+        }
+      }
+      while (pending) {  // hash_table.hpp:41-51, every pending item's next slot in flight
+        unsigned next = 0;
+#pragma unroll
+        for (int i = 0; i < IT; ++i) {
+          if ((pending >> i) & 1u) {
+            if (e[i].x == k[i]) sum += (long long)e[i].y + (long long)p[i];
+            else if (e[i].x != kEmptyKey) next |= 1u << i;
+          }
+        }
+        pending = next;
+#pragma unroll
+        for (int i = 0; i < IT; ++i) {
+          if ((pending >> i) & 1u) {
+            sl[i] = (sl[i] + 1) & mask;
+            e[i] = SMEM ? slots[sl[i]] : __ldg(slots + sl[i]);
+          }
+        }
+      }
+    }
+    sum = warp_sum(sum);
+    if (lane == 0) red[warp] = sum;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long t = 0;
+    for (int w = 0; w < kJW; ++w) t += red[w];
+    if (t) atomicAdd(out, (unsigned long long)t);
+  }
+}
+
 int occupancy(const void* fn, int bt, size_t smem) {
   static std::mutex mu;
   static std::map<std::pair<const void*, size_t>, int> cache;
@@ -711,7 +836,40 @@ int64_t join_probe_sum(crys_ctx* ctx, const int32_t* d_keys, const int32_t* d_pa
   ctx->scratch.reserve(64);
   auto* out = ctx->scratch.as<unsigned long long>() + 1;
   CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(unsigned long long), st));
-  if (n > 0) {
+  const bool aligned = ((reinterpret_cast<uintptr_t>(d_keys) | reinterpret_cast<uintptr_t>(d_payloads)) & 15) == 0 &&
+                       (n & 3) == 0;
+  if (n > 0 && aligned) {
+    // TMA ring: 4 stages x 32 KB; the table joins it in shared memory when it fits
+    const size_t tbytes = sizeof(int2) * (size_t)ht->capacity;
+    constexpr size_t ring4 = 4 * 2 * kJTile * 4 + 2 * 4 * 8;
+    constexpr size_t ring6 = 6 * 2 * kJTile * 4 + 2 * 6 * 8;
+    constexpr size_t ring2 = 2 * 2 * kJTile * 4 + 2 * 2 * 8;
+    const bool smem = ring4 + tbytes <= 227 * 1024;
+    const bool smem2 = !smem && ring2 + tbytes <= 227 * 1024;  // a shallower ring keeps 128 KB tables on chip
+    const int64_t ntiles = (n + kJTile - 1) / kJTile;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, ctx->num_sms));
+    const uint32_t mask = (uint32_t)(ht->capacity - 1);
+    timing_kernel_begin(ctx);
+    if (smem2) {
+      auto fn = join_ring_kernel<2, true>;
+      ensure_dyn_smem((const void*)fn, ring2 + tbytes);
+      fn<<<grid, (kJW + 1) * 32, ring2 + tbytes, st>>>(d_keys, d_payloads, n, ht->slots.as<int2>(), mask,
+                                                       ht->shift, out);
+    } else if (smem) {
+      auto fn = join_ring_kernel<4, true>;
+      ensure_dyn_smem((const void*)fn, ring4 + tbytes);
+      fn<<<grid, (kJW + 1) * 32, ring4 + tbytes, st>>>(d_keys, d_payloads, n, ht->slots.as<int2>(), mask,
+                                                       ht->shift, out);
+    } else {
+      auto fn = join_ring_kernel<6, false>;
+      ensure_dyn_smem((const void*)fn, ring6);
+      fn<<<grid, (kJW + 1) * 32, ring6, st>>>(d_keys, d_payloads, n, ht->slots.as<int2>(), mask, ht->shift,
+                                              out);
+    }
+    timing_kernel_end(ctx);
+    count_launch(ctx);
+    CUDA_TRY(cudaGetLastError());
+  } else if (n > 0) {
     constexpr int BT = 256, IPT = 16;
     const size_t tbytes = sizeof(int2) * (size_t)ht->capacity;
     const bool smem = tbytes <= 96 * 1024;

@@ -209,7 +209,8 @@ struct OsPass {
 // of a thread are issued back to back, then a short serial per-warp counter
 // update gives each item its stable rank (warp-striped order = input order).
 // DBG 1 skips the look-back (timing experiments only; wrong output).
-template <int DBG>
+// RANK 0: warp match.any peers; 1: nine ballots (default, see below).
+template <int DBG, int RANK>
 __global__ void __launch_bounds__(kOsBT, 2) onesweep_kernel(OsPass a) {
   extern __shared__ __align__(128) uint32_t os_sm[];
   int32_t* s_k = reinterpret_cast<int32_t*>(os_sm);           // [kOsTile] staged -> digit-sorted keys
@@ -279,7 +280,19 @@ __global__ void __launch_bounds__(kOsBT, 2) onesweep_kernel(OsPass a) {
     const int sl = wbase + k * 32 + lane;
     key[k] = s_k[sl];
     const uint32_t d = sl < valid ? digit_of(key[k], a.start, mask) : 256u;
-    rd[k] = __match_any_sync(0xffffffffu, d);
+    if constexpr (RANK == 0) {
+      rd[k] = __match_any_sync(0xffffffffu, d);
+    } else {
+      // lanes with the same 9-bit value (digit or 256 = outside): 9 ballots,
+      // each on the fast vote path (match.any runs on the ADU at ~1/60 rate on sm_100a)
+      unsigned m = 0xffffffffu;
+#pragma unroll
+      for (int b = 0; b < 9; ++b) {
+        const unsigned v = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        m &= ((d >> b) & 1u) ? v : ~v;
+      }
+      rd[k] = m;
+    }
   }
   uint32_t* wc = s_wc + warp * 256;
   const unsigned lt = lanemask_lt();
@@ -359,7 +372,8 @@ __global__ void __launch_bounds__(kOsBT, 2) onesweep_kernel(OsPass a) {
   }
 }
 
-// Tuning/experiment knob: CRYS_OS_DBG=1 launches the no-look-back variant.
+// Tuning/experiment knob: CRYS_OS_DBG=1 launches the no-look-back variant,
+// 2 the match.any ranking.
 int os_dbg() {
   static const int v = [] {
     const char* e = getenv("CRYS_OS_DBG");
@@ -369,10 +383,11 @@ int os_dbg() {
 }
 
 void launch_onesweep(const OsPass& a, unsigned grid, size_t smem, cudaStream_t st) {
-  if (os_dbg() == 1)
-    onesweep_kernel<1><<<grid, kOsBT, smem, st>>>(a);
-  else
-    onesweep_kernel<0><<<grid, kOsBT, smem, st>>>(a);
+  switch (os_dbg()) {
+    case 1: onesweep_kernel<1, 1><<<grid, kOsBT, smem, st>>>(a); break;
+    case 2: onesweep_kernel<0, 0><<<grid, kOsBT, smem, st>>>(a); break;
+    default: onesweep_kernel<0, 1><<<grid, kOsBT, smem, st>>>(a); break;
+  }
 }
 
 // radix_histogram (radix.cpp:33-53): counts[owner][digit], owner = the
@@ -422,9 +437,11 @@ size_t os_smem() {
 void os_attr() {
   static bool done = false;
   if (!done) {
-    CUDA_TRY(cudaFuncSetAttribute((const void*)onesweep_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CUDA_TRY(cudaFuncSetAttribute((const void*)onesweep_kernel<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)os_smem()));
-    CUDA_TRY(cudaFuncSetAttribute((const void*)onesweep_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CUDA_TRY(cudaFuncSetAttribute((const void*)onesweep_kernel<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)os_smem()));
+    CUDA_TRY(cudaFuncSetAttribute((const void*)onesweep_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)os_smem()));
     done = true;
   }
