@@ -464,6 +464,7 @@ void launch_pipeline_cfg(crys_ctx* ctx, const pipe::PipeArgs& pa, int64_t cells,
   switch (pipe_cfg()) {
     case 1: launch_pipeline_k0<NJ, NC, 16, 4096, 2>(ctx, pa, cells, name); break;
     case 2: launch_pipeline_k0<NJ, NC, 16, 2048, S>(ctx, pa, cells, name); break;
+
     default: launch_pipeline_k0<NJ, NC, 16, 2048, S>(ctx, pa, cells, name); break;
   }
 }
