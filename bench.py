@@ -215,6 +215,28 @@ def run_reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def paper_model(rows, kern_ms, tot_ms, ms_step):
+    """Fraction of the paper's bandwidth-saturation model (cost_models.py, the
+    reference's cost_models.cpp with a B200 profile): per query the fact
+    columns streamed once at the measured HBM bandwidth (16L / 24L), and for
+    q2.1 also the reference's model_q21 (gpu_like, 32 B lines)."""
+    from paper_2003_01178_b200 import cost_models as cm
+    prof = cm.b200_profile()
+    q_ms = [cm.model_ssb_query(q, rows, prof).total_ms for q in range(13)]
+    q21 = cm.Q21Params.ssb_sf20()
+    q21.l = float(rows)
+    m21 = cm.model_q21(q21, prof, "gpu_like").total_ms
+    return {"profile": f"b200: read=write={prof.read_bw / 1e9:.1f} GB/s (MEASURED_PEAKS), 32 B lines, "
+                       f"L2 126 MB @ {cm.B200_L2_BW / 1e12:.0f} TB/s",
+            "model_ms": dict(zip(QUERY_NAMES, [round(x, 4) for x in q_ms])),
+            "frac_fused_kernel": dict(zip(QUERY_NAMES, [round(m / k, 3) for m, k in zip(q_ms, kern_ms)])),
+            "frac_whole_query": dict(zip(QUERY_NAMES, [round(m / t, 3) for m, t in zip(q_ms, tot_ms)])),
+            "q21_model_q21_gpu_like_ms": round(m21, 4),
+            "q21_frac_model_q21": round(m21 / kern_ms[3], 3),
+            "suite_model_ms": round(sum(q_ms), 4),
+            "suite_frac": round(sum(q_ms) / ms_step, 3)}
+
+
 # --------------------------------------------------------------- GPU arm
 
 def host_columns_needed(q):
@@ -332,6 +354,7 @@ def run_ours(args, rank, world):
             alg = sum(fact_bytes(q, rows_total) for q in range(13))
             achieved = alg / (sum(kern_ms) * 1e-3) / 1e9
             traffic, tsrc = ncu_traffic()
+            line["model"] = paper_model(rows_total, kern_ms, tot_ms, ms_step)
             line["roofline"] = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
                                 "unit": "GB/s", "frac": round(achieved / hbm, 4),
                                 "traffic": round(traffic) if traffic else None,

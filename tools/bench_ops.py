@@ -22,6 +22,7 @@ sys.path.insert(0, ROOT)
 
 import torch  # noqa: E402
 
+from paper_2003_01178_b200 import cost_models as cm  # noqa: E402
 from paper_2003_01178_b200 import tq  # noqa: E402
 
 
@@ -70,11 +71,16 @@ def main():
     ctx = tq.Context.default(0)
     ctx.bind_torch_stream()
 
-    def emit(rec, nbytes, kms, tms):
+    prof = cm.b200_profile()
+
+    def emit(rec, nbytes, kms, tms, model=None):
         gbs = nbytes / (kms * 1e-3) / 1e9
         rec.update({"kernel_ms": round(kms, 4), "call_ms": round(tms, 4), "bytes": int(nbytes),
                     "gbs": round(gbs, 1), "frac_of_peak": round(gbs / hbm, 4), "peak_gbs": hbm,
                     "peak_kind": kind})
+        if model is not None:  # the paper's model (cost_models.py, B200 profile)
+            rec["model_ms"] = round(model.total_ms, 4)
+            rec["frac_of_model"] = round(model.total_ms / kms, 4)
         print(json.dumps(rec), flush=True)
 
     if "select" in only:
@@ -92,7 +98,7 @@ def main():
                 rec = {"bench": "select", "variant": name, "n": n, "sigma": float(sigma), "matched": m}
                 if not args.quick and sigma in counts:
                     rec["golden_ok"] = m == counts[sigma]
-                emit(rec, 4 * n + 4 * m, kms, tms)
+                emit(rec, 4 * n + 4 * m, kms, tms, cm.model_select(n, m / n, prof))
         del x, out
 
     if "project" in only:
@@ -104,7 +110,7 @@ def main():
         for name, fn in (("linear", lambda: tq.project_linear_into(x1, x2, 0.75, -1.25, o)),
                          ("sigmoid", lambda: tq.project_sigmoid_into(x1, x2, 0.75, -1.25, o))):
             kms, tms, _ = timed(ctx, fn, args.reps)
-            emit({"bench": "project", "variant": name, "n": n}, 12 * n, kms, tms)
+            emit({"bench": "project", "variant": name, "n": n}, 12 * n, kms, tms, cm.model_project(n, prof))
         del x1, x2, o
 
     if "join" in only:
@@ -132,7 +138,7 @@ def main():
                    "build_ms": round(build_ms, 4)}
             if not args.quick and H in gold:
                 rec["golden_ok"] = cs == gold[H]
-            emit(rec, 8 * P, kms, tms)
+            emit(rec, 8 * P, kms, tms, cm.model_join_probe(P, H, prof))
             ht.free()
             del bk, bp
             H *= 8 if args.quick else 2
@@ -165,7 +171,7 @@ def main():
             ok = bool(torch.all(k[1:] >= k[:-1]).item())
             emit({"bench": "sort", "variant": name, "n": n, "sorted": ok,
                   "convention": "80N bytes (20N per 8-bit pass x 4, tools/tq_main.cpp:482-483)"},
-                 80 * n, statistics.median(ks), statistics.median(ts))
+                 80 * n, statistics.median(ks), statistics.median(ts), cm.model_sort(n, 4, prof))
 
 
 if __name__ == "__main__":
