@@ -85,6 +85,24 @@ class ShardedSSB:
         self.db = tq.DeviceDatabase.generate(sf, seed, self.lo_begin, self.lo_end, ctx=self.ctx)
         self._bufs = {}
 
+    @classmethod
+    def over(cls, db: "tq.DeviceDatabase", group=None, device: Optional[int] = None) -> "ShardedSSB":
+        """Driver over an existing shard database (e.g. one uploaded from this
+        rank's host columns with DeviceDatabase.upload_host)."""
+        import torch
+        import torch.distributed as dist
+        self = cls.__new__(cls)
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.device = torch.cuda.current_device() if device is None else device
+        self.ctx = db.ctx
+        self.sf = None
+        self.lo_begin = self.lo_end = None
+        self.db = db
+        self._bufs = {}
+        return self
+
     def partial(self, qid, config: tq.TileConfig = tq.TileConfig()):
         """This shard's dense partial aggregate (async on torch's current stream)."""
         import torch

@@ -170,3 +170,22 @@ def test_gpu_generator_bit_exact_sf20(tq, sf20):
                 "customer.c_city", "supplier.s_city"):
         t, c = key.split(".")
         assert col_digest(sf20.download(t, c)) == cols[key]["digest"], key
+
+
+def test_sharded_driver_over_uploaded_shard(tq):
+    """dist.ShardedSSB.over(): the partial + compaction path over a shard
+    database uploaded from host columns (bench.py's N>1 e2e path, world 1)."""
+    from oracle.oracle import Oracle
+    from paper_2003_01178_b200 import dist as cdist
+    orc = Oracle()
+    lo, hi = 500_000, 3_700_001
+    host = orc.generate(1, 42, lo_begin=lo, lo_end=hi)
+    db = tq.DeviceDatabase.from_host({}, sf=1, seed=42)
+    db.upload_host(host)
+    sh = cdist.ShardedSSB.over(db)
+    for q in range(13):
+        res = sh.run_query(q)
+        exp, surv = orc.query(host, q)
+        assert res.as_tuples() == exp, QUERY_NAMES[q]
+        assert res.survivors == surv[:len(res.survivors)], QUERY_NAMES[q]
+    db.free()
