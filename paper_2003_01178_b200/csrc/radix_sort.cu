@@ -283,13 +283,19 @@ __global__ void __launch_bounds__(kOsBT, 2) onesweep_kernel(OsPass a) {
     if constexpr (RANK == 0) {
       rd[k] = __match_any_sync(0xffffffffu, d);
     } else {
-      // lanes with the same 9-bit value (digit or 256 = outside): 9 ballots,
-      // each on the fast vote path (match.any runs on the ADU at ~1/60 rate on sm_100a)
+      // lanes with the same digit: one ballot per digit bit on the fast vote
+      // path (match.any runs on the ADU at ~1/60 rate on sm_100a); m &= v or
+      // ~v is one LOP3 with the xor mask (bit - 1).  A partial tile adds the
+      // in-tile bit (d = 256 marks a slot past the end).
       unsigned m = 0xffffffffu;
 #pragma unroll
-      for (int b = 0; b < 9; ++b) {
-        const unsigned v = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-        m &= ((d >> b) & 1u) ? v : ~v;
+      for (int b = 0; b < 8; ++b) {
+        const unsigned bit = (d >> b) & 1u;
+        m &= __ballot_sync(0xffffffffu, bit) ^ (bit - 1u);
+      }
+      if (valid < kOsTile) {
+        const unsigned bit = d >> 8;
+        m &= __ballot_sync(0xffffffffu, bit) ^ (bit - 1u);
       }
       rd[k] = m;
     }
