@@ -140,24 +140,25 @@ __device__ __forceinline__ int32_t digit_of(const DimBuildDesc& d, int32_t pay) 
   return (uint32_t)u < (uint32_t)d.gcard ? u : -1;
 }
 
-// claim byte/half `off` of a code table: absent -> code; anything else is a
-// duplicate key (BuildError, hash_table.cpp:51-93)
+// claim byte/half `off` of a code table: absent (all ones) -> code with ONE
+// atomicAnd (clearing the bits that are 0 in the code); anything but all ones
+// before is a duplicate key (BuildError, hash_table.cpp:51-93) -- the table
+// content no longer matters once the build has failed.
 template <int BITS>
 __device__ __forceinline__ bool claim_code(void* tbl, uint32_t off, uint32_t code) {
   constexpr uint32_t kMask = (1u << BITS) - 1u;
   constexpr uint32_t kPer = 32 / BITS;
   uint32_t* w = reinterpret_cast<uint32_t*>(tbl) + off / kPer;
   const unsigned sh = (off % kPer) * BITS;
-  uint32_t old = *reinterpret_cast<volatile uint32_t*>(w), assumed;
-  do {
-    if (((old >> sh) & kMask) != kMask) return false;
-    assumed = old;
-    old = atomicCAS(w, assumed, (assumed & ~(kMask << sh)) | ((code & kMask) << sh));
-  } while (old != assumed);
-  return true;
+  const uint32_t old = atomicAnd(w, ~((~code & kMask) << sh));
+  return ((old >> sh) & kMask) == kMask;
 }
 
-__global__ void dim_filter_kernel(const DimBuildArgs a) {
+// build_dim_table for every join at once (grid.y = join).  Each thread owns
+// kDimU rows per pass and issues all of their column loads before any
+// predicate is evaluated (one memory latency per pass, not one per column).
+constexpr int kDimU = 4;
+__global__ void __launch_bounds__(256) dim_filter_kernel(const DimBuildArgs a) {
   const DimBuildDesc& d = a.d[blockIdx.y];
   HtMeta* m = a.meta + blockIdx.y;
   const unsigned lane = lane_id();
@@ -168,50 +169,62 @@ __global__ void dim_filter_kernel(const DimBuildArgs a) {
   if (threadIdx.x == 0) s_count = 0;
   __syncthreads();
   const bool hashed = d.kind == kTabHash;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < d.rows;
-       base += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = base + threadIdx.x;
-    bool pass = row < d.rows;
-    if (pass) {
-      for (int f = 0; f < d.nf; ++f) {
-        const int32_t v = d.fcol[f][row];
-        bool hit = false;
-        for (int r = 0; r < d.nranges[f]; ++r) hit |= v >= d.r[f][r][0] && v <= d.r[f][r][1];
-        pass = pass && hit;
+  const int64_t span = (int64_t)blockDim.x * kDimU;
+  for (int64_t base = (int64_t)blockIdx.x * span; base < d.rows; base += (int64_t)gridDim.x * span) {
+    int32_t fv[2][kDimU], key[kDimU], pay[kDimU];
+#pragma unroll
+    for (int u = 0; u < kDimU; ++u) {
+      const int64_t row = base + u * blockDim.x + threadIdx.x;
+      const bool in = row < d.rows;
+#pragma unroll
+      for (int f = 0; f < 2; ++f) fv[f][u] = (in && f < d.nf) ? __ldg(d.fcol[f] + row) : 0;
+      key[u] = in ? __ldg(d.key + row) : 0;
+      pay[u] = (in && d.payload) ? __ldg(d.payload + row) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kDimU; ++u) {
+      const int64_t row = base + u * blockDim.x + threadIdx.x;
+      bool pass = row < d.rows;
+#pragma unroll
+      for (int f = 0; f < 2; ++f) {
+        if (f < d.nf) {
+          bool hit = false;
+          for (int r = 0; r < d.nranges[f]; ++r) hit |= fv[f][u] >= d.r[f][r][0] && fv[f][u] <= d.r[f][r][1];
+          pass = pass && hit;
+        }
       }
+      const unsigned bal = __ballot_sync(0xffffffffu, pass);
+      if (bal == 0) continue;
+      const int leader = __ffs(bal) - 1;
+      int pos0 = 0;
+      if (hashed) {
+        if ((int)lane == leader) pos0 = atomicAdd(&m->count, __popc(bal));
+        pos0 = __shfl_sync(0xffffffffu, pos0, leader);
+      } else if ((int)lane == leader) {
+        atomicAdd(&s_count, __popc(bal));
+      }
+      if (!pass) continue;
+      const int32_t dig = digit_of(d, pay[u]);
+      if (hashed) {
+        d.compact[pos0 + __popc(bal & lanemask_lt())] = make_int2(key[u], dig);
+        continue;
+      }
+      const uint32_t off = (uint32_t)key[u] - d.kmin;  // < nkeys by the column statistics
+      if (off >= d.nkeys) {
+        atomicCAS(&m->err, 0, 4);  // statistics do not cover the key: cannot happen for valid stats
+        continue;
+      }
+      bool ok;
+      if (d.kind == kTabBitmap) {
+        const uint32_t bit = 1u << (off & 31);
+        ok = !(atomicOr(reinterpret_cast<uint32_t*>(d.tbl) + (off >> 5), bit) & bit);
+      } else if (d.kind == kTabU8) {
+        ok = claim_code<8>(d.tbl, off, dig < 0 ? pipe::kU8Bad : (uint32_t)dig);
+      } else {
+        ok = claim_code<16>(d.tbl, off, dig < 0 ? pipe::kU16Bad : (uint32_t)dig);
+      }
+      if (!ok) atomicCAS(&m->err, 0, 2);  // duplicate key (BuildError)
     }
-    const unsigned bal = __ballot_sync(0xffffffffu, pass);
-    if (bal == 0) continue;
-    const int leader = __ffs(bal) - 1;
-    int pos0 = 0;
-    if (hashed) {
-      if ((int)lane == leader) pos0 = atomicAdd(&m->count, __popc(bal));
-      pos0 = __shfl_sync(0xffffffffu, pos0, leader);
-    } else if ((int)lane == leader) {
-      atomicAdd(&s_count, __popc(bal));
-    }
-    if (!pass) continue;
-    const int32_t key = d.key[row];
-    const int32_t dig = digit_of(d, d.payload ? d.payload[row] : 0);
-    if (d.kind == kTabHash) {
-      d.compact[pos0 + __popc(bal & lanemask_lt())] = make_int2(key, dig);
-      continue;
-    }
-    const uint32_t off = (uint32_t)key - d.kmin;  // < nkeys by the column statistics
-    if (off >= d.nkeys) {
-      atomicCAS(&m->err, 0, 4);  // statistics do not cover the key: cannot happen for valid stats
-      continue;
-    }
-    bool ok;
-    if (d.kind == kTabBitmap) {
-      const uint32_t bit = 1u << (off & 31);
-      ok = !(atomicOr(reinterpret_cast<uint32_t*>(d.tbl) + (off >> 5), bit) & bit);
-    } else if (d.kind == kTabU8) {
-      ok = claim_code<8>(d.tbl, off, dig < 0 ? pipe::kU8Bad : (uint32_t)dig);
-    } else {
-      ok = claim_code<16>(d.tbl, off, dig < 0 ? pipe::kU16Bad : (uint32_t)dig);
-    }
-    if (!ok) atomicCAS(&m->err, 0, 2);  // duplicate key (BuildError)
   }
   __syncthreads();
   if (threadIdx.x == 0 && !hashed && s_count) atomicAdd(&m->count, s_count);
@@ -271,18 +284,33 @@ __device__ __forceinline__ T block_sum(T v, T* red) {
 // (INIT, AND, AND), SUM(extendedprice * discount) in 8 bytes.  A later
 // column is read only in vectors that still hold a live row (BlockLoadSel),
 // so dead 32 B sectors are never fetched.
-template <int BT, int IPT>
+// PF: the NEXT tile's first column is loaded before this tile's dependent
+// (selective) loads, so the chain of three selective latencies overlaps a
+// streaming read.
+template <int BT, int IPT, bool PF = false>
 __global__ void __launch_bounds__(BT) ssb_flight1_kernel(const Flight1Args a) {
   using L = VecLayout<BT, IPT>;
   __shared__ long long red[BT / 32];
   long long sum = 0;
   unsigned cnt = 0;
   const int64_t ntiles = (a.n + L::TILE - 1) / L::TILE;
+  int32_t nx[IPT];
+  if (PF && blockIdx.x < ntiles)
+    BlockLoad<BT, IPT>(a.fcol[0] + (int64_t)blockIdx.x * L::TILE,
+                       (int)min((int64_t)L::TILE, a.n - (int64_t)blockIdx.x * L::TILE), nx);
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t base = tile * L::TILE;
     const int valid = (int)min((int64_t)L::TILE, a.n - base);
     int32_t x[IPT], d[IPT], e[IPT];
-    BlockLoad<BT, IPT>(a.fcol[0] + base, valid, x);
+    if constexpr (PF) {
+#pragma unroll
+      for (int k = 0; k < IPT; ++k) x[k] = nx[k];
+      const int64_t nt = tile + gridDim.x;
+      if (nt < ntiles)
+        BlockLoad<BT, IPT>(a.fcol[0] + nt * L::TILE, (int)min((int64_t)L::TILE, a.n - nt * L::TILE), nx);
+    } else {
+      BlockLoad<BT, IPT>(a.fcol[0] + base, valid, x);
+    }
     unsigned f = BlockPred<IPT>(x, a.flo[0], a.fhi[0], BlockValidMask<BT, IPT>(valid));
     BlockLoadSel<BT, IPT>(a.fcol[1] + base, valid, f, d);
     f = BlockPredAnd<IPT>(d, a.flo[1], a.fhi[1], f);
@@ -352,7 +380,7 @@ struct F1Launch {
 
 // Results are tile-invariant (test_ssb.cpp:251-261), so the TileConfig of a
 // query is validated but the GPU runs its own tuned shape; CRYS_F1_TILE=BTxIPT
-// forces a compiled shape (ablation / tuning).
+// forces a compiled (non-prefetching) shape (ablation / tuning).
 F1Launch select_flight1() {
   static const std::pair<int, int> forced = [] {
     const char* e = getenv("CRYS_F1_TILE");
@@ -364,7 +392,9 @@ F1Launch select_flight1() {
   if (forced.first == B && forced.second == I) return {ssb_flight1_kernel<B, I>, B, I};
   CRYS_F1_SHAPES(X)
 #undef X
-  return {ssb_flight1_kernel<kNativeBT, kNativeIPT>, kNativeBT, kNativeIPT};
+  // default: 256 x 8 with the next tile's first column prefetched (measured on
+  // B200, tools/tune_f1pf.sh: q1.2 0.204 -> 0.193 ms, q1.3 0.184 -> 0.177 ms)
+  return {ssb_flight1_kernel<256, 8, true>, 256, 8};
 }
 
 int blocks_per_sm(const void* fn, int bt, size_t smem) {
@@ -635,7 +665,8 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int
   if (nj) {
     const int tpb = 256;
     const int gx_rows = (int)std::min<int64_t>((max_rows + tpb - 1) / tpb, (int64_t)ctx->num_sms * 8);
-    dim_filter_kernel<<<dim3(std::max(gx_rows, 1), nj), tpb, 0, st>>>(da);
+    const int gx_filter = (int)std::min<int64_t>((max_rows + tpb * kDimU - 1) / (tpb * kDimU), (int64_t)ctx->num_sms * 8);
+    dim_filter_kernel<<<dim3(std::max(gx_filter, 1), nj), tpb, 0, st>>>(da);
     CRYS_LAUNCHED("dim_filter_kernel");
     count_launch(ctx);
     if (any_ht) {  // linear-probing builds (hash_table.cpp:20-94) for sparse key domains
