@@ -114,6 +114,15 @@ typedef struct {
  * statistics are computed on the host while the DMA runs.  The host arrays
  * must stay alive until the queries that read them have completed. */
 crys_status crys_db_upload_host(crys_db* db, const crys_host_column* cols, int ncols);
+/* One column from a file in the reference's CRYS format (column_io.hpp:3-13;
+ * replaces load_column, column_io.cpp:65-100) straight into HBM: the payload
+ * streams through double-buffered pinned staging on the copy stream and later
+ * queries wait on the column's ready event.  int32 only; EIO on a missing
+ * file, bad magic, unsupported version, float32 kind or short payload
+ * (BadMagicError / KindMismatchError / TruncatedFileError, column_io.hpp:24-32). */
+crys_status crys_db_load_column_file(crys_db* db, const char* table, const char* column, const char* path);
+/* Writes a column in the CRYS format (replaces save_column, column_io.cpp:50-63). */
+crys_status crys_db_save_column_file(const crys_db* db, const char* table, const char* column, const char* path);
 /* Device pointer + rows of a column (borrowed; valid until the db is freed). */
 crys_status crys_db_column(const crys_db* db, const char* table, const char* column,
                            const int32_t** d_data, int64_t* rows);

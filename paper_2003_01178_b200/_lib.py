@@ -51,6 +51,8 @@ SIGNATURES = [
     ("crys_db_create", C.c_int, [_P, C.c_int64, C.c_uint64, C.POINTER(_P)]),
     ("crys_db_upload_column", C.c_int, [_P, C.c_char_p, C.c_char_p, _P, C.c_int64]),
     ("crys_db_upload_host", C.c_int, [_P, C.POINTER(crys_host_column), C.c_int]),
+    ("crys_db_load_column_file", C.c_int, [_P, C.c_char_p, C.c_char_p, C.c_char_p]),
+    ("crys_db_save_column_file", C.c_int, [_P, C.c_char_p, C.c_char_p, C.c_char_p]),
     ("crys_db_column", C.c_int, [_P, C.c_char_p, C.c_char_p, C.POINTER(_P), _I64P]),
     ("crys_db_download_column", C.c_int, [_P, C.c_char_p, C.c_char_p, _P, C.c_int64]),
     ("crys_db_free", None, [_P]),

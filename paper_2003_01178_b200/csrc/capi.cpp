@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -47,6 +48,8 @@ crys_ctx::~crys_ctx() {
   qws.reset();
   sws.reset();
   delete staging;
+  for (auto& e : io_ev)
+    if (e) cudaEventDestroy(e);
   if (copy_stream) cudaStreamDestroy(copy_stream);
   if (own_stream) cudaStreamDestroy(own_stream);
 }
@@ -405,6 +408,119 @@ crys_status crys_db_upload_host(crys_db* db, const crys_host_column* cols, int n
     }
     // dimension statistics on the host while the DMA runs
     for (int i = 0; i < ncols; ++i) host_stats(*issued[(size_t)i], cols[i].table, cols[i].h_data, cols[i].rows);
+  });
+}
+
+// ---------------------------------------------------------------- CRYS column files
+// The reference's on-disk column format (column_io.hpp:3-13, column_io.cpp:
+// 50-100): "CRYS", u16 version 1, u8 kind (0 int32, 1 float32), u8 0, u64
+// count, then raw little-endian 4-byte elements.  Loading streams the payload
+// through two pinned staging buffers: the file read of chunk i+1 overlaps the
+// DMA of chunk i on the copy stream; the column's ready event then gates the
+// queries that read it (as crys_db_upload_host).
+namespace {
+constexpr size_t kIoChunk = size_t(32) << 20;  // bytes per staging buffer
+
+struct FileCloser {
+  void operator()(FILE* f) const {
+    if (f) fclose(f);
+  }
+};
+
+void io_ready(crys_ctx* ctx) {
+  if (!ctx->copy_stream) CUDA_TRY(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    ctx->io[i].reserve(kIoChunk);
+    if (!ctx->io_ev[i]) CUDA_TRY(cudaEventCreateWithFlags(&ctx->io_ev[i], cudaEventDisableTiming));
+  }
+}
+}  // namespace
+
+crys_status crys_db_load_column_file(crys_db* db, const char* table, const char* column, const char* path) {
+  return guarded([&] {
+    CRYS_CHECK(db && table && column && path, CRYS_ECONFIG, "null argument");
+    crys_ctx* ctx = db->ctx;
+    bind(ctx);
+    std::unique_ptr<FILE, FileCloser> f(fopen(path, "rb"));
+    CRYS_CHECK(f != nullptr, CRYS_EIO, std::string("cannot open for reading: ") + path);
+    unsigned char h[16];
+    CRYS_CHECK(fread(h, 1, 16, f.get()) == 16, CRYS_EIO, std::string("truncated header: ") + path);
+    CRYS_CHECK(std::memcmp(h, "CRYS", 4) == 0, CRYS_EIO, std::string("bad magic: ") + path);
+    CRYS_CHECK((h[4] | (h[5] << 8)) == 1, CRYS_EIO, std::string("unsupported format version: ") + path);
+    CRYS_CHECK(h[6] <= 1, CRYS_EIO, std::string("unknown element kind byte: ") + path);
+    CRYS_CHECK(h[6] == 0, CRYS_EIO,
+               std::string("element kind mismatch: ") + path + " holds float32, expected int32");
+    uint64_t n = 0;
+    for (int i = 0; i < 8; ++i) n |= (uint64_t)h[8 + i] << (8 * i);
+    CRYS_CHECK(n < (uint64_t(1) << 40), CRYS_EIO, std::string("implausible element count: ") + path);
+    io_ready(ctx);
+    // WAR against queued work that may still read the previous buffer
+    cudaEvent_t fence;
+    CUDA_TRY(cudaEventCreateWithFlags(&fence, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(fence, ctx->stream));
+    CUDA_TRY(cudaStreamWaitEvent(ctx->copy_stream, fence, 0));
+    CUDA_TRY(cudaEventDestroy(fence));
+    auto& c = db->cols[std::string(table) + "." + column];
+    if (!c.buf) c.buf.reset(new crys::DevBuf());
+    if (sizeof(int32_t) * (size_t)std::max<uint64_t>(n, 1) > c.buf->bytes) {
+      CUDA_TRY(cudaStreamSynchronize(ctx->copy_stream));
+      c.buf->reserve(sizeof(int32_t) * (size_t)std::max<uint64_t>(n, 1));
+    }
+    c.rows = (int64_t)n;
+    const bool stats = std::string(table) != "lineorder" && n > 0;
+    int32_t lo = INT32_MAX, hi = INT32_MIN;
+    const size_t total = 4 * (size_t)n;
+    for (size_t off = 0, i = 0; off < total; off += kIoChunk, ++i) {
+      const int b = (int)(i & 1);
+      CUDA_TRY(cudaEventSynchronize(ctx->io_ev[b]));  // staging buffer b free again
+      const size_t len = std::min(kIoChunk, total - off);
+      CRYS_CHECK(fread(ctx->io[b].p, 1, len, f.get()) == len, CRYS_EIO, std::string("truncated payload: ") + path);
+      if (stats) {
+        const int32_t* v = ctx->io[b].as<int32_t>();
+        for (size_t k = 0; k < len / 4; ++k) {
+          lo = v[k] < lo ? v[k] : lo;
+          hi = v[k] > hi ? v[k] : hi;
+        }
+      }
+      CUDA_TRY(cudaMemcpyAsync(c.buf->as<char>() + off, ctx->io[b].p, len, cudaMemcpyHostToDevice,
+                               ctx->copy_stream));
+      CUDA_TRY(cudaEventRecord(ctx->io_ev[b], ctx->copy_stream));
+    }
+    if (!c.ready) CUDA_TRY(cudaEventCreateWithFlags(&c.ready, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(c.ready, ctx->copy_stream));
+    c.pending = true;
+    c.stats = stats;
+    c.vmin = stats ? lo : 0;
+    c.vmax = stats ? hi : -1;
+    if (std::string(table) == "lineorder") {
+      db->lo_begin = 0;
+      db->lo_end = (int64_t)n;
+    }
+  });
+}
+
+crys_status crys_db_save_column_file(const crys_db* db, const char* table, const char* column, const char* path) {
+  return guarded([&] {
+    CRYS_CHECK(db && table && column && path, CRYS_ECONFIG, "null argument");
+    crys_ctx* ctx = db->ctx;
+    bind(ctx);
+    int64_t n = 0;
+    const int32_t* d = db->col(table, column, &n);  // orders after a pending upload
+    io_ready(ctx);
+    std::unique_ptr<FILE, FileCloser> f(fopen(path, "wb"));
+    CRYS_CHECK(f != nullptr, CRYS_EIO, std::string("cannot open for writing: ") + path);
+    unsigned char h[16] = {'C', 'R', 'Y', 'S', 1, 0, 0, 0};
+    for (int i = 0; i < 8; ++i) h[8 + i] = (unsigned char)((uint64_t)n >> (8 * i));
+    CRYS_CHECK(fwrite(h, 1, 16, f.get()) == 16, CRYS_EIO, std::string("write failed: ") + path);
+    const size_t total = 4 * (size_t)n;
+    for (size_t off = 0; off < total; off += kIoChunk) {
+      const size_t len = std::min(kIoChunk, total - off);
+      CUDA_TRY(cudaMemcpyAsync(ctx->io[0].p, reinterpret_cast<const char*>(d) + off, len,
+                               cudaMemcpyDeviceToHost, ctx->stream));
+      CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+      CRYS_CHECK(fwrite(ctx->io[0].p, 1, len, f.get()) == len, CRYS_EIO, std::string("write failed: ") + path);
+    }
+    CRYS_CHECK(fflush(f.get()) == 0, CRYS_EIO, std::string("write failed: ") + path);
   });
 }
 

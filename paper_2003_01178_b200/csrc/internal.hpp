@@ -134,6 +134,8 @@ struct crys_ctx {
   std::unique_ptr<crys::SortWorkspace, crys::WsDeleter> sws;
   crys_db* staging = nullptr;  // device copies for crys_run_query_host
   cudaStream_t copy_stream = nullptr;  // H2D of crys_db_upload_host (lazy)
+  crys::PinnedBuf io[2];               // CRYS column file staging (double-buffered)
+  cudaEvent_t io_ev[2] = {nullptr, nullptr};
   ~crys_ctx();
 };
 

@@ -22,6 +22,8 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import json
+import os
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence, Tuple
 
@@ -380,6 +382,18 @@ class DeviceDatabase:
         check(LIB.crys_db_upload_host(self.h, arr, len(cols)))
         self._host_keep = keep
 
+    def load_column_file(self, table: str, column: str, path: str) -> None:
+        """load_column (column_io.cpp:65-100) of a CRYS file straight into HBM."""
+        check(LIB.crys_db_load_column_file(self.h, table.encode(), column.encode(), os.fsencode(path)))
+
+    def save_column_file(self, table: str, column: str, path: str) -> None:
+        """save_column (column_io.cpp:50-63) of an HBM column."""
+        check(LIB.crys_db_save_column_file(self.h, table.encode(), column.encode(), os.fsencode(path)))
+
+    def has_column(self, table: str, column: str) -> bool:
+        p, n = C.c_void_p(), C.c_int64()
+        return LIB.crys_db_column(self.h, table.encode(), column.encode(), C.byref(p), C.byref(n)) == 0
+
     def upload(self, table: str, column: str, data) -> None:
         a = np.ascontiguousarray(data, dtype=np.int32)
         check(LIB.crys_db_upload_column(self.h, table.encode(), column.encode(),
@@ -407,6 +421,63 @@ class DeviceDatabase:
             self.free()
         except Exception:
             pass
+
+
+SSB_TABLES = ["lineorder", "date", "supplier", "customer", "part"]
+
+
+def load_database(directory: str, ctx: Optional[Context] = None) -> DeviceDatabase:
+    """load_database (column_io.cpp:142-190): manifest.json + one CRYS file per
+    column, every column streamed into HBM (IoError on a malformed manifest,
+    file or a length that disagrees with the manifest)."""
+    mpath = os.path.join(directory, "manifest.json")
+    try:
+        with open(mpath) as f:
+            manifest = json.load(f)
+    except OSError:
+        raise IoError(f"cannot open manifest in {directory}")
+    except ValueError as e:
+        raise IoError(f"manifest parse error in {directory}: {e}")
+    try:
+        if manifest["format"] != "crys-manifest":
+            raise IoError(f"not a database manifest: {directory}")
+        db = DeviceDatabase.from_host({}, ctx=ctx, sf=int(manifest["scale_factor"]), seed=int(manifest["seed"]))
+        for t in SSB_TABLES:
+            for jc in manifest["tables"][t]["columns"]:
+                if jc["kind"] != "int32":
+                    raise IoError(f"element kind mismatch: {jc['file']} holds {jc['kind']}, expected int32")
+                db.load_column_file(t, jc["name"], os.path.join(directory, jc["file"]))
+                _, n = db.column_ptr(t, jc["name"])
+                if n != int(jc["length"]):
+                    raise IoError(f"column length disagrees with manifest: {jc['name']}")
+    except (KeyError, TypeError) as e:
+        raise IoError(f"manifest field error in {directory}: {e}")
+    return db
+
+
+def save_database(db: DeviceDatabase, directory: str, scale_factor: int, seed: int,
+                  dictionaries: Optional[Dict[str, List[str]]] = None) -> None:
+    """save_database (column_io.cpp:104-140): one CRYS file per HBM column of the
+    SSB tables + manifest.json in the reference's layout."""
+    os.makedirs(directory, exist_ok=True)
+    tables = {}
+    for t in SSB_TABLES:
+        names = LO_COLS if t == "lineorder" else DIM_COLS[t]
+        cols, rows = [], 0
+        for c in names:
+            if not db.has_column(t, c):
+                continue
+            file = f"{t}.{c}.col"
+            db.save_column_file(t, c, os.path.join(directory, file))
+            _, n = db.column_ptr(t, c)
+            rows = n
+            cols.append({"name": c, "file": file, "kind": "int32", "length": n})
+        tables[t] = {"rows": rows, "columns": cols}
+    manifest = {"format": "crys-manifest", "version": 1, "scale_factor": int(scale_factor), "seed": int(seed),
+                "tables": tables, "dictionaries": dictionaries or {}}
+    with open(os.path.join(directory, "manifest.json"), "w") as f:
+        json.dump(manifest, f, indent=2)
+        f.write("\n")
 
 
 def random_i32(out, seed: int, stream: int, lo: int, hi: int, index0: int = 0) -> None:
