@@ -143,3 +143,70 @@ def reduce_local(buf, qid, ctx: tq.Context) -> tq.QueryResult:
     torch.cuda.current_stream(buf.device).synchronize()
     res.survivors = [int(x) for x in buf[2 * cells:2 * cells + 4].cpu().numpy()[:max(nj, 1)]]
     return res
+
+
+# ----------------------------------------------------------------- sharded sort
+# the first 8-bit MSB pass, an all-to-all exchange by digit
+# range, then a local sort.  Each rank holds a contiguous shard of the pairs
+# (global order = rank order); afterwards rank r holds one contiguous KEY range,
+# so the concatenation over ranks is the global sort.  With the stable (LSB)
+# local sort the result equals the single-GPU stable sort: equal keys arrive
+# grouped by source rank, each group in its stable-partition (input) order.
+
+def split_digits(global_counts, world: int):
+    """Contiguous top-digit ranges [b[r], b[r+1]) balancing the pair count."""
+    c = np.asarray(global_counts, np.int64)
+    total = int(c.sum())
+    cum = np.concatenate([[0], np.cumsum(c)])
+    bounds = [0]
+    for r in range(1, world):
+        target = (total * r + world - 1) // world
+        d = int(np.searchsorted(cum, target, side="left"))
+        bounds.append(min(max(d, bounds[-1]), len(c)))
+    bounds.append(len(c))
+    return bounds
+
+
+class DeviceSortOps:
+    """The device half of sharded_sort (every step a libcrystal_b200 kernel)."""
+
+    def top_histogram(self, keys):
+        return tq.radix_histogram(keys, 24, 8, 1)[0]
+
+    def partition_top(self, keys, payloads):
+        import torch
+        ok, op = torch.empty_like(keys), torch.empty_like(payloads)
+        tq.radix_partition(keys, payloads, ok, op, 24, 8)
+        return ok, op
+
+    def local_sort(self, keys, payloads, algo):
+        if algo == "msb":
+            tq.msb_radix_sort(keys, payloads)
+        else:
+            tq.lsb_radix_sort(keys, payloads)
+
+
+def sharded_sort(keys, payloads, algo: str = "lsb", group=None, ops=None):
+    """This rank's output key range of the global (key, payload) sort."""
+    import torch
+    import torch.distributed as dist
+    ops = ops or DeviceSortOps()
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    hist = torch.as_tensor(np.asarray(ops.top_histogram(keys), np.int64))
+    if keys.is_cuda:
+        hist = hist.to(keys.device)
+    gathered = [torch.empty_like(hist) for _ in range(world)]
+    dist.all_gather(gathered, hist, group=group)
+    all_h = np.stack([g.cpu().numpy() for g in gathered])  # [world, 256]
+    bounds = split_digits(all_h.sum(axis=0), world)
+    send = [int(all_h[rank, bounds[r]:bounds[r + 1]].sum()) for r in range(world)]
+    recv = [int(all_h[r, bounds[rank]:bounds[rank + 1]].sum()) for r in range(world)]
+    pk, pp = ops.partition_top(keys, payloads)
+    ok = torch.empty(sum(recv), dtype=keys.dtype, device=keys.device)
+    op = torch.empty(sum(recv), dtype=payloads.dtype, device=payloads.device)
+    dist.all_to_all_single(ok, pk, recv, send, group=group)
+    dist.all_to_all_single(op, pp, recv, send, group=group)
+    if ok.numel():
+        ops.local_sort(ok, op, algo)
+    return ok, op

@@ -790,3 +790,30 @@ def lsb_radix_sort(keys, payloads, workers: int = 1, bits_per_pass: int = 8) -> 
 def msb_radix_sort(keys, payloads, workers: int = 1) -> None:
     """radix.cpp:210-216: keys ascending, (key, payload) pairs preserved."""
     _sort(keys, payloads, _lib.CRYS_SORT_MSB, 8)
+
+
+def radix_histogram(keys, start_bit: int, num_bits: int, num_owners: int = 1) -> np.ndarray:
+    """radix_histogram (radix.cpp:33-53) on the device: counts[owner][digit],
+    owner = contiguous chunk of ceil(n / num_owners) keys."""
+    pk, n = _dev(keys, "int32")
+    if not (1 <= num_bits <= 8 and start_bit >= 0 and start_bit + num_bits <= 32):
+        raise ConfigError("RadixPass: bit range exceeds 32-bit keys")
+    out = np.zeros((int(num_owners), 1 << int(num_bits)), np.int64)
+    ctx = _ctx_for(keys)
+    check(LIB.crys_radix_histogram(ctx.h, C.c_void_p(pk), n, int(start_bit), int(num_bits), int(num_owners),
+                                   out.ctypes.data_as(C.c_void_p)))
+    return out
+
+
+def radix_partition(keys, payloads, out_keys, out_payloads, start_bit: int, num_bits: int) -> None:
+    """radix_shuffle with a stable pass (radix.cpp:75-136): the pairs stably
+    partitioned by digit, out of place, on the device."""
+    pk, n = _dev(keys, "int32")
+    pp, n2 = _dev(payloads, "int32")
+    ok, n3 = _dev(out_keys, "int32")
+    op, n4 = _dev(out_payloads, "int32")
+    if not n == n2 == n3 == n4:
+        raise ContractError("radix partition: length mismatch")
+    ctx = _ctx_for(keys)
+    check(LIB.crys_radix_partition(ctx.h, C.c_void_p(pk), C.c_void_p(pp), n, int(start_bit), int(num_bits),
+                                   C.c_void_p(ok), C.c_void_p(op)))

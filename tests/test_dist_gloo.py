@@ -68,3 +68,86 @@ def test_sharded_ssb_gloo(world):
         rows, surv = res[qid]
         assert rows == golden_rows(rec)
         assert surv == rec["survivors"]
+
+
+# ---------------------------------------------------------------- sharded sort
+
+class _NumpySortOps:
+    """Test stand-in for dist.DeviceSortOps on CPU tensors (the product runs
+    these three steps as libcrystal_b200 kernels)."""
+
+    @staticmethod
+    def _top(k):
+        return ((k.astype(np.int64) & 0xFFFFFFFF) ^ 0x80000000) >> 24
+
+    def top_histogram(self, keys):
+        return np.bincount(self._top(keys.numpy()), minlength=256).astype(np.int64)
+
+    def partition_top(self, keys, payloads):
+        import torch
+        o = np.argsort(self._top(keys.numpy()), kind="stable")
+        return torch.from_numpy(keys.numpy()[o].copy()), torch.from_numpy(payloads.numpy()[o].copy())
+
+    def local_sort(self, keys, payloads, algo):
+        o = np.argsort(keys.numpy(), kind="stable")
+        k, p = keys.numpy()[o].copy(), payloads.numpy()[o].copy()
+        keys.numpy()[:] = k
+        payloads.numpy()[:] = p
+
+
+def _sort_worker(rank, world, port, case, out):
+    import torch
+    import torch.distributed as dist
+    from paper_2003_01178_b200 import dist as cdist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        keys, pays = _sort_case(case)
+        lo, hi = cdist.shard_range(len(keys), rank, world)
+        k, p = cdist.sharded_sort(torch.from_numpy(keys[lo:hi].copy()), torch.from_numpy(pays[lo:hi].copy()),
+                                  "lsb", ops=_NumpySortOps())
+        out.put((rank, k.numpy(), p.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def _sort_case(case):
+    rng = np.random.default_rng(7)
+    n = 20_011
+    if case == "uniform":
+        keys = rng.integers(-(2 ** 31), 2 ** 31 - 1, n, dtype=np.int64).astype(np.int32)
+    elif case == "narrow":
+        keys = rng.integers(-3, 4, n).astype(np.int32)  # two top digits, many ties
+    else:
+        keys = np.full(n, 5, np.int32)  # one rank receives everything
+    return keys, np.arange(n, dtype=np.int32)
+
+
+@pytest.mark.parametrize("case", ["uniform", "narrow", "constant"])
+def test_sharded_sort_gloo(case):
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sort_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    keys, pays = _sort_case(case)
+    o = np.argsort(keys, kind="stable")
+    assert np.array_equal(np.concatenate([k for _, k, _ in parts]), keys[o])
+    assert np.array_equal(np.concatenate([p for _, _, p in parts]), pays[o])
+
+
+def test_split_digits_balanced():
+    from paper_2003_01178_b200 import dist as cdist
+    c = np.zeros(256, np.int64)
+    c[10], c[11], c[200] = 100, 100, 100
+    b = cdist.split_digits(c, 3)
+    assert b[0] == 0 and b[-1] == 256 and all(x <= y for x, y in zip(b, b[1:]))
+    sizes = [int(c[b[r]:b[r + 1]].sum()) for r in range(3)]
+    assert sizes == [100, 100, 100]

@@ -321,3 +321,40 @@ def test_project_inputs_match_reference_stream(env):
     tq.project_inputs(x1, x2, 42)
     e1, e2 = orc.project_inputs(n, 42)
     assert np.array_equal(x1.cpu().numpy(), e1) and np.array_equal(x2.cpu().numpy(), e2)
+
+
+def test_radix_histogram_and_partition_wrappers(env):
+    torch, tq, orc = env
+    kh = orc.random_i32(300_001, 9, 9, -(2 ** 31), 2 ** 31 - 1)
+    k = _cuda(torch, kh)
+    p = torch.arange(len(kh), dtype=torch.int32, device="cuda")
+    dig = ((kh.astype(np.int64) & 0xFFFFFFFF) ^ 0x80000000) >> 24
+    h = tq.radix_histogram(k, 24, 8, 3)
+    chunk = -(-len(kh) // 3)
+    for o in range(3):
+        assert np.array_equal(h[o], np.bincount(dig[o * chunk:(o + 1) * chunk], minlength=256))
+    ok, op = torch.empty_like(k), torch.empty_like(p)
+    tq.radix_partition(k, p, ok, op, 24, 8)
+    order = np.argsort(dig, kind="stable")
+    assert np.array_equal(ok.cpu().numpy(), kh[order]) and np.array_equal(op.cpu().numpy(), order)
+
+
+def test_sharded_sort_single_rank_nccl(env):
+    """dist.sharded_sort through the device ops and NCCL (world 1 on one GPU;
+    the multi-rank exchange logic is covered by the gloo tests)."""
+    import socket
+    import torch.distributed as dist
+    from paper_2003_01178_b200 import dist as cdist
+    torch, tq, orc = env
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", rank=0, world_size=1, init_method=f"tcp://127.0.0.1:{port}")
+    try:
+        kh = orc.random_i32(1 << 20, 3, 4, -1000, 1000)
+        k, p = cdist.sharded_sort(_cuda(torch, kh), torch.arange(len(kh), dtype=torch.int32, device="cuda"))
+        o = np.argsort(kh, kind="stable")
+        assert np.array_equal(k.cpu().numpy(), kh[o]) and np.array_equal(p.cpu().numpy(), o)
+    finally:
+        dist.destroy_process_group()
