@@ -22,7 +22,8 @@
 namespace crys {
 namespace {
 
-// Tuning knob CRYS_SEL_CFG picks the input-order select instantiation.
+// A/B knob: CRYS_SEL_CFG=1 runs the single-pass look-back select instead of
+// reduce-then-scan (both produce the input-order result).
 int sel_cfg() {
   static const int cfg = [] {
     const char* e = getenv("CRYS_SEL_CFG");
@@ -38,18 +39,12 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 }
 
 // Input-order selection (select_branching/predicated_into, workers=1: output
-// in input order).  Single pass with a decoupled look-back over tiles.
-// Tile layout is WARP-CONTIGUOUS: warp w owns slots [w*32*IPT, (w+1)*32*IPT),
+// in input order).  Tile layout is WARP-CONTIGUOUS: warp w owns slots [w*32*IPT, (w+1)*32*IPT),
 // lane l's vector v is the 4 slots at w*32*IPT + v*128 + 4*l, so a warp's
 // order is (v, lane, element) and every load is a 128-bit coalesced read.
 // Positions come from per-vector warp scans (popc + shuffles) and one barrier
 // for the warp totals; the compacted tile is staged in shared memory and
 // stored with coalesced writes.
-//   PERSIST = false: one tile per CTA, tile = blockIdx.x (dispatch order).
-//   PERSIST = true : resident CTAs take tiles from an atomic counter and
-//                    prefetch the next tile's vectors before the current
-//                    tile's look-back + store (dynamic order keeps the
-//                    look-back chain short).
 template <int BT, int IPT>
 struct SelTile {
   static constexpr int NV = IPT / 4;
@@ -143,100 +138,29 @@ __device__ __forceinline__ int sel_compact(const int4 (&v)[IPT / 4], int valid, 
   return total;
 }
 
-// Persistent WAVE form: CTA c takes tiles c, c+G, c+2G, ... (static, so no
-// tile is ever held unpublished behind another); per tile it counts, PUBLISHES
-// the aggregate at once, issues the next tile's loads, then looks back (one
-// block-wide round trip covers the whole previous wave) and stores.  The
-// next tile's HBM reads are in flight during the look-back wait.
+// Single-pass form (A/B only, CRYS_SEL_CFG=1): one tile per CTA (tile =
+// blockIdx.x, dispatch order), block-wide decoupled look-back.  Correct, but
+// the look-back latency under load makes it slower than reduce-then-scan
+// (profiles/r01_select_tuning.txt).
 template <int BT, int IPT>
-__global__ void __launch_bounds__(BT) select_wave_kernel(const int32_t* __restrict__ in, int64_t n,
-                                                         int32_t lo, int32_t hi, int32_t* __restrict__ out,
-                                                         unsigned long long* status, long long ntiles,
-                                                         long long* total_out) {
-  using T = SelTile<BT, IPT>;
-  __shared__ __align__(16) int32_t s_items[T::TILE];
-  __shared__ int s_warp[T::W];
-  __shared__ long long s_red[T::W + T::W / 2 + 1];
-  long long tile = blockIdx.x;
-  if (tile >= ntiles) return;
-  int4 v[IPT / 4];
-  sel_load<BT, IPT>(in, tile * T::TILE, (int)min((int64_t)T::TILE, (int64_t)(n - tile * T::TILE)), v);
-  for (; tile < ntiles; tile += gridDim.x) {
-    const int64_t base = tile * T::TILE;
-    const int valid = (int)min((int64_t)T::TILE, (int64_t)(n - base));
-    unsigned bits[IPT / 4];
-    int pos[IPT / 4];
-    int woff;
-    const int total = sel_count<BT, IPT>(v, valid, lo, hi, s_warp, bits, pos, woff);
-    if (threadIdx.x == 0) lookback_publish(status, tile, total);
-    sel_scatter<IPT>(v, bits, pos, woff, s_items);
-    const long long nt = tile + gridDim.x;
-    if (nt < ntiles)  // prefetch: overwrites v (already scattered to smem)
-      sel_load<BT, IPT>(in, nt * T::TILE, (int)min((int64_t)T::TILE, (int64_t)(n - nt * T::TILE)), v);
-    const long long off = block_lookback<BT>(status, tile, total, s_red, true);
-    for (int i = threadIdx.x; i < total; i += BT) out[off + i] = s_items[i];
-    if (threadIdx.x == 0 && tile == ntiles - 1) *total_out = off + total;
-    __syncthreads();  // s_items / s_warp reuse
-  }
-}
-
-template <int BT, int IPT, bool PERSIST, bool NOLB = false>
 __global__ void __launch_bounds__(BT) select_input_kernel(const int32_t* __restrict__ in, int64_t n,
                                                           int32_t lo, int32_t hi,
                                                           int32_t* __restrict__ out,
                                                           unsigned long long* status,
-                                                          unsigned long long* tile_counter,
                                                           long long ntiles, long long* total_out) {
   using T = SelTile<BT, IPT>;
   __shared__ __align__(16) int32_t s_items[T::TILE];
   __shared__ int s_warp[T::W];
-  __shared__ long long s_off, s_next;
   __shared__ long long s_red[T::W + T::W / 2 + 1];
-  if constexpr (!PERSIST) {
-    const long long tile = blockIdx.x;
-    const int64_t base = tile * T::TILE;
-    const int valid = (int)min((int64_t)T::TILE, (int64_t)(n - base));
-    int4 v[IPT / 4];
-    sel_load<BT, IPT>(in, base, valid, v);
-    const int total = sel_compact<BT, IPT>(v, valid, lo, hi, s_items, s_warp);
-    long long off;
-    if constexpr (NOLB) {  // timing experiment: no look-back (tile-private output slots)
-      __syncthreads();
-      off = tile * T::TILE;
-    } else {
-      off = block_lookback<BT>(status, tile, total, s_red);
-    }
-    for (int i = threadIdx.x; i < total; i += BT) out[off + i] = s_items[i];
-    if (threadIdx.x == 0 && tile == ntiles - 1) *total_out = off + total;
-  } else {
-    if (threadIdx.x == 0) s_next = (long long)atomicAdd(tile_counter, 1ull);
-    __syncthreads();
-    long long tile = s_next;
-    int4 v[IPT / 4], nv[IPT / 4];
-    if (tile < ntiles)
-      sel_load<BT, IPT>(in, tile * T::TILE, (int)min((int64_t)T::TILE, (int64_t)(n - tile * T::TILE)), v);
-    while (tile < ntiles) {
-      const int64_t base = tile * T::TILE;
-      const int valid = (int)min((int64_t)T::TILE, (int64_t)(n - base));
-      if (threadIdx.x == 0) s_next = (long long)atomicAdd(tile_counter, 1ull);
-      const int total = sel_compact<BT, IPT>(v, valid, lo, hi, s_items, s_warp);  // barrier inside
-      const long long nt = s_next;
-      if (nt < ntiles)
-        sel_load<BT, IPT>(in, nt * T::TILE, (int)min((int64_t)T::TILE, (int64_t)(n - nt * T::TILE)), nv);
-      if (threadIdx.x < 32) {
-        const long long off = tile_lookback(status, tile, total);
-        if (threadIdx.x == 0) s_off = off;
-      }
-      __syncthreads();
-      const long long off = s_off;
-      for (int i = threadIdx.x; i < total; i += BT) out[off + i] = s_items[i];
-      if (threadIdx.x == 0 && tile == ntiles - 1) *total_out = off + total;
-      __syncthreads();  // s_items / s_off / s_next reuse
-      tile = nt;
-#pragma unroll
-      for (int j = 0; j < IPT / 4; ++j) v[j] = nv[j];
-    }
-  }
+  const long long tile = blockIdx.x;
+  const int64_t base = tile * T::TILE;
+  const int valid = (int)min((int64_t)T::TILE, (int64_t)(n - base));
+  int4 v[IPT / 4];
+  sel_load<BT, IPT>(in, base, valid, v);
+  const int total = sel_compact<BT, IPT>(v, valid, lo, hi, s_items, s_warp);
+  const long long off = block_lookback<BT>(status, tile, total, s_red);
+  for (int i = threadIdx.x; i < total; i += BT) out[off + i] = s_items[i];
+  if (threadIdx.x == 0 && tile == ntiles - 1) *total_out = off + total;
 }
 
 // Reduce-then-scan form (no look-back latency on the critical path): pass 1
@@ -707,7 +631,7 @@ int64_t select_i32(crys_ctx* ctx, const int32_t* d_in, int64_t n, int32_t lo, in
   int chunk = 0;
   const int cfg = sel_cfg();
   if (order == CRYS_ORDER_INPUT) {
-    tile = cfg == 1 || cfg == 3 ? 8192 : 4096;  // cfg 6/7: 4096
+    tile = 4096;  // 128 threads x 32 items
   } else {
     CRYS_CHECK(order == CRYS_ORDER_CRYSTAL, CRYS_ECONFIG, "unknown select order");
     const int64_t S = (int64_t)bt * ipt;
@@ -720,48 +644,24 @@ int64_t select_i32(crys_ctx* ctx, const int32_t* d_in, int64_t n, int32_t lo, in
   const int64_t ntiles = (n + tile - 1) / tile;
   ctx->status.reserve(sizeof(unsigned long long) * (size_t)(ntiles + 2));
   auto* status = ctx->status.as<unsigned long long>();
-  auto* counter = status + ntiles;
   auto* total = reinterpret_cast<long long*>(status + ntiles + 1);
   CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(unsigned long long) * (size_t)(ntiles + 2), st));
   timing_kernel_begin(ctx);
   if (order == CRYS_ORDER_INPUT) {
-    auto launch = [&](auto fn, int bt_, bool persist) {
-      int grid = (int)ntiles;
-      if (persist) grid = (int)std::min<int64_t>(ntiles, (int64_t)occupancy((const void*)fn, bt_, 0) * ctx->num_sms);
-      fn<<<grid, bt_, 0, st>>>(d_in, n, lo, hi, d_out, status, counter, ntiles, total);
-    };
-    switch (cfg) {
-      case 1: launch(select_input_kernel<256, 32, false>, 256, false); break;
-      case 2: launch(select_input_kernel<256, 16, true>, 256, true); break;
-      case 3: launch(select_input_kernel<256, 32, true>, 256, true); break;
-      case 4: launch(select_input_kernel<128, 32, false>, 128, false); break;
-      case 5: launch(select_input_kernel<128, 32, false, true>, 128, false); break;
-      case 8: case 0: {
-        constexpr int BT = 128, IPT = 32;
-        ctx->scratch2.reserve(sizeof(unsigned) * (size_t)ntiles + sizeof(long long) * (size_t)(ntiles + 1) + 64);
-        unsigned* counts = ctx->scratch2.as<unsigned>();
-        long long* offs = reinterpret_cast<long long*>(counts + ((ntiles + 1) & ~1LL));
-        const int gc = (int)std::min<int64_t>(ntiles, (int64_t)occupancy((const void*)select_count_kernel<BT, IPT>, BT, 0) * ctx->num_sms);
-        select_count_kernel<BT, IPT><<<gc, BT, 0, st>>>(d_in, n, lo, hi, ntiles, counts);
-        select_scan_kernel<<<1, 1024, 0, st>>>(counts, ntiles, offs);
-        select_write_kernel<BT, IPT><<<(unsigned)ntiles, BT, 0, st>>>(d_in, n, lo, hi, ntiles, offs, d_out);
-        CUDA_TRY(cudaMemcpyAsync(total, offs + ntiles, sizeof(long long), cudaMemcpyDeviceToDevice, st));
-        count_launch(ctx, 2);
-        break;
-      }
-      case 6: {
-        auto fn = select_wave_kernel<256, 16>;
-        const int g = (int)std::min<int64_t>(ntiles, (int64_t)occupancy((const void*)fn, 256, 0) * ctx->num_sms);
-        fn<<<g, 256, 0, st>>>(d_in, n, lo, hi, d_out, status, ntiles, total);
-        break;
-      }
-      case 7: {
-        auto fn = select_wave_kernel<128, 32>;
-        const int g = (int)std::min<int64_t>(ntiles, (int64_t)occupancy((const void*)fn, 128, 0) * ctx->num_sms);
-        fn<<<g, 128, 0, st>>>(d_in, n, lo, hi, d_out, status, ntiles, total);
-        break;
-      }
-      default: launch(select_input_kernel<256, 16, false>, 256, false); break;  // cfg 9
+    constexpr int BT = 128, IPT = 32;
+    if (cfg == 1) {
+      select_input_kernel<BT, IPT><<<(unsigned)ntiles, BT, 0, st>>>(d_in, n, lo, hi, d_out, status, ntiles, total);
+    } else {
+      ctx->scratch2.reserve(sizeof(unsigned) * (size_t)ntiles + sizeof(long long) * (size_t)(ntiles + 1) + 64);
+      unsigned* counts = ctx->scratch2.as<unsigned>();
+      long long* offs = reinterpret_cast<long long*>(counts + ((ntiles + 1) & ~1LL));
+      const int gc = (int)std::min<int64_t>(
+          ntiles, (int64_t)occupancy((const void*)select_count_kernel<BT, IPT>, BT, 0) * ctx->num_sms);
+      select_count_kernel<BT, IPT><<<gc, BT, 0, st>>>(d_in, n, lo, hi, ntiles, counts);
+      select_scan_kernel<<<1, 1024, 0, st>>>(counts, ntiles, offs);
+      select_write_kernel<BT, IPT><<<(unsigned)ntiles, BT, 0, st>>>(d_in, n, lo, hi, ntiles, offs, d_out);
+      CUDA_TRY(cudaMemcpyAsync(total, offs + ntiles, sizeof(long long), cudaMemcpyDeviceToDevice, st));
+      count_launch(ctx, 2);
     }
   } else if (ipt <= 32) {
     const size_t dyn2 = sizeof(int32_t) * (size_t)chunk;
