@@ -202,35 +202,62 @@ __global__ void __launch_bounds__(BT) select_count_kernel(const int32_t* __restr
   }
 }
 
-// Exclusive scan of the per-tile counts into 64-bit offsets (+ the total at [ntiles]).
-__global__ void __launch_bounds__(1024) select_scan_kernel(const unsigned* counts, long long ntiles,
-                                                           long long* offsets) {
+// Exclusive scan of the per-tile counts, two tiny kernels with coalesced
+// 128-bit reads (a single CTA walking 131 K counts serially took 119 us):
+// select_scan_local_kernel scans each 4096-count block into local offsets and
+// a block total; select_scan_blocks_kernel scans the block totals into bases
+// (bases[nblk] = the grand total).  Offset of tile c = local[c] + bases[c>>12].
+constexpr int kScanBlk = 4096;
+__global__ void __launch_bounds__(1024) select_scan_local_kernel(const unsigned* counts, long long ntiles,
+                                                                 long long* local, long long* btot) {
   __shared__ long long sm[33];
-  const long long per = (ntiles + 1023) / 1024;
-  const long long b = threadIdx.x * per, e = min(ntiles, b + per);
-  long long local = 0;
-  for (long long i = b; i < e; ++i) local += counts[i];
+  const long long b0 = (long long)blockIdx.x * kScanBlk + 4 * threadIdx.x;
+  unsigned v[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) v[k] = b0 + k < ntiles ? counts[b0 + k] : 0u;
+  const long long mine = (long long)v[0] + v[1] + v[2] + v[3];
   long long tot;
-  long long run = BlockScan<1024>(local, sm, tot);
-  for (long long i = b; i < e; ++i) {
-    offsets[i] = run;
-    run += counts[i];
+  long long run = BlockScan<1024>(mine, sm, tot);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (b0 + k < ntiles) local[b0 + k] = run;
+    run += v[k];
   }
-  if (threadIdx.x == 0) offsets[ntiles] = tot;
+  if (threadIdx.x == 0) btot[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(1024) select_scan_blocks_kernel(const long long* btot, int nblk,
+                                                                  long long* bases) {
+  __shared__ long long sm[33];
+  long long run = 0;
+  for (int b0 = 0; b0 < nblk; b0 += 1024) {  // nblk <= 1024 for < 2^32 rows
+    const long long v = b0 + (int)threadIdx.x < nblk ? btot[b0 + threadIdx.x] : 0;
+    long long tot;
+    const long long ex = BlockScan<1024>(v, sm, tot);
+    if (b0 + (int)threadIdx.x < nblk) bases[b0 + threadIdx.x] = run + ex;
+    run += tot;
+  }
+  if (threadIdx.x == 0) bases[nblk] = run;
+}
+
+__device__ __forceinline__ long long sel_offset(const long long* local, const long long* bases, long long c,
+                                                long long ntiles) {
+  return c < ntiles ? local[c] + bases[c / kScanBlk] : bases[(ntiles + kScanBlk - 1) / kScanBlk];
 }
 
 template <int BT, int IPT>
 __global__ void __launch_bounds__(BT) select_write_kernel(const int32_t* __restrict__ in, int64_t n,
                                                           int32_t lo, int32_t hi, long long ntiles,
-                                                          const long long* offsets, int32_t* __restrict__ out) {
+                                                          const long long* local, const long long* bases,
+                                                          int32_t* __restrict__ out) {
   using T = SelTile<BT, IPT>;
   __shared__ __align__(16) int32_t s_items[T::TILE];
   __shared__ int s_warp[T::W];
   const long long tile = blockIdx.x;
   const int64_t base = tile * T::TILE;
   const int valid = (int)min((int64_t)T::TILE, (int64_t)(n - base));
-  const long long off = offsets[tile];
-  const int total = (int)(offsets[tile + 1] - off);
+  const long long off = sel_offset(local, bases, tile, ntiles);
+  const int total = (int)(sel_offset(local, bases, tile + 1, ntiles) - off);
   if (total == 0) return;  // whole CTA: uniform
   int4 v[IPT / 4];
   sel_load<BT, IPT>(in, base, valid, v);
@@ -334,10 +361,14 @@ __global__ void __launch_bounds__(kCrysPB) select_crystal_kernel(
 // packed 16 bits per g into one 64-bit block scan, and matches land in the
 // chunk's shared-memory output at their Crystal positions.  One look-back per
 // chunk.  IPTM >= ipt is the unrolled item bound (items stay in registers).
-template <int IPTM, int G>
+// KNOWN: the chunk offsets come from a count pass + scan (offsets[c]) instead
+// of the look-back (the reduce-then-scan form, as for the input-order select).
+template <int IPTM, int G, bool KNOWN = false>
 __global__ void __launch_bounds__(kCrysPB) select_crystal_reg_kernel(
     const int32_t* __restrict__ in, int64_t n, int32_t lo, int32_t hi, int bt, int ipt, int chunk,
-    int32_t* __restrict__ out, unsigned long long* status, long long* total_out) {
+    int32_t* __restrict__ out, unsigned long long* status, long long* total_out,
+    const long long* local = nullptr, const long long* bases = nullptr) {
+  const unsigned bt_magic = (unsigned)((0x100000000ull + (unsigned)bt - 1) / (unsigned)bt);  // ceil(2^32 / bt)
   static_assert(G >= 1 && G <= 4, "four 16-bit count fields per scan word");
   extern __shared__ int32_t s_dyn[];
   int32_t* s_out = s_dyn;  // [chunk]
@@ -346,6 +377,14 @@ __global__ void __launch_bounds__(kCrysPB) select_crystal_reg_kernel(
   const long long c = blockIdx.x;
   const int64_t base = c * (int64_t)chunk;
   const int valid = (int)min((int64_t)chunk, n - base);
+  const long long nchunks = (n + chunk - 1) / chunk;
+  if constexpr (KNOWN) {
+    const long long o = sel_offset(local, bases, c, nchunks);
+    if (sel_offset(local, bases, c + 1, nchunks) == o) {  // no match in this chunk (uniform exit)
+      if (threadIdx.x == 0 && base + chunk >= n) *total_out = o;
+      return;
+    }
+  }
   const int S = bt * ipt;
   const int pairs = ((valid + S - 1) / S) * bt;
   const int32_t* src = in + base;
@@ -359,7 +398,8 @@ __global__ void __launch_bounds__(kCrysPB) select_crystal_reg_kernel(
       f[g] = 0;
       const int p = p0 + g * kCrysPB + (int)threadIdx.x;
       if (p < pairs) {
-        const int j = p / bt, t = p - j * bt;
+        // j = p / bt by a multiply-high (exact: p * bt < 2^32 here)
+        const int j = (int)__umulhi((unsigned)p, bt_magic), t = p - j * bt;
         const int b = j * S + t;
 #pragma unroll
         for (int k = 0; k < IPTM; ++k) {
@@ -386,9 +426,47 @@ __global__ void __launch_bounds__(kCrysPB) select_crystal_reg_kernel(
     run = before;
   }
   __syncthreads();  // s_out complete (the look-back's barriers would also order it)
-  const long long off = block_lookback<kCrysPB>(status, c, run, s_red);
+  long long off;
+  if constexpr (KNOWN) {
+    off = sel_offset(local, bases, c, nchunks);
+  } else {
+    off = block_lookback<kCrysPB>(status, c, run, s_red);
+  }
   for (int i = threadIdx.x; i < run; i += kCrysPB) out[off + i] = s_out[i];
   if (threadIdx.x == 0 && base + chunk >= n) *total_out = off + run;
+}
+
+// Per-chunk match counts for the Crystal-order reduce-then-scan (chunks of any
+// length; scalar coalesced loads, four in flight per thread).
+__global__ void __launch_bounds__(256) select_chunk_count_kernel(const int32_t* __restrict__ in, int64_t n,
+                                                                 int32_t lo, int32_t hi, int chunk,
+                                                                 long long nchunks, unsigned* counts) {
+  __shared__ int s_warp[8];
+  for (long long c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const int64_t base = c * (int64_t)chunk;
+    const int valid = (int)min((int64_t)chunk, n - base);
+    int cnt = 0;
+    int i = threadIdx.x;
+    for (; i + 3 * 256 < valid; i += 4 * 256) {
+      const int32_t a = ld_stream1(in + base + i), b = ld_stream1(in + base + i + 256);
+      const int32_t e = ld_stream1(in + base + i + 512), f = ld_stream1(in + base + i + 768);
+      cnt += (a >= lo && a <= hi) + (b >= lo && b <= hi) + (e >= lo && e <= hi) + (f >= lo && f <= hi);
+    }
+    for (; i < valid; i += 256) {
+      const int32_t a = ld_stream1(in + base + i);
+      cnt += (a >= lo && a <= hi);
+    }
+    cnt = warp_sum(cnt);
+    if (lane_id() == 0) s_warp[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) t += s_warp[w];
+      counts[c] = (unsigned)t;
+    }
+    __syncthreads();
+  }
 }
 
 // project.hpp:49-64.  Linear: float mul, float mul, float add with no FMA
@@ -618,6 +696,33 @@ int occupancy(const void* fn, int bt, size_t smem) {
   return cache[key];
 }
 
+struct ScanBufs {
+  unsigned* counts = nullptr;
+  long long* local = nullptr;
+  long long* btot = nullptr;
+  long long* bases = nullptr;
+  int nblk = 0;
+};
+
+// counts[ntiles] | local[ntiles] | btot[nblk] | bases[nblk + 1] in ctx->scratch2
+ScanBufs scan_bufs(crys_ctx* ctx, int64_t ntiles) {
+  ScanBufs b;
+  b.nblk = (int)((ntiles + kScanBlk - 1) / kScanBlk);
+  CRYS_CHECK(b.nblk <= 1024 * 64, CRYS_ENOTBUILT, "select: too many tiles");
+  const size_t nc = ((size_t)ntiles + 1) & ~(size_t)1;
+  ctx->scratch2.reserve(4 * nc + 8 * ((size_t)ntiles + 2 * (size_t)b.nblk + 1) + 64);
+  b.counts = ctx->scratch2.as<unsigned>();
+  b.local = reinterpret_cast<long long*>(b.counts + nc);
+  b.btot = b.local + ntiles;
+  b.bases = b.btot + b.nblk;
+  return b;
+}
+
+void launch_scan(const ScanBufs& b, int64_t ntiles, cudaStream_t st) {
+  select_scan_local_kernel<<<b.nblk, 1024, 0, st>>>(b.counts, ntiles, b.local, b.btot);
+  select_scan_blocks_kernel<<<1, 1024, 0, st>>>(b.btot, b.nblk, b.bases);
+}
+
 }  // namespace
 
 int64_t select_i32(crys_ctx* ctx, const int32_t* d_in, int64_t n, int32_t lo, int32_t hi,
@@ -652,29 +757,48 @@ int64_t select_i32(crys_ctx* ctx, const int32_t* d_in, int64_t n, int32_t lo, in
     if (cfg == 1) {
       select_input_kernel<BT, IPT><<<(unsigned)ntiles, BT, 0, st>>>(d_in, n, lo, hi, d_out, status, ntiles, total);
     } else {
-      ctx->scratch2.reserve(sizeof(unsigned) * (size_t)ntiles + sizeof(long long) * (size_t)(ntiles + 1) + 64);
-      unsigned* counts = ctx->scratch2.as<unsigned>();
-      long long* offs = reinterpret_cast<long long*>(counts + ((ntiles + 1) & ~1LL));
+      ScanBufs sb = scan_bufs(ctx, ntiles);
       const int gc = (int)std::min<int64_t>(
           ntiles, (int64_t)occupancy((const void*)select_count_kernel<BT, IPT>, BT, 0) * ctx->num_sms);
-      select_count_kernel<BT, IPT><<<gc, BT, 0, st>>>(d_in, n, lo, hi, ntiles, counts);
-      select_scan_kernel<<<1, 1024, 0, st>>>(counts, ntiles, offs);
-      select_write_kernel<BT, IPT><<<(unsigned)ntiles, BT, 0, st>>>(d_in, n, lo, hi, ntiles, offs, d_out);
-      CUDA_TRY(cudaMemcpyAsync(total, offs + ntiles, sizeof(long long), cudaMemcpyDeviceToDevice, st));
-      count_launch(ctx, 2);
+      select_count_kernel<BT, IPT><<<gc, BT, 0, st>>>(d_in, n, lo, hi, ntiles, sb.counts);
+      launch_scan(sb, ntiles, st);
+      select_write_kernel<BT, IPT><<<(unsigned)ntiles, BT, 0, st>>>(d_in, n, lo, hi, ntiles, sb.local, sb.bases,
+                                                                    d_out);
+      CUDA_TRY(cudaMemcpyAsync(total, sb.bases + sb.nblk, sizeof(long long), cudaMemcpyDeviceToDevice, st));
+      count_launch(ctx, 4);
     }
   } else if (ipt <= 32) {
+    // reduce-then-scan (CRYS_SEL_CFG=1: single pass with the look-back)
     const size_t dyn2 = sizeof(int32_t) * (size_t)chunk;
+    const bool known = cfg != 1;
+    ScanBufs sb{};
+    if (known) {
+      sb = scan_bufs(ctx, ntiles);
+      const int gc = (int)std::min<int64_t>(ntiles, (int64_t)ctx->num_sms * 8);
+      select_chunk_count_kernel<<<gc, 256, 0, st>>>(d_in, n, lo, hi, chunk, ntiles, sb.counts);
+      launch_scan(sb, ntiles, st);
+      count_launch(ctx, 3);
+    }
     auto launch = [&](auto fn) {
       occupancy((const void*)fn, kCrysPB, dyn2);
-      fn<<<(unsigned)ntiles, kCrysPB, dyn2, st>>>(d_in, n, lo, hi, bt, ipt, chunk, d_out, status, total);
+      fn<<<(unsigned)ntiles, kCrysPB, dyn2, st>>>(d_in, n, lo, hi, bt, ipt, chunk, d_out, status, total, sb.local,
+                                                  sb.bases);
     };
-    if (ipt <= 1) launch(select_crystal_reg_kernel<1, 4>);
-    else if (ipt <= 2) launch(select_crystal_reg_kernel<2, 4>);
-    else if (ipt <= 4) launch(select_crystal_reg_kernel<4, 4>);
-    else if (ipt <= 8) launch(select_crystal_reg_kernel<8, 2>);
-    else if (ipt <= 16) launch(select_crystal_reg_kernel<16, 1>);
-    else launch(select_crystal_reg_kernel<32, 1>);
+    if (known) {
+      if (ipt <= 1) launch(select_crystal_reg_kernel<1, 4, true>);
+      else if (ipt <= 2) launch(select_crystal_reg_kernel<2, 4, true>);
+      else if (ipt <= 4) launch(select_crystal_reg_kernel<4, 4, true>);
+      else if (ipt <= 8) launch(select_crystal_reg_kernel<8, 2, true>);
+      else if (ipt <= 16) launch(select_crystal_reg_kernel<16, 1, true>);
+      else launch(select_crystal_reg_kernel<32, 1, true>);
+    } else {
+      if (ipt <= 1) launch(select_crystal_reg_kernel<1, 4>);
+      else if (ipt <= 2) launch(select_crystal_reg_kernel<2, 4>);
+      else if (ipt <= 4) launch(select_crystal_reg_kernel<4, 4>);
+      else if (ipt <= 8) launch(select_crystal_reg_kernel<8, 2>);
+      else if (ipt <= 16) launch(select_crystal_reg_kernel<16, 1>);
+      else launch(select_crystal_reg_kernel<32, 1>);
+    }
   } else {
     occupancy((const void*)select_crystal_kernel, kCrysPB, dyn);
     select_crystal_kernel<<<(unsigned)ntiles, kCrysPB, dyn, st>>>(d_in, n, lo, hi, bt, ipt, chunk, d_out,
