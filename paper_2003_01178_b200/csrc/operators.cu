@@ -368,7 +368,8 @@ __global__ void __launch_bounds__(kCrysPB) select_crystal_reg_kernel(
     const int32_t* __restrict__ in, int64_t n, int32_t lo, int32_t hi, int bt, int ipt, int chunk,
     int32_t* __restrict__ out, unsigned long long* status, long long* total_out,
     const long long* local = nullptr, const long long* bases = nullptr) {
-  const unsigned bt_magic = (unsigned)((0x100000000ull + (unsigned)bt - 1) / (unsigned)bt);  // ceil(2^32 / bt)
+  // ceil(2^32 / bt) (bt = 1 would need 2^32: handled without the multiply)
+  const unsigned bt_magic = bt > 1 ? (unsigned)((0x100000000ull + (unsigned)bt - 1) / (unsigned)bt) : 0u;
   static_assert(G >= 1 && G <= 4, "four 16-bit count fields per scan word");
   extern __shared__ int32_t s_dyn[];
   int32_t* s_out = s_dyn;  // [chunk]
@@ -399,7 +400,7 @@ __global__ void __launch_bounds__(kCrysPB) select_crystal_reg_kernel(
       const int p = p0 + g * kCrysPB + (int)threadIdx.x;
       if (p < pairs) {
         // j = p / bt by a multiply-high (exact: p * bt < 2^32 here)
-        const int j = (int)__umulhi((unsigned)p, bt_magic), t = p - j * bt;
+        const int j = bt == 1 ? p : (int)__umulhi((unsigned)p, bt_magic), t = p - j * bt;
         const int b = j * S + t;
 #pragma unroll
         for (int k = 0; k < IPTM; ++k) {

@@ -64,7 +64,7 @@ def test_select_edges_vs_oracle(env, n, op):
     k = tq.select_branching_into(x, pred, out)
     exp = orc.select(xh, op, lo, hi) if n else np.zeros(0, np.int32)
     assert k == len(exp) and np.array_equal(out[:k].cpu().numpy(), exp)
-    for bt, ipt in ((128, 4), (3, 5), (1024, 8)):
+    for bt, ipt in ((128, 4), (3, 5), (1024, 8), (1, 4), (2, 1), (7, 32)):
         k = tq.select_tile_into(x, pred, out, tq.TileConfig(bt, ipt))
         exp = orc.select(xh, op, lo, hi, order="crystal", bt=bt, ipt=ipt) if n else np.zeros(0, np.int32)
         assert k == len(exp) and np.array_equal(out[:k].cpu().numpy(), exp)
