@@ -50,6 +50,8 @@ crys_ctx::~crys_ctx() {
   delete staging;
   for (auto& e : io_ev)
     if (e) cudaEventDestroy(e);
+  if (graph_fence) cudaEventDestroy(graph_fence);
+  if (graph_stream) cudaStreamDestroy(graph_stream);
   if (copy_stream) cudaStreamDestroy(copy_stream);
   if (own_stream) cudaStreamDestroy(own_stream);
 }

@@ -135,6 +135,8 @@ struct crys_ctx {
   crys_db* staging = nullptr;  // device copies for crys_run_query_host
   cudaStream_t copy_stream = nullptr;  // H2D of crys_db_upload_host (lazy)
   crys::PinnedBuf io[2];               // CRYS column file staging (double-buffered)
+  cudaStream_t graph_stream = nullptr; // query graphs are captured/replayed here (lazy)
+  cudaEvent_t graph_fence = nullptr;
   cudaEvent_t io_ev[2] = {nullptr, nullptr};
   ~crys_ctx();
 };

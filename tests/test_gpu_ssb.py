@@ -189,3 +189,29 @@ def test_sharded_driver_over_uploaded_shard(tq):
         assert res.as_tuples() == exp, QUERY_NAMES[q]
         assert res.survivors == surv[:len(res.survivors)], QUERY_NAMES[q]
     db.free()
+
+
+def test_graph_replay_and_invalidation(tq):
+    """Per-query CUDA-graph replay: direct run, capture, replays all equal the
+    goldens; a column re-upload (new address / statistics) re-captures and the
+    results follow the new data."""
+    from oracle.oracle import Oracle
+    host = Oracle().generate(1, 42)
+    db = tq.DeviceDatabase.from_host(host)
+    for rep in range(4):
+        for q in (0, 3, 6, 10, 12):
+            rec = golden("sf1")["queries"][QUERY_NAMES[q]]
+            stats = tq.QueryStats()
+            assert tq.run_query(db, q, tq.TileConfig(), 1, stats).as_tuples() == golden_rows(rec), (rep, q)
+            assert stats.survivors == rec["survivors"]
+    # change the data under the cached graphs: every supplier moves to region 1
+    mod = {t: dict(c) for t, c in host.items()}
+    mod["supplier"] = dict(host["supplier"])
+    mod["supplier"]["s_region"] = np.ones_like(host["supplier"]["s_region"])
+    db.upload("supplier", "s_region", mod["supplier"]["s_region"])
+    orc = Oracle()
+    for rep in range(3):
+        for q in (3, 6, 10):
+            exp, surv = orc.query(mod, q)
+            assert tq.run_query(db, q).as_tuples() == exp, (rep, q)
+    db.free()
