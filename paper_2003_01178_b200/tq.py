@@ -24,6 +24,7 @@ import ctypes as C
 import enum
 import json
 import os
+import threading
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence, Tuple
 
@@ -504,10 +505,30 @@ def generate_ssb(sf: int, seed: int = 42, ctx: Optional[Context] = None) -> Devi
     return DeviceDatabase.generate(sf, seed, ctx=ctx)
 
 
+_OUT = threading.local()
+
+
+def _out_buffers(qid: int, maxr: int):
+    """Per-thread, per-query output buffers of the C ABI, allocated once: a
+    fresh np.empty of q4.3's 1.75 M-row bound costs an mmap/munmap pair on
+    every call.  Results are copied out (_rows_from_buffers)."""
+    cache = getattr(_OUT, "bufs", None)
+    if cache is None:
+        cache = _OUT.bufs = {}
+    b = cache.get(qid)
+    if b is None:
+        groups = np.empty(3 * maxr, np.int32)
+        sums = np.empty(maxr, np.int64)
+        surv = np.zeros(4, np.int64)
+        b = cache[qid] = (groups, sums, surv, C.c_void_p(groups.ctypes.data), C.c_void_p(sums.ctypes.data),
+                         C.c_void_p(surv.ctypes.data))
+    return b
+
+
 def _rows_from_buffers(qid, groups, sums, n) -> QueryResult:
     labels = _GROUP_LABELS[int(qid)]
     ng = len(labels)
-    g = np.ascontiguousarray(groups[:3 * n].reshape(n, 3)[:, :ng]) if n else np.zeros((0, ng), np.int32)
+    g = groups[:3 * n].reshape(n, 3)[:, :ng].copy() if n else np.zeros((0, ng), np.int32)
     return QueryResult(list(labels), groups=g, sums=np.array(sums[:n], np.int64))
 
 
@@ -534,15 +555,13 @@ def run_query(db, qid, config: TileConfig = TileConfig(), workers: int = 1,
     qid = int(qid)
     cells, ng, nj = _shape(qid)
     maxr = max(cells, 1)
-    groups = np.empty(3 * maxr, np.int32)  # untouched pages cost nothing; only n rows are written
-    sums = np.empty(maxr, np.int64)
-    surv = np.zeros(4, np.int64)
+    groups, sums, surv, gp, sp, vp = _out_buffers(qid, maxr)  # reused; rows are copied out below
+    surv[:] = 0
     n = C.c_int64()
     if isinstance(db, DeviceDatabase):
         ctx = db.ctx
         check(LIB.crys_run_query(ctx.h, db.h, qid, config.block_threads, config.items_per_thread,
-                                 groups.ctypes.data_as(C.c_void_p), sums.ctypes.data_as(C.c_void_p),
-                                 maxr, C.byref(n), surv.ctypes.data_as(C.c_void_p)))
+                                 gp, sp, maxr, C.byref(n), vp))
     else:
         ctx = ctx or Context.default()
         cols, keep = [], []
