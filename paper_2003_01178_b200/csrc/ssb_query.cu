@@ -369,7 +369,6 @@ __global__ void finalize_kernel(const unsigned long long* sums, const unsigned l
 // ---------------------------------------------------------- dispatch
 
 #define CRYS_F1_SHAPES(X) X(128, 4) X(256, 16) X(128, 16) X(512, 8) X(256, 8)
-constexpr int kNativeBT = 256, kNativeIPT = 16;  // flight 1 shape for uncompiled TileConfigs
 
 using F1Fn = void (*)(const Flight1Args);
 
@@ -386,7 +385,7 @@ F1Launch select_flight1() {
     const char* e = getenv("CRYS_F1_TILE");
     int b = 0, i = 0;
     if (e && sscanf(e, "%dx%d", &b, &i) == 2) return std::make_pair(b, i);
-    return std::make_pair(kNativeBT, kNativeIPT);
+    return std::make_pair(0, 0);  // no override: the prefetching default below
   }();
 #define X(B, I) \
   if (forced.first == B && forced.second == I) return {ssb_flight1_kernel<B, I>, B, I};
