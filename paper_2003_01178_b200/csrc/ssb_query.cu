@@ -482,18 +482,30 @@ int pipe_cfg() {
   return cfg;
 }
 
+// CRYS_TUNE=0 disables the per-query pipeline autotuner (default instantiation).
+bool tune_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CRYS_TUNE");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
 template <int NJ, int NC>
 void launch_pipeline_cfg(crys_ctx* ctx, const pipe::PipeArgs& pa, int64_t cells,
-                         const std::string& name) {
+                         const std::string& name, int cfg) {
   // Ring depth: 4 x 32 KB (q2/q3) or 3 x 48 KB (q4) stages.  Measured on
   // B200 (profiles/r01_pipeline_tuning.txt): the bytes in flight matter far
   // more than keeping a later join's table in shared memory -- dropping a
-  // stage to fit q3.1's date table costs 2.3x.
+  // stage to fit q3.1's date table costs 2.3x.  cfg 3/4 trade shared memory
+  // for more consumer warps (24 x 3072-row tiles / 20 x 2560): faster when
+  // the plan's tables and aggregate do not need that memory (picked per
+  // query by the autotuner below).
   constexpr int S = NC <= 4 ? 4 : 3;
-  switch (pipe_cfg()) {
+  switch (cfg) {
     case 1: launch_pipeline_k0<NJ, NC, 16, 4096, 2>(ctx, pa, cells, name); break;
-    case 2: launch_pipeline_k0<NJ, NC, 16, 2048, S>(ctx, pa, cells, name); break;
-
+    case 3: launch_pipeline_k0<NJ, NC, 24, 3072, NC <= 4 ? 3 : 2>(ctx, pa, cells, name); break;
+    case 4: launch_pipeline_k0<NJ, NC, 20, 2560, NC <= 4 ? 4 : 3>(ctx, pa, cells, name); break;
     default: launch_pipeline_k0<NJ, NC, 16, 2048, S>(ctx, pa, cells, name); break;
   }
 }
@@ -512,6 +524,19 @@ struct QueryGraph {
   int64_t kernels = 0;  // kernel nodes in the graph (launch accounting)
 };
 
+// Autotuning of the join-pipeline instantiation for 4-column plans (q2.x,
+// q3.x): on a database's first execution of such a query every candidate runs
+// twice back to back (aggregate re-zeroed before each run; the second run of
+// each is timed with CUDA events), the fastest is kept for every later call.
+// Results are identical for every candidate (the plans are tile-invariant);
+// only the shared-memory split between ring, tables and aggregate differs.
+constexpr int kTuneCand[3] = {0, 4, 3};
+struct PipeTune {
+  int chosen = -1;  // index into kTuneCand once decided
+  cudaEvent_t e0[3] = {nullptr, nullptr, nullptr}, e1[3] = {nullptr, nullptr, nullptr};
+  bool in_flight = false;  // the query in flight carries the measurements
+};
+
 struct QueryWorkspace {
   DevBuf agg;      // u64 [2*cells] + counters: surv[4] + err
   DevBuf meta;     // HtMeta[4]
@@ -521,9 +546,16 @@ struct QueryWorkspace {
   DevBuf result;   // ResultHeader + RowOut[cells]
   PinnedBuf host;
   std::map<std::pair<const crys_db*, int>, QueryGraph> graphs;
+  std::map<std::pair<const crys_db*, int>, PipeTune> tune;
+  PipeTune* measuring = nullptr;  // set by enqueue_query, completed after the sync
   ~QueryWorkspace() {
     for (auto& kv : graphs)
       if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    for (auto& kv : tune)
+      for (int k = 0; k < 3; ++k) {
+        if (kv.second.e0[k]) cudaEventDestroy(kv.second.e0[k]);
+        if (kv.second.e1[k]) cudaEventDestroy(kv.second.e1[k]);
+      }
   }
 };
 
@@ -547,7 +579,8 @@ static int64_t bit_ceil64(int64_t v) {
 // hands in caller-zeroed buffers.
 static void enqueue_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt,
                           unsigned long long* d_agg, unsigned long long* d_surv, int32_t* d_err,
-                          unsigned long long* zero_extra, int64_t zero_extra_n, bool prologue_zero) {
+                          unsigned long long* zero_extra, int64_t zero_extra_n, bool prologue_zero,
+                          bool tune_ok = false) {
   const QueryPlan& plan = plan_for(qid);
   CRYS_CHECK(bt > 0 && ipt > 0, CRYS_ECONFIG, "TileConfig: block_threads/items_per_thread must be positive");
   QueryWorkspace& ws = ws_of(ctx);
@@ -706,13 +739,41 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int
     CRYS_CHECK(plan.agg != kAggExtPriceTimesDiscount, CRYS_ENOTBUILT, "join flights aggregate revenue");
     pa.col[nj] = db->col("lineorder", "lo_revenue", &rows);
     if (plan.agg == kAggRevenueMinusSupplyCost) pa.col[nj + 1] = db->col("lineorder", "lo_supplycost", &rows);
+    int cfg = pipe_cfg();  // CRYS_PIPE_CFG > 0 forces an instantiation
+    auto launch = [&](int c) {
+      if (nj == 3 && plan.agg == kAggRevenue)
+        launch_pipeline_cfg<3, 4>(ctx, pa, cells, plan.name, c);
+      else if (nj == 4 && plan.agg == kAggRevenueMinusSupplyCost)
+        launch_pipeline_cfg<4, 6>(ctx, pa, cells, plan.name, c);
+      else
+        fail(CRYS_ENOTBUILT, "no fused pipeline for this plan shape");
+    };
+    if (cfg == 0 && nj == 3 && tune_enabled() && tune_ok) {
+      PipeTune& tn = ws.tune[{db, qid}];
+      if (tn.chosen >= 0) {
+        cfg = kTuneCand[tn.chosen];
+      } else {  // every candidate twice, the second run timed; the last run's result is kept
+        for (int k = 0; k < 3; ++k) {
+          if (!tn.e0[k]) {
+            CUDA_TRY(cudaEventCreate(&tn.e0[k]));
+            CUDA_TRY(cudaEventCreate(&tn.e1[k]));
+          }
+          for (int rep = 0; rep < 2; ++rep) {
+            if (k + rep > 0)  // re-zero [sums | counts | survivors | err] (the prologue zeroed it once)
+              CUDA_TRY(cudaMemsetAsync(d_agg, 0, sizeof(unsigned long long) * (size_t)(2 * cells + 5), st));
+            if (rep == 1) CUDA_TRY(cudaEventRecord(tn.e0[k], st));
+            launch(kTuneCand[k]);
+            if (rep == 1) CUDA_TRY(cudaEventRecord(tn.e1[k], st));
+            count_launch(ctx);
+          }
+        }
+        tn.in_flight = true;
+        ws.measuring = &tn;
+        return;
+      }
+    }
     timing_kernel_begin(ctx);
-    if (nj == 3 && plan.agg == kAggRevenue)
-      launch_pipeline_cfg<3, 4>(ctx, pa, cells, plan.name);
-    else if (nj == 4 && plan.agg == kAggRevenueMinusSupplyCost)
-      launch_pipeline_cfg<4, 6>(ctx, pa, cells, plan.name);
-    else
-      fail(CRYS_ENOTBUILT, "no fused pipeline for this plan shape");
+    launch(cfg);
     timing_kernel_end(ctx);
     count_launch(ctx);
     return;
@@ -871,12 +932,34 @@ void ssb_run_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt, R
   auto* surv = agg + 2 * cells;
   auto* err = reinterpret_cast<int32_t*>(surv + 4);
   auto enqueue = [&] {
+    ws.measuring = nullptr;
     enqueue_query(ctx, db, qid, bt, ipt, agg, surv, err, ws.result.as<unsigned long long>(),
-                  sizeof(ResultHeader) / 8, true);
+                  sizeof(ResultHeader) / 8, true, true);
     finalize_enqueue(ctx, qid, agg, surv, err, true);
+  };
+  // after the host part (stream synchronised): pick the fastest candidate
+  auto tune_done = [&] {
+    PipeTune* tn = ws.measuring;
+    ws.measuring = nullptr;
+    if (!tn || !tn->in_flight) return;
+    tn->in_flight = false;
+    float best = 1e30f;
+    for (int k = 0; k < 3; ++k) {
+      float ms = 0;
+      CUDA_TRY(cudaEventElapsedTime(&ms, tn->e0[k], tn->e1[k]));
+      if (ms < best) {
+        best = ms;
+        tn->chosen = k;
+      }
+    }
   };
   bool pending = false;
   for (const auto& kv : db->cols) pending = pending || kv.second.pending;
+  {  // still autotuning this (db, query): direct runs, no graph
+    auto it = ws.tune.find({db, qid});
+    const bool tunable = plan.joins.size() == 3 && tune_enabled() && pipe_cfg() == 0;
+    if (tunable && (it == ws.tune.end() || it->second.chosen < 0)) pending = true;
+  }
   // Graph replay: the launch sequence of a query is fixed for a given database
   // and workspace, so after one direct run (which sizes every buffer) it is
   // captured once and then replayed with ONE launch.  Not with per-query
@@ -885,6 +968,7 @@ void ssb_run_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt, R
     timing_begin(ctx);
     enqueue();
     finalize_host_part(ctx, qid, out);
+    tune_done();
     timing_end(ctx);
     return;
   }
@@ -913,6 +997,7 @@ void ssb_run_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt, R
     }
     enqueue();
     finalize_host_part(ctx, qid, out);
+    tune_done();
     g.sig = query_signature(ctx, db);
     return;
   }
