@@ -497,7 +497,7 @@ void launch_pipeline_cfg(crys_ctx* ctx, const pipe::PipeArgs& pa, int64_t cells,
   // Ring depth: 4 x 32 KB (q2/q3) or 3 x 48 KB (q4) stages.  Measured on
   // B200 (profiles/r01_pipeline_tuning.txt): the bytes in flight matter far
   // more than keeping a later join's table in shared memory -- dropping a
-  // stage to fit q3.1's date table costs 2.3x.  cfg 3/4 trade shared memory
+  // stage to fit q3.1's date table costs 2.3x.  cfg 3/4/6 trade shared memory
   // for more consumer warps (24 x 3072-row tiles / 20 x 2560): faster when
   // the plan's tables and aggregate do not need that memory (picked per
   // query by the autotuner below).
@@ -506,6 +506,7 @@ void launch_pipeline_cfg(crys_ctx* ctx, const pipe::PipeArgs& pa, int64_t cells,
     case 1: launch_pipeline_k0<NJ, NC, 16, 4096, 2>(ctx, pa, cells, name); break;
     case 3: launch_pipeline_k0<NJ, NC, 24, 3072, NC <= 4 ? 3 : 2>(ctx, pa, cells, name); break;
     case 4: launch_pipeline_k0<NJ, NC, 20, 2560, NC <= 4 ? 4 : 3>(ctx, pa, cells, name); break;
+    case 6: launch_pipeline_k0<NJ, NC, 20, 2560, NC <= 4 ? 3 : 2>(ctx, pa, cells, name); break;
     default: launch_pipeline_k0<NJ, NC, 16, 2048, S>(ctx, pa, cells, name); break;
   }
 }
@@ -530,10 +531,11 @@ struct QueryGraph {
 // each is timed with CUDA events), the fastest is kept for every later call.
 // Results are identical for every candidate (the plans are tile-invariant);
 // only the shared-memory split between ring, tables and aggregate differs.
-constexpr int kTuneCand[3] = {0, 4, 3};
+constexpr int kTuneN = 4;
+constexpr int kTuneCand[kTuneN] = {0, 4, 3, 6};
 struct PipeTune {
   int chosen = -1;  // index into kTuneCand once decided
-  cudaEvent_t e0[3] = {nullptr, nullptr, nullptr}, e1[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t e0[kTuneN] = {}, e1[kTuneN] = {};
   bool in_flight = false;  // the query in flight carries the measurements
 };
 
@@ -552,7 +554,7 @@ struct QueryWorkspace {
     for (auto& kv : graphs)
       if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
     for (auto& kv : tune)
-      for (int k = 0; k < 3; ++k) {
+      for (int k = 0; k < kTuneN; ++k) {
         if (kv.second.e0[k]) cudaEventDestroy(kv.second.e0[k]);
         if (kv.second.e1[k]) cudaEventDestroy(kv.second.e1[k]);
       }
@@ -753,7 +755,7 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int
       if (tn.chosen >= 0) {
         cfg = kTuneCand[tn.chosen];
       } else {  // every candidate twice, the second run timed; the last run's result is kept
-        for (int k = 0; k < 3; ++k) {
+        for (int k = 0; k < kTuneN; ++k) {
           if (!tn.e0[k]) {
             CUDA_TRY(cudaEventCreate(&tn.e0[k]));
             CUDA_TRY(cudaEventCreate(&tn.e1[k]));
@@ -944,7 +946,7 @@ void ssb_run_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt, R
     if (!tn || !tn->in_flight) return;
     tn->in_flight = false;
     float best = 1e30f;
-    for (int k = 0; k < 3; ++k) {
+    for (int k = 0; k < kTuneN; ++k) {
       float ms = 0;
       CUDA_TRY(cudaEventElapsedTime(&ms, tn->e0[k], tn->e1[k]));
       if (ms < best) {
