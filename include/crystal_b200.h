@@ -69,7 +69,11 @@ const char* crys_version(void);
  * per-call std::thread pool of parallel_for_blocks (kernel.cpp:60-103). */
 crys_status crys_init(int device, crys_ctx** out);
 void crys_destroy(crys_ctx* ctx);
-/* Run subsequent work on `cuda_stream` (a cudaStream_t; NULL = ctx stream). */
+/* Run subsequent work on `cuda_stream` (a cudaStream_t; NULL = the ctx's own
+ * stream).  The legacy default stream (handle 0, e.g. torch's default stream)
+ * is CRYS_STREAM_LEGACY -- passing 0 would select the ctx's own non-blocking
+ * stream, which does NOT order with work on the legacy stream. */
+#define CRYS_STREAM_LEGACY ((void*)0x1) /* == cudaStreamLegacy */
 crys_status crys_set_stream(crys_ctx* ctx, void* cuda_stream);
 crys_status crys_synchronize(crys_ctx* ctx);
 /* Number of kernels this ctx launched since creation (telemetry for bench). */

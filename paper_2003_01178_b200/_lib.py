@@ -16,6 +16,7 @@ CRYS_OK, CRYS_ECONFIG, CRYS_ECONTRACT, CRYS_EBUILD, CRYS_EIO, CRYS_ECUDA, CRYS_E
 CRYS_LT, CRYS_LE, CRYS_GT, CRYS_GE, CRYS_EQ, CRYS_BETWEEN = range(6)
 CRYS_ORDER_INPUT, CRYS_ORDER_CRYSTAL = 0, 1
 CRYS_SORT_LSB, CRYS_SORT_MSB = 0, 1
+CRYS_STREAM_LEGACY = 0x1  # cudaStreamLegacy
 
 
 class crys_pred(C.Structure):

@@ -180,7 +180,10 @@ class Context:
         """Run subsequent calls on torch's current stream (ordering with torch ops)."""
         import torch
         s = torch.cuda.current_stream(self.device)
-        check(LIB.crys_set_stream(self.h, C.c_void_p(s.cuda_stream)))
+        # torch's default stream is the legacy stream (handle 0): bind it as
+        # cudaStreamLegacy, not NULL (NULL selects the ctx's own non-blocking
+        # stream, which would race with torch and NCCL ops on the default stream)
+        check(LIB.crys_set_stream(self.h, C.c_void_p(s.cuda_stream or _lib.CRYS_STREAM_LEGACY)))
 
     def launches(self) -> int:
         return LIB.crys_kernel_launches(self.h)

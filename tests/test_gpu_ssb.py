@@ -215,3 +215,46 @@ def test_graph_replay_and_invalidation(tq):
             exp, surv = orc.query(mod, q)
             assert tq.run_query(db, q).as_tuples() == exp, (rep, q)
     db.free()
+
+
+@pytest.mark.slow
+def test_ssb_sf100_matches_reference(tq):
+    """BASELINE configs[4] size: all 13 queries at SF=100 (600 M lineorder rows)
+    on one B200 == the reference's own results."""
+    db = tq.DeviceDatabase.generate(100, 42)
+    try:
+        for q in range(13):
+            rec = golden("sf100")["queries"][QUERY_NAMES[q]]
+            stats = tq.QueryStats()
+            assert tq.run_query(db, q, tq.TileConfig(), 1, stats).as_tuples() == golden_rows(rec), QUERY_NAMES[q]
+            assert stats.survivors == rec["survivors"], QUERY_NAMES[q]
+    finally:
+        db.free()
+
+
+@pytest.mark.slow
+def test_ssb_sf100_eight_shards_merged(tq):
+    """The 8-GPU decomposition of SF=100 run shard by shard on one GPU: each
+    row-range shard generated in HBM, its dense partial from the same kernel
+    the multi-GPU path uses (crys_query_partial), the eight partials summed
+    (what the NCCL reduce does) and compacted on the device."""
+    import torch
+    from paper_2003_01178_b200 import dist as cdist
+    world = 8
+    total = cdist.lineorder_rows(100)
+    acc = {}
+    for r in range(world):
+        lo, hi = cdist.shard_range(total, r, world)
+        db = tq.DeviceDatabase.generate(100, 42, lo, hi)
+        sh = cdist.ShardedSSB.over(db)
+        for q in range(13):
+            buf = sh.partial(q)
+            acc[q] = buf.clone() if q not in acc else acc[q] + buf
+        torch.cuda.synchronize()
+        db.free()
+    ctx = tq.Context.default(torch.cuda.current_device())
+    for q in range(13):
+        rec = golden("sf100")["queries"][QUERY_NAMES[q]]
+        res = cdist.reduce_local(acc[q], q, ctx)
+        assert res.as_tuples() == golden_rows(rec), QUERY_NAMES[q]
+        assert res.survivors == rec["survivors"][:len(res.survivors)], QUERY_NAMES[q]
