@@ -32,12 +32,6 @@ int sel_cfg() {
   return cfg;
 }
 
-__device__ __forceinline__ unsigned lanemask_lt() {
-  unsigned m;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-  return m;
-}
-
 // Input-order selection (select_branching/predicated_into, workers=1: output
 // in input order).  Tile layout is WARP-CONTIGUOUS: warp w owns slots [w*32*IPT, (w+1)*32*IPT),
 // lane l's vector v is the 4 slots at w*32*IPT + v*128 + 4*l, so a warp's
@@ -47,7 +41,6 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // stored with coalesced writes.
 template <int BT, int IPT>
 struct SelTile {
-  static constexpr int NV = IPT / 4;
   static constexpr int TILE = BT * IPT;
   static constexpr int W = BT / 32;
   static_assert(IPT % 4 == 0, "128-bit vectors");

@@ -166,7 +166,6 @@ template <int NJ, int NC, int W, int TILE, int STAGES, int K0, bool S0>
 __global__ void __launch_bounds__((W + 1) * 32, 1) ssb_pipeline_kernel(const PipeArgs a) {
   constexpr int R = TILE / W;   // rows per consumer warp per stage
   constexpr int V = R / 128;    // int4 key vectors per lane (phase A)
-  constexpr int IT = V * 4;     // phase-A items per lane
   static_assert(R % 128 == 0 && V >= 1 && V <= 4, "phase A: 4..16 rows per lane");
   static_assert(NC - NJ == 1 || NC - NJ == 2, "aggregate columns");
   extern __shared__ __align__(128) unsigned char smem[];
