@@ -358,3 +358,22 @@ def test_sharded_sort_single_rank_nccl(env):
         assert np.array_equal(k.cpu().numpy(), kh[o]) and np.array_equal(p.cpu().numpy(), o)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.slow
+def test_project_sigmoid_2e26_vs_reference_math(env):
+    """The table-based double exp on a large sample: float results equal the
+    reference's float(1/(1+exp(-z))) with glibc's double exp (oracle, -O2,
+    no FMA contraction); at most a last-bit difference is tolerated per 2^26
+    (a double ulp survives rounding to float ~2^-29 of the time)."""
+    torch, tq, orc = env
+    n = 1 << 26
+    x1, x2 = orc.project_inputs(n, 77)
+    d1, d2 = _cuda(torch, x1), _cuda(torch, x2)
+    out = torch.empty_like(d1)
+    tq.project_sigmoid_into(d1, d2, 0.75, -1.25, out)
+    got = out.cpu().numpy().view(np.int32)
+    exp = orc.project(x1, x2, 0.75, -1.25, sigmoid=True).view(np.int32)
+    diff = np.nonzero(got != exp)[0]
+    assert len(diff) <= 1, len(diff)
+    assert np.all(np.abs(got[diff].astype(np.int64) - exp[diff]) <= 1)
