@@ -82,6 +82,21 @@ inline void set_decode(ProbeTab& t) {
 
 // PTX helpers (mbarrier, 1-D TMA bulk copy): async.cuh
 
+// 64-bit add into shared memory as 32-bit halves: sm_100a has no native
+// 64-bit shared atomic add (atomicAdd(u64*) on shared compiles to an
+// ATOMS.CAST.SPIN.64 compare-and-swap loop, which serialises under the
+// contention of a few hot groups, e.g. q3.1's 150 live cells).  One native
+// ATOMS.ADD on the low word; the high word only takes the carry out of it
+// plus the sign extension of a negative value (q4: revenue - supplycost).
+__device__ __forceinline__ void smem_add_i64(unsigned long long* cell, long long v) {
+  unsigned* w = reinterpret_cast<unsigned*>(cell);  // little-endian: w[0] low, w[1] high
+  const unsigned lo = (unsigned)v;
+  const unsigned hi = (unsigned)((unsigned long long)v >> 32);
+  const unsigned old = atomicAdd(w, lo);
+  const unsigned carry = (old + lo) < old ? 1u : 0u;
+  if (hi + carry) atomicAdd(w + 1, hi + carry);
+}
+
 // ------------------------------------------------------------- probes
 // Split into fetch (one load) and decode so a caller issues the loads of
 // several probes before consuming any.
@@ -305,7 +320,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) ssb_pipeline_kernel(const Pip
           long long v = q.va;
           if (NC - NJ == 2) v -= (long long)q.vb;
           if (a.smem_agg >= 0) {
-            atomicAdd(&s_sum[idx], (unsigned long long)v);
+            smem_add_i64(&s_sum[idx], v);
             atomicAdd(&s_cnt[idx], 1u);
           } else {
             atomicAdd(&a.g_sum[idx], (unsigned long long)v);
