@@ -157,7 +157,7 @@ __device__ __forceinline__ bool claim_code(void* tbl, uint32_t off, uint32_t cod
 // build_dim_table for every join at once (grid.y = join).  Each thread owns
 // kDimU rows per pass and issues all of their column loads before any
 // predicate is evaluated (one memory latency per pass, not one per column).
-constexpr int kDimU = 4;
+constexpr int kDimU = 2;
 __global__ void __launch_bounds__(256) dim_filter_kernel(const DimBuildArgs a) {
   const DimBuildDesc& d = a.d[blockIdx.y];
   HtMeta* m = a.meta + blockIdx.y;
