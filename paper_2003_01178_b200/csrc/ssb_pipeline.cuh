@@ -68,6 +68,7 @@ struct PipeArgs {
   unsigned long long* g_cnt;   // [cells]
   unsigned long long* surv;    // [4]
   int32_t* err;
+  int32_t l2_ahead;            // > 0: bulk-prefetch tile it + l2_ahead into L2 when issuing tile it
 };
 
 // Host: fill the uniform-decode fields of a direct table.
@@ -213,6 +214,14 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) ssb_pipeline_kernel(const Pip
 #pragma unroll
     for (int c = 0; c < NC; ++c)
       tma_load_1d(ring + ((size_t)s * NC + c) * TILE, a.col[c] + base, bytes, full + s, policy);
+    if (a.l2_ahead > 0) {  // the tile l2_ahead loads later: into L2 now (more bytes in flight than the ring holds)
+      const int64_t pb = (blockIdx.x + (int64_t)(it + a.l2_ahead) * gridDim.x) * (int64_t)TILE;
+      if (pb < a.n) {
+        const uint32_t pbytes = (uint32_t)((min((int64_t)TILE, a.n - pb) * 4 + 15) & ~15ll);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) l2_prefetch_bulk(a.col[c] + pb, pbytes);
+      }
+    }
   };
   if (warp == W && lane == 0) {
     policy = policy_evict_first();

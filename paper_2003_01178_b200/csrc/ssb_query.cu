@@ -482,6 +482,16 @@ int pipe_cfg() {
   return cfg;
 }
 
+// CRYS_L2_AHEAD=k: the producer also bulk-prefetches into L2 the tile it will
+// load k iterations later (0 = off).
+int l2_ahead() {
+  static const int v = [] {
+    const char* e = getenv("CRYS_L2_AHEAD");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 // CRYS_TUNE=0 disables the per-query pipeline autotuner (default instantiation).
 bool tune_enabled() {
   static const bool on = [] {
@@ -531,10 +541,20 @@ struct QueryGraph {
 // each is timed with CUDA events), the fastest is kept for every later call.
 // Results are identical for every candidate (the plans are tile-invariant);
 // only the shared-memory split between ring, tables and aggregate differs.
-constexpr int kTuneN = 4;
-constexpr int kTuneCand[kTuneN] = {0, 4, 3, 6};
+// Candidates: (instantiation, L2 look-ahead distance).  4-column plans
+// (q2.x, q3.x) try four instantiations with and without the L2 bulk prefetch;
+// 6-column plans (q4.x, whose 48 KB stages leave no room for wider rings)
+// only the look-ahead distances of the default instantiation.
+struct TuneCand {
+  int cfg, l2;
+};
+constexpr int kTuneN = 8;
+constexpr TuneCand kTune4[kTuneN] = {{0, 0}, {4, 0}, {3, 0}, {6, 0}, {0, 2}, {4, 2}, {3, 2}, {6, 2}};
+constexpr int kTuneN6 = 3;
+constexpr TuneCand kTune6[kTuneN6] = {{0, 0}, {0, 2}, {0, 4}};
 struct PipeTune {
-  int chosen = -1;  // index into kTuneCand once decided
+  int chosen = -1;  // index into the plan shape's candidate list once decided
+  int ncand = 0;
   cudaEvent_t e0[kTuneN] = {}, e1[kTuneN] = {};
   bool in_flight = false;  // the query in flight carries the measurements
 };
@@ -733,6 +753,7 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int
   if (nj) {
     pa.n = n;
     pa.meta = ws.meta.as<HtMeta>();
+    pa.l2_ahead = l2_ahead();
     pa.cells = (int32_t)cells;
     pa.g_sum = d_agg;
     pa.g_cnt = d_agg + cells;
@@ -742,20 +763,25 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int
     pa.col[nj] = db->col("lineorder", "lo_revenue", &rows);
     if (plan.agg == kAggRevenueMinusSupplyCost) pa.col[nj + 1] = db->col("lineorder", "lo_supplycost", &rows);
     int cfg = pipe_cfg();  // CRYS_PIPE_CFG > 0 forces an instantiation
-    auto launch = [&](int c) {
+    auto launch = [&](TuneCand c) {
+      pa.l2_ahead = c.l2;
       if (nj == 3 && plan.agg == kAggRevenue)
-        launch_pipeline_cfg<3, 4>(ctx, pa, cells, plan.name, c);
+        launch_pipeline_cfg<3, 4>(ctx, pa, cells, plan.name, c.cfg);
       else if (nj == 4 && plan.agg == kAggRevenueMinusSupplyCost)
-        launch_pipeline_cfg<4, 6>(ctx, pa, cells, plan.name, c);
+        launch_pipeline_cfg<4, 6>(ctx, pa, cells, plan.name, c.cfg);
       else
         fail(CRYS_ENOTBUILT, "no fused pipeline for this plan shape");
     };
-    if (cfg == 0 && nj == 3 && tune_enabled() && tune_ok) {
+    TuneCand run{cfg, l2_ahead()};
+    const TuneCand* cands = nj == 3 ? kTune4 : kTune6;
+    const int ncand = nj == 3 ? kTuneN : kTuneN6;
+    if (cfg == 0 && l2_ahead() == 0 && (nj == 3 || nj == 4) && tune_enabled() && tune_ok) {
       PipeTune& tn = ws.tune[{db, qid}];
       if (tn.chosen >= 0) {
-        cfg = kTuneCand[tn.chosen];
+        run = cands[tn.chosen];
       } else {  // every candidate twice, the second run timed; the last run's result is kept
-        for (int k = 0; k < kTuneN; ++k) {
+        tn.ncand = ncand;
+        for (int k = 0; k < ncand; ++k) {
           if (!tn.e0[k]) {
             CUDA_TRY(cudaEventCreate(&tn.e0[k]));
             CUDA_TRY(cudaEventCreate(&tn.e1[k]));
@@ -764,7 +790,7 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int
             if (k + rep > 0)  // re-zero [sums | counts | survivors | err] (the prologue zeroed it once)
               CUDA_TRY(cudaMemsetAsync(d_agg, 0, sizeof(unsigned long long) * (size_t)(2 * cells + 5), st));
             if (rep == 1) CUDA_TRY(cudaEventRecord(tn.e0[k], st));
-            launch(kTuneCand[k]);
+            launch(cands[k]);
             if (rep == 1) CUDA_TRY(cudaEventRecord(tn.e1[k], st));
             count_launch(ctx);
           }
@@ -775,7 +801,7 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int
       }
     }
     timing_kernel_begin(ctx);
-    launch(cfg);
+    launch(run);
     timing_kernel_end(ctx);
     count_launch(ctx);
     return;
@@ -946,7 +972,7 @@ void ssb_run_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt, R
     if (!tn || !tn->in_flight) return;
     tn->in_flight = false;
     float best = 1e30f;
-    for (int k = 0; k < kTuneN; ++k) {
+    for (int k = 0; k < tn->ncand; ++k) {
       float ms = 0;
       CUDA_TRY(cudaEventElapsedTime(&ms, tn->e0[k], tn->e1[k]));
       if (ms < best) {
@@ -959,7 +985,8 @@ void ssb_run_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt, R
   for (const auto& kv : db->cols) pending = pending || kv.second.pending;
   {  // still autotuning this (db, query): direct runs, no graph
     auto it = ws.tune.find({db, qid});
-    const bool tunable = plan.joins.size() == 3 && tune_enabled() && pipe_cfg() == 0;
+    const bool tunable = (plan.joins.size() == 3 || plan.joins.size() == 4) && tune_enabled() &&
+                         pipe_cfg() == 0 && l2_ahead() == 0;
     if (tunable && (it == ws.tune.end() || it->second.chosen < 0)) pending = true;
   }
   // Graph replay: the launch sequence of a query is fixed for a given database
