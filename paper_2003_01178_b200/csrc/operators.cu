@@ -660,7 +660,7 @@ constexpr int kJR = kJTile / kJW;
 template <int STAGES, bool SMEM>
 __global__ void __launch_bounds__((kJW + 1) * 32, 1) join_ring_kernel(
     const int32_t* __restrict__ keys, const int32_t* __restrict__ pays, int64_t n,
-    const int2* __restrict__ gslots, uint32_t mask, int shift, unsigned long long* out) {
+    const int2* __restrict__ gslots, uint32_t mask, int shift, unsigned long long* out, int l2_ahead) {
   constexpr int IT = kJR / 32;  // rows per lane per stage
   extern __shared__ __align__(128) unsigned char smem[];
   int32_t* ring = reinterpret_cast<int32_t*>(smem);
@@ -688,6 +688,14 @@ __global__ void __launch_bounds__((kJW + 1) * 32, 1) join_ring_kernel(
     pipe::mbar_expect_tx(full + s, 2 * bytes);
     pipe::tma_load_1d(ring + (size_t)s * 2 * kJTile, keys + base, bytes, full + s, policy);
     pipe::tma_load_1d(ring + (size_t)s * 2 * kJTile + kJTile, pays + base, bytes, full + s, policy);
+    if (l2_ahead > 0) {  // the tile l2_ahead loads later: into L2 now
+      const int64_t pb = (blockIdx.x + (int64_t)(it + l2_ahead) * gridDim.x) * (int64_t)kJTile;
+      if (pb < n) {
+        const uint32_t pbytes = (uint32_t)(min((int64_t)kJTile, n - pb) * 4);
+        pipe::l2_prefetch_bulk(keys + pb, pbytes);
+        pipe::l2_prefetch_bulk(pays + pb, pbytes);
+      }
+    }
   };
   if (warp == kJW && lane == 0) {
     policy = pipe::policy_evict_first();
@@ -768,6 +776,18 @@ __global__ void __launch_bounds__((kJW + 1) * 32, 1) join_ring_kernel(
     for (int w = 0; w < kJW; ++w) t += red[w];
     if (t) atomicAdd(out, (unsigned long long)t);
   }
+}
+
+// The probe ring's producer also bulk-prefetches tile it + k into L2 when the
+// table is on chip (k = 2; measured 0.361 -> 0.347 ms at 8 KB).  With the table
+// probed through L2 the prefetched lines compete with it (1.07 -> 1.12 ms at
+// 4 MB), so k = 0 there.  CRYS_JOIN_L2=k overrides both.
+int join_l2_ahead(bool table_on_chip) {
+  static const int v = [] {
+    const char* e = getenv("CRYS_JOIN_L2");
+    return e ? atoi(e) : -1;
+  }();
+  return v >= 0 ? v : (table_on_chip ? 2 : 0);
 }
 
 int occupancy(const void* fn, int bt, size_t smem) {
@@ -966,17 +986,17 @@ int64_t join_probe_sum(crys_ctx* ctx, const int32_t* d_keys, const int32_t* d_pa
       auto fn = join_ring_kernel<2, true>;
       ensure_dyn_smem((const void*)fn, ring2 + tbytes);
       fn<<<grid, (kJW + 1) * 32, ring2 + tbytes, st>>>(d_keys, d_payloads, n, ht->slots.as<int2>(), mask,
-                                                       ht->shift, out);
+                                                       ht->shift, out, join_l2_ahead(true));
     } else if (smem) {
       auto fn = join_ring_kernel<4, true>;
       ensure_dyn_smem((const void*)fn, ring4 + tbytes);
       fn<<<grid, (kJW + 1) * 32, ring4 + tbytes, st>>>(d_keys, d_payloads, n, ht->slots.as<int2>(), mask,
-                                                       ht->shift, out);
+                                                       ht->shift, out, join_l2_ahead(true));
     } else {
       auto fn = join_ring_kernel<6, false>;
       ensure_dyn_smem((const void*)fn, ring6);
       fn<<<grid, (kJW + 1) * 32, ring6, st>>>(d_keys, d_payloads, n, ht->slots.as<int2>(), mask, ht->shift,
-                                              out);
+                                              out, join_l2_ahead(false));
     }
     timing_kernel_end(ctx);
     count_launch(ctx);

@@ -200,6 +200,7 @@ struct OsPass {
   uint32_t* status;         // [tiles][256] look-back words
   uint32_t* tile_counter;
   int32_t total_tiles;      // single-segment tile count (segmented: first_tile[nseg])
+  int32_t l2_ahead;         // > 0: bulk-prefetch the tile this many tiles ahead into L2
 };
 
 // One stable pass: tile ranking + per-digit decoupled look-back + scatter.
@@ -264,6 +265,15 @@ __global__ void __launch_bounds__(kOsBT, 1024 / kOsBT) onesweep_kernel(OsPass a)
       pipe::mbar_expect_tx(&s_bar, 8u * (uint32_t)valid);
       pipe::tma_load_1d(s_k, a.kin + base, 4u * (uint32_t)valid, &s_bar, pol);
       pipe::tma_load_1d(s_p, a.pin + base, 4u * (uint32_t)valid, &s_bar, pol);
+      // the tile a CTA will claim ~one resident wave later: into L2 now
+      // (single-segment passes, where tile ids map to contiguous rows)
+      if (a.l2_ahead > 0 && !a.segs) {
+        const int64_t pb = base + (int64_t)a.l2_ahead * kOsTile;
+        if (pb + kOsTile <= ssize) {
+          pipe::l2_prefetch_bulk(a.kin + pb, 4u * kOsTile);
+          pipe::l2_prefetch_bulk(a.pin + pb, 4u * kOsTile);
+        }
+      }
     }
     pipe::mbar_wait(&s_bar, 0);
   } else {
@@ -383,6 +393,17 @@ __global__ void __launch_bounds__(kOsBT, 1024 / kOsBT) onesweep_kernel(OsPass a)
     a.kout[dst] = kk;
     a.pout[dst] = s_p[i];
   }
+}
+
+// Each onesweep tile also bulk-prefetches tile + k into L2 (CRYS_OS_L2=k,
+// 0 = off).  Default 296 (two CTAs' worth per SM ahead): LSB 2^28 7.68 ->
+// 7.47 ms on B200 (148..592 all within 0.1 %, 1184 worse).
+int os_l2_ahead() {
+  static const int v = [] {
+    const char* e = getenv("CRYS_OS_L2");
+    return e ? atoi(e) : 296;
+  }();
+  return v;
 }
 
 // Tuning/experiment knob: CRYS_OS_DBG=1 launches the no-look-back variant,
@@ -515,6 +536,7 @@ bool onesweep_passes(crys_ctx* ctx, SortWorkspace& ws, int32_t* sk, int32_t* sp,
     a.status = ws.status.as<uint32_t>() + (int64_t)p * 256 * tiles;
     a.tile_counter = ws.counters.as<uint32_t>() + p;
     a.total_tiles = (int32_t)tiles;
+    a.l2_ahead = os_l2_ahead();
     launch_onesweep(a, (unsigned)tiles, os_smem(), st);
     CRYS_LAUNCHED("onesweep_kernel");
     count_launch(ctx);
@@ -577,6 +599,7 @@ void msb_sort(crys_ctx* ctx, SortWorkspace& ws, int32_t* keys, int32_t* pays, in
     a.start = 24; a.bits = 8; a.segs = nullptr; a.n = n;
     a.bases = hist; a.bases_stride = 0;
     a.status = status; a.tile_counter = ctr; a.total_tiles = (int32_t)tiles1;
+    a.l2_ahead = os_l2_ahead();
     launch_onesweep(a, (unsigned)tiles1, os_smem(), st);
     CRYS_LAUNCHED("onesweep_kernel msb top");
   }
@@ -593,6 +616,7 @@ void msb_sort(crys_ctx* ctx, SortWorkspace& ws, int32_t* keys, int32_t* pays, in
     a.status = status + 256 * (tiles1 + p * tiles_seg);
     a.tile_counter = ctr + 1 + p;
     a.total_tiles = (int32_t)tiles_seg;
+    a.l2_ahead = os_l2_ahead();
     launch_onesweep(a, (unsigned)tiles_seg, os_smem(), st);
     CRYS_LAUNCHED("onesweep_kernel msb segmented");
     std::swap(ik, ok);
