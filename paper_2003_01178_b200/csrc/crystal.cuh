@@ -77,6 +77,21 @@ __device__ __forceinline__ void BlockLoad(const int32_t* __restrict__ tile, int 
   }
 }
 
+// BlockLoad for a tile base that may not be 16 B aligned (a caller's span
+// starting mid-vector): same VecLayout, scalar loads.
+template <int BT, int IPT>
+__device__ __forceinline__ void BlockLoadUnaligned(const int32_t* __restrict__ tile, int valid,
+                                                   int32_t (&items)[IPT]) {
+  using L = VecLayout<BT, IPT>;
+#pragma unroll
+  for (int v = 0; v < L::NV; ++v) {
+    const int s = v * BT * L::VEC + threadIdx.x * L::VEC;
+#pragma unroll
+    for (int e = 0; e < L::VEC; ++e)
+      if (s + e < valid) items[v * L::VEC + e] = ld_stream1(tile + s + e);
+  }
+}
+
 // BlockLoadSel (block_ops.hpp:36-50): load only vectors holding a set flag.
 // A fully false bitmap touches no source memory, as in the reference.
 template <int BT, int IPT>

@@ -50,16 +50,19 @@ template <int BT, int IPT>
 __device__ __forceinline__ void sel_load(const int32_t* __restrict__ in, int64_t base, int valid,
                                          int4 (&v)[IPT / 4]) {
   const int wb = (threadIdx.x >> 5) * 32 * IPT + 4 * (int)lane_id();
+  // tiles are 16 KB apart, so one check of the span's base decides the path
+  const bool vec_ok = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
 #pragma unroll
   for (int j = 0; j < IPT / 4; ++j) {
     const int s = wb + j * 128;
-    if (s + 4 <= valid) {
+    if (vec_ok && s + 4 <= valid) {
       v[j] = ld_stream4(in + base + s);
     } else {
       v[j] = make_int4(0, 0, 0, 0);
       if (s + 0 < valid) v[j].x = ld_stream1(in + base + s + 0);
       if (s + 1 < valid) v[j].y = ld_stream1(in + base + s + 1);
       if (s + 2 < valid) v[j].z = ld_stream1(in + base + s + 2);
+      if (s + 3 < valid) v[j].w = ld_stream1(in + base + s + 3);
     }
   }
 }
@@ -574,7 +577,10 @@ template <bool SIGMOID>
 __global__ void __launch_bounds__(256) project_kernel(const float* __restrict__ x1,
                                                       const float* __restrict__ x2, int64_t n,
                                                       float a, float b, float* __restrict__ out) {
-  const int64_t n4 = n / 4;
+  // float4 body only when all three spans are 16 B aligned (else scalar)
+  const bool vec_ok = ((reinterpret_cast<uintptr_t>(x1) | reinterpret_cast<uintptr_t>(x2) |
+                        reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+  const int64_t n4 = vec_ok ? n / 4 : 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
     const float4 u = ld_stream4f(x1 + 4 * i);
@@ -614,6 +620,7 @@ __global__ void __launch_bounds__(BT) join_probe_kernel(const int32_t* __restric
   using L = VecLayout<BT, IPT>;
   extern __shared__ int2 s_slots[];
   __shared__ long long red[BT / 32];
+  const bool aligned = ((reinterpret_cast<uintptr_t>(keys) | reinterpret_cast<uintptr_t>(pays)) & 15) == 0;
   if constexpr (SMEM) {
     const int cap = (int)mask + 1;
     for (int i = threadIdx.x; i < cap; i += BT) s_slots[i] = __ldg(slots + i);
@@ -625,8 +632,13 @@ __global__ void __launch_bounds__(BT) join_probe_kernel(const int32_t* __restric
     const int64_t base = tile * L::TILE;
     const int valid = (int)min((int64_t)L::TILE, n - base);
     int32_t k[IPT], p[IPT], hit[IPT];
-    BlockLoad<BT, IPT>(keys + base, valid, k);
-    BlockLoad<BT, IPT>(pays + base, valid, p);
+    if (aligned) {
+      BlockLoad<BT, IPT>(keys + base, valid, k);
+      BlockLoad<BT, IPT>(pays + base, valid, p);
+    } else {
+      BlockLoadUnaligned<BT, IPT>(keys + base, valid, k);
+      BlockLoadUnaligned<BT, IPT>(pays + base, valid, p);
+    }
     unsigned f = BlockValidMask<BT, IPT>(valid);
     if constexpr (SMEM)
       BlockProbeHashTableSmem<IPT>(k, f, hit, s_slots, mask, shift);

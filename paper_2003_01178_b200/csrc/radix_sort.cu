@@ -100,7 +100,9 @@ __global__ void __launch_bounds__(kHistBT) os_hist_kernel(const int32_t* __restr
     __syncthreads();
     int64_t i = b + threadIdx.x;
     // align to 4 elements, then 128-bit loads
-    const int64_t ab = min(e, (b + 3) & ~(int64_t)3);
+    // first element at a 16 B ADDRESS boundary (the span itself may start mid-vector)
+    const int64_t mis = (int64_t)(((16u - (uint32_t)(reinterpret_cast<uintptr_t>(keys + b) & 15u)) & 15u) >> 2);
+    const int64_t ab = min(e, b + mis);
     for (; i < ab; i += kHistBT)
       for (int p = 0; p < npass; ++p) atomicAdd(&h[p][digit_of(keys[i], start0 + p * bits, mask)], 1u);
     const int64_t nvec = (e - ab) >> 2;  // whole 16 B vectors from ab

@@ -377,3 +377,57 @@ def test_project_sigmoid_2e26_vs_reference_math(env):
     diff = np.nonzero(got != exp)[0]
     assert len(diff) <= 1, len(diff)
     assert np.all(np.abs(got[diff].astype(np.int64) - exp[diff]) <= 1)
+
+
+def test_misaligned_and_ragged_inputs(env):
+    """Device spans that start off a 16 B boundary (a torch slice) and lengths
+    that are not multiples of the vector width: every operator must take its
+    scalar path, not fault, and match the oracle."""
+    torch, tq, orc = env
+    n = 100_003
+    kh = orc.random_i32(n + 3, 5, 6, -1000, 1000)
+    base = _cuda(torch, kh)
+    for off in (1, 2, 3):
+        x = base[off:off + n - off]
+        xh = kh[off:off + n - off]
+        out = torch.empty(len(xh) + 4, dtype=torch.int32, device="cuda")[1:len(xh) + 1]
+        k = tq.select_branching_into(x, tq.PredicateSpec.lt(17), out)
+        assert np.array_equal(out[:k].cpu().numpy(), orc.select(xh, "lt", 17)), off
+        k = tq.select_tile_into(x, tq.PredicateSpec.lt(17), out, tq.TileConfig(128, 4))
+        assert np.array_equal(out[:k].cpu().numpy(), orc.select(xh, "lt", 17, order="crystal", bt=128, ipt=4)), off
+        # sort of a misaligned slice (LSB stable)
+        kk = x.clone()[0:0]
+        kk = torch.empty(len(xh) + 1, dtype=torch.int32, device="cuda")[1:]
+        kk.copy_(x)
+        pp = torch.empty(len(xh) + 1, dtype=torch.int32, device="cuda")[1:]
+        pp.copy_(torch.arange(len(xh), dtype=torch.int32, device="cuda"))
+        tq.lsb_radix_sort(kk, pp)
+        o = np.argsort(xh, kind="stable")
+        assert np.array_equal(kk.cpu().numpy(), xh[o]) and np.array_equal(pp.cpu().numpy(), o), off
+    # join probe over misaligned / ragged probe spans
+    bk = torch.arange(1, 1001, dtype=torch.int32, device="cuda")
+    bp = _cuda(torch, orc.random_i32(1000, 42, 4, 0, 999))
+    ht = tq.HashTable.build(bk, bp, 4096)
+    pk_h = orc.random_i32(50_001, 42, 5, 1, 1000)
+    pp_h = orc.random_i32(50_001, 42, 3, 0, 999)
+    pk_d = _cuda(torch, np.concatenate([[0], pk_h]).astype(np.int32))[1:]
+    pp_d = _cuda(torch, np.concatenate([[0], pp_h]).astype(np.int32))[1:]
+    bph = bp.cpu().numpy()
+    exp = int(np.sum(bph[pk_h - 1].astype(np.int64) + pp_h.astype(np.int64)))
+    assert tq.join_probe_tile(pk_d, pp_d, ht) == exp
+    ht.free()
+
+
+def test_project_misaligned_spans(env):
+    torch, tq, orc = env
+    n = 10_001
+    x1, x2 = orc.project_inputs(n + 1, 9)
+    d1 = _cuda(torch, x1)[1:]
+    d2 = _cuda(torch, x2)[1:]
+    out = torch.empty(n + 1, dtype=torch.float32, device="cuda")[1:]
+    tq.project_linear_into(d1, d2, 0.75, -1.25, out)
+    assert np.array_equal(out.cpu().numpy().view(np.int32),
+                          orc.project(x1[1:], x2[1:], 0.75, -1.25).view(np.int32))
+    tq.project_sigmoid_into(d1, d2, 0.75, -1.25, out)
+    assert np.array_equal(out.cpu().numpy().view(np.int32),
+                          orc.project(x1[1:], x2[1:], 0.75, -1.25, sigmoid=True).view(np.int32))
