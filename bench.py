@@ -44,6 +44,12 @@ FACT_COLS = [4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 6, 6, 6]
 METRIC = "SSB q1.1-q4.3 ms/query and scan GB/s vs HBM roofline"
 
 
+def local_device():
+    if os.environ.get("CRYS_BENCH_ONE_GPU") == "1":
+        return 0
+    return int(os.environ.get("LOCAL_RANK", 0))
+
+
 def fact_bytes(q, rows):
     return 4 * FACT_COLS[q] * rows
 
@@ -311,7 +317,7 @@ def run_ours(args, rank, world):
     from paper_2003_01178_b200 import dist as cdist
     from paper_2003_01178_b200 import tq
 
-    dev = int(os.environ.get("LOCAL_RANK", 0))
+    dev = local_device()
     torch.cuda.set_device(dev)
     sf = args.sf or (20 if world == 1 else 100)
     cfg = tq.TileConfig(args.bt, args.ipt)
@@ -525,8 +531,10 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(local_device())
+        # CRYS_BENCH_BACKEND=gloo (+ CRYS_BENCH_ONE_GPU=1) lets the N>1 code path
+        # run on a single-GPU box as a functional check; never a reported number
+        dist.init_process_group(os.environ.get("CRYS_BENCH_BACKEND", "nccl"))
     line, sh, sf = run_ours(args, rank, world)
     e2e = None if args.no_e2e else e2e_host(args, sh, sf, rank, world)
     if rank == 0:
