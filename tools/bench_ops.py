@@ -20,6 +20,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_2003_01178_b200 import cost_models as cm  # noqa: E402
@@ -63,6 +64,9 @@ def main():
     ap.add_argument("--quick", action="store_true", help="smaller sizes (smoke)")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--only", default="select,project,join,sort")
+    ap.add_argument("--cpu", action="store_true",
+                    help="also time the reference's own CPU operators (oracle/_ref, all host cores) "
+                         "on the same inputs: one line per op with impl=reference-cpu")
     args = ap.parse_args()
     hbm, kind = peak()
     g = golden()
@@ -174,5 +178,73 @@ def main():
                  80 * n, statistics.median(ks), statistics.median(ts), cm.model_sort(n, 4, prof))
 
 
+def cpu_reference(only, quick):
+    """The reference's CPU operators (its own C++ compiled into oracle/_ref,
+    workers = host cores), timed on the same generated inputs -- the baseline
+    beside the GPU numbers, not the target."""
+    import time
+    from oracle.oracle import Oracle, RefImpl
+    orc, ref = Oracle(), RefImpl()
+    cores = os.cpu_count() or 1
+
+    def t(fn, reps=2):
+        fn()
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            ts.append((time.perf_counter() - t0) * 1e3)
+        return min(ts)
+
+    def emit(rec, nbytes, ms):
+        rec.update({"impl": "reference-cpu", "cores": cores, "ms": round(ms, 3),
+                    "gbs": round(nbytes / (ms * 1e-3) / 1e9, 2)})
+        print(json.dumps(rec), flush=True)
+
+    if "select" in only:
+        n = (1 << 24) if quick else (1 << 29)
+        x = orc.random_i32(n, 42, 1, 0, (1 << 20) - 1)
+        lo = 1 << 19
+        m = len(ref.select(0, x, "lt", lo, workers=cores))
+        emit({"bench": "select", "variant": "branching", "n": n, "sigma": 0.5},
+             4 * n + 4 * m, t(lambda: ref.select(0, x, "lt", lo, workers=cores)))
+        emit({"bench": "select", "variant": "tile_arrival_128x4", "n": n, "sigma": 0.5},
+             4 * n + 4 * m, t(lambda: ref.select(3, x, "lt", lo, 0, 128, 4, 1, cores)))
+        del x
+    if "project" in only:
+        n = (1 << 24) if quick else (1 << 29)
+        x1, x2 = orc.project_inputs(n, 42)
+        for sig in (False, True):
+            emit({"bench": "project", "variant": "sigmoid" if sig else "linear", "n": n}, 12 * n,
+                 t(lambda: ref.project(x1, x2, 0.75, -1.25, sig, workers=cores)))
+        del x1, x2
+    if "join" in only:
+        P = (1 << 24) if quick else (1 << 28)
+        pp = orc.random_i32(P, 42, 3, 0, 999)
+        for H in (65536, 16 << 20, 1 << 30):
+            cap = H // 8
+            bn = cap // 2
+            bk = np.arange(1, bn + 1, dtype=np.int32)
+            bp = orc.random_i32(bn, 42, 4, 0, 999)
+            pk = orc.random_i32(P, 42, 5, 1, bn)
+            st, h = ref.ht_build(bk, bp, cap, workers=cores)
+            emit({"bench": "join_probe", "variant": "tile", "ht_bytes": H, "P": P}, 8 * P,
+                 t(lambda: ref.join_probe(h, pk, pp, 2, 128, 4, cores), reps=1))
+            ref.ht_free(h)
+    if "sort" in only:
+        n = (1 << 24) if quick else (1 << 28)
+        k0 = orc.random_i32(n, 42, 6, -(2 ** 31) // 2, (2 ** 31 - 1) // 2)
+        for msb in (False, True):
+            k, p = k0.copy(), np.arange(n, dtype=np.int32)
+            t0 = time.perf_counter()
+            ref.sort(k, p, msb, cores)
+            emit({"bench": "sort", "variant": "msb_8bit" if msb else "lsb_4x8", "n": n}, 80 * n,
+                 (time.perf_counter() - t0) * 1e3)
+
+
 if __name__ == "__main__":
     main()
+    if "--cpu" in sys.argv:
+        only = set(sys.argv[sys.argv.index("--only") + 1].split(",")) if "--only" in sys.argv else \
+            {"select", "project", "join", "sort"}
+        cpu_reference(only, "--quick" in sys.argv)
