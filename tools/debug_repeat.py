@@ -1,4 +1,6 @@
-"""Repeat SSB queries on SF=1 against the goldens; report any mismatch (flakiness hunt)."""
+"""Repeat SSB queries against the goldens; report any mismatch (flakiness hunt).
+
+    python tools/debug_repeat.py [reps] [qids] [sf]      (sf 1 or 20; graphs + autotuner active)"""
 import os
 import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -8,8 +10,9 @@ from paper_2003_01178_b200 import tq  # noqa: E402
 
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 20
 qs = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else list(range(13))
-db = tq.DeviceDatabase.generate(1, 42)
-g = golden("sf1")["queries"]
+sf = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+db = tq.DeviceDatabase.generate(sf, 42)
+g = golden(f"sf{sf}")["queries"]
 bad = 0
 for r in range(reps):
     for q in qs:
