@@ -373,15 +373,35 @@ __global__ void __launch_bounds__(kOsBT, 1024 / kOsBT) onesweep_kernel(OsPass a)
     const int d = threadIdx.x;
     uint32_t excl = 0;
     if constexpr (DBG != 1) {
-      for (int t = tile - 1; t >= first; --t) {
-        uint32_t w;
-        unsigned ns = 32;
-        while (((w = ld_relaxed(a.status + (int64_t)t * 256 + d)) >> 30) == 0) {
-          __nanosleep(ns);
-          ns = min(ns * 2, 512u);
+      // windows of kLB predecessors per round trip (independent loads), the
+      // closest inclusive prefix ends the walk; a not-yet-published word is
+      // re-polled on its own (the one-at-a-time walk spent 22 % of the
+      // kernel's stall samples in this loop)
+      constexpr int kLB = 4;  // measured: 1 -> 7.45, 2 -> 7.03, 4 -> 6.96, 8 -> 7.15, 16 -> 7.52 ms (LSB 2^28)
+      for (int t0 = tile - 1; t0 >= first; t0 -= kLB) {
+        uint32_t w[kLB];
+#pragma unroll
+        for (int j = 0; j < kLB; ++j)
+          w[j] = t0 - j >= first ? ld_relaxed(a.status + (int64_t)(t0 - j) * 256 + d) : kOsPre;
+        bool done = false;
+#pragma unroll
+        for (int j = 0; j < kLB; ++j) {
+          if (done) continue;
+          if ((w[j] >> 30) == 0) {
+            unsigned ns = 32;
+            while (((w[j] = ld_relaxed(a.status + (int64_t)(t0 - j) * 256 + d)) >> 30) == 0) {
+              __nanosleep(ns);
+              ns = min(ns * 2, 512u);
+            }
+          }
+          if (t0 - j < first) {
+            done = true;
+            continue;
+          }
+          excl += w[j] & kOsVal;
+          if ((w[j] >> 30) == 2) done = true;
         }
-        excl += w & kOsVal;
-        if ((w >> 30) == 2) break;
+        if (done) break;
       }
     }
     if (t_in != 0) st_relaxed(a.status + (int64_t)tile * 256 + d, kOsPre | (excl + cnt));
