@@ -267,11 +267,11 @@ __global__ void __launch_bounds__(kOsBT, 1024 / kOsBT) onesweep_kernel(OsPass a)
       pipe::mbar_expect_tx(&s_bar, 8u * (uint32_t)valid);
       pipe::tma_load_1d(s_k, a.kin + base, 4u * (uint32_t)valid, &s_bar, pol);
       pipe::tma_load_1d(s_p, a.pin + base, 4u * (uint32_t)valid, &s_bar, pol);
-      // the tile a CTA will claim ~one resident wave later: into L2 now
-      // (single-segment passes, where tile ids map to contiguous rows)
-      if (a.l2_ahead > 0 && !a.segs) {
+      // the rows a CTA will claim ~one resident wave later: into L2 now
+      // (tile ids follow the array order, also across MSB segments)
+      if (a.l2_ahead > 0) {
         const int64_t pb = base + (int64_t)a.l2_ahead * kOsTile;
-        if (pb + kOsTile <= ssize) {
+        if (pb + kOsTile <= a.n) {
           pipe::l2_prefetch_bulk(a.kin + pb, 4u * kOsTile);
           pipe::l2_prefetch_bulk(a.pin + pb, 4u * kOsTile);
         }
