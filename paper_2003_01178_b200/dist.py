@@ -168,15 +168,16 @@ def split_digits(global_counts, world: int):
 
 
 class DeviceSortOps:
-    """The device half of sharded_sort (every step a libcrystal_b200 kernel)."""
+    """The device half of sharded_sort / partitioned_join (every step a
+    libcrystal_b200 kernel).  Digits are 8-bit radix digits at `start`."""
 
-    def top_histogram(self, keys):
-        return tq.radix_histogram(keys, 24, 8, 1)[0]
+    def histogram(self, keys, start):
+        return tq.radix_histogram(keys, start, 8, 1)[0]
 
-    def partition_top(self, keys, payloads):
+    def partition(self, keys, payloads, start):
         import torch
         ok, op = torch.empty_like(keys), torch.empty_like(payloads)
-        tq.radix_partition(keys, payloads, ok, op, 24, 8)
+        tq.radix_partition(keys, payloads, ok, op, start, 8)
         return ok, op
 
     def local_sort(self, keys, payloads, algo):
@@ -185,28 +186,84 @@ class DeviceSortOps:
         else:
             tq.lsb_radix_sort(keys, payloads)
 
+    def join_checksum(self, bkeys, bpays, pkeys, ppays):
+        cap = 2
+        while cap < 2 * max(1, bkeys.numel()):
+            cap <<= 1
+        ht = tq.HashTable.build(bkeys, bpays, cap)
+        try:
+            return tq.join_probe_tile(pkeys, ppays, ht)
+        finally:
+            ht.free()
 
-def sharded_sort(keys, payloads, algo: str = "lsb", group=None, ops=None):
-    """This rank's output key range of the global (key, payload) sort."""
+
+def _digit_exchange(keys, payloads, start, group, ops, hist_all=None):
+    """Route every (key, payload) to the rank owning its 8-bit digit at
+    `start` (balanced contiguous digit ranges): local stable partition + one
+    all_to_all per column.  Received pairs are grouped by source rank, each
+    group in its partition (input) order."""
     import torch
     import torch.distributed as dist
-    ops = ops or DeviceSortOps()
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    hist = torch.as_tensor(np.asarray(ops.top_histogram(keys), np.int64))
-    if keys.is_cuda:
-        hist = hist.to(keys.device)
-    gathered = [torch.empty_like(hist) for _ in range(world)]
-    dist.all_gather(gathered, hist, group=group)
-    all_h = np.stack([g.cpu().numpy() for g in gathered])  # [world, 256]
-    bounds = split_digits(all_h.sum(axis=0), world)
-    send = [int(all_h[rank, bounds[r]:bounds[r + 1]].sum()) for r in range(world)]
-    recv = [int(all_h[r, bounds[rank]:bounds[rank + 1]].sum()) for r in range(world)]
-    pk, pp = ops.partition_top(keys, payloads)
+    if hist_all is None:
+        hist = torch.as_tensor(np.asarray(ops.histogram(keys, start), np.int64))
+        if keys.is_cuda:
+            hist = hist.to(keys.device)
+        gathered = [torch.empty_like(hist) for _ in range(world)]
+        dist.all_gather(gathered, hist, group=group)
+        hist_all = np.stack([g.cpu().numpy() for g in gathered])  # [world, 256]
+    bounds = split_digits(hist_all.sum(axis=0), world)
+    send = [int(hist_all[rank, bounds[r]:bounds[r + 1]].sum()) for r in range(world)]
+    recv = [int(hist_all[r, bounds[rank]:bounds[rank + 1]].sum()) for r in range(world)]
+    pk, pp = ops.partition(keys, payloads, start)
     ok = torch.empty(sum(recv), dtype=keys.dtype, device=keys.device)
     op = torch.empty(sum(recv), dtype=payloads.dtype, device=payloads.device)
     dist.all_to_all_single(ok, pk, recv, send, group=group)
     dist.all_to_all_single(op, pp, recv, send, group=group)
+    return ok, op, hist_all
+
+
+def sharded_sort(keys, payloads, algo: str = "lsb", group=None, ops=None):
+    """This rank's output key range of the global (key, payload) sort."""
+    ops = ops or DeviceSortOps()
+    ok, op, _ = _digit_exchange(keys, payloads, 24, group, ops)
     if ok.numel():
         ops.local_sort(ok, op, algo)
     return ok, op
+
+
+def partitioned_join_checksum(build_keys, build_payloads, probe_keys, probe_payloads, group=None, ops=None,
+                              digit_start: int = 0) -> int:
+    """Radix-partitioned hash join across ranks (PAPER 690):
+    build and probe sides are both routed by the same 8-bit key digit (the low
+    byte by default -- SSB-style dense keys spread evenly there), so every
+    rank joins only its key range: a 1/W-sized hash table built locally, the
+    local Q4 checksum (join.cpp:69-96: build payload + probe payload over
+    matches), and one SUM all-reduce.  Equal to the single-GPU checksum.
+    The digit ranges are balanced on the BUILD side's histogram."""
+    import torch
+    import torch.distributed as dist
+    ops = ops or DeviceSortOps()
+    bk, bp, hist_all = _digit_exchange(build_keys, build_payloads, digit_start, group, ops)
+    # the probe side follows the build side's digit ranges
+    world = dist.get_world_size(group)
+    hp = torch.as_tensor(np.asarray(ops.histogram(probe_keys, digit_start), np.int64))
+    if probe_keys.is_cuda:
+        hp = hp.to(probe_keys.device)
+    gathered = [torch.empty_like(hp) for _ in range(world)]
+    dist.all_gather(gathered, hp, group=group)
+    probe_all = np.stack([g.cpu().numpy() for g in gathered])
+    bounds = split_digits(hist_all.sum(axis=0), world)
+    rank = dist.get_rank(group)
+    send = [int(probe_all[rank, bounds[r]:bounds[r + 1]].sum()) for r in range(world)]
+    recv = [int(probe_all[r, bounds[rank]:bounds[rank + 1]].sum()) for r in range(world)]
+    ppk, ppp = ops.partition(probe_keys, probe_payloads, digit_start)
+    pk = torch.empty(sum(recv), dtype=probe_keys.dtype, device=probe_keys.device)
+    pp = torch.empty(sum(recv), dtype=probe_payloads.dtype, device=probe_payloads.device)
+    dist.all_to_all_single(pk, ppk, recv, send, group=group)
+    dist.all_to_all_single(pp, ppp, recv, send, group=group)
+    local = int(ops.join_checksum(bk, bp, pk, pp)) if pk.numel() and bk.numel() else 0
+    t = torch.tensor([local], dtype=torch.int64, device=probe_keys.device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return int(t.item())

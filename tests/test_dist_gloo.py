@@ -74,18 +74,18 @@ def test_sharded_ssb_gloo(world):
 
 class _NumpySortOps:
     """Test stand-in for dist.DeviceSortOps on CPU tensors (the product runs
-    these three steps as libcrystal_b200 kernels)."""
+    these steps as libcrystal_b200 kernels)."""
 
     @staticmethod
-    def _top(k):
-        return ((k.astype(np.int64) & 0xFFFFFFFF) ^ 0x80000000) >> 24
+    def _digit(k, start):
+        return (((k.astype(np.int64) & 0xFFFFFFFF) ^ 0x80000000) >> start) & 0xFF
 
-    def top_histogram(self, keys):
-        return np.bincount(self._top(keys.numpy()), minlength=256).astype(np.int64)
+    def histogram(self, keys, start):
+        return np.bincount(self._digit(keys.numpy(), start), minlength=256).astype(np.int64)
 
-    def partition_top(self, keys, payloads):
+    def partition(self, keys, payloads, start):
         import torch
-        o = np.argsort(self._top(keys.numpy()), kind="stable")
+        o = np.argsort(self._digit(keys.numpy(), start), kind="stable")
         return torch.from_numpy(keys.numpy()[o].copy()), torch.from_numpy(payloads.numpy()[o].copy())
 
     def local_sort(self, keys, payloads, algo):
@@ -93,6 +93,10 @@ class _NumpySortOps:
         k, p = keys.numpy()[o].copy(), payloads.numpy()[o].copy()
         keys.numpy()[:] = k
         payloads.numpy()[:] = p
+
+    def join_checksum(self, bk, bp, pk, pp):
+        m = dict(zip(bk.numpy().tolist(), bp.numpy().tolist()))
+        return sum(m[k] + p for k, p in zip(pk.numpy().tolist(), pp.numpy().tolist()) if k in m)
 
 
 def _sort_worker(rank, world, port, case, out):
@@ -151,3 +155,50 @@ def test_split_digits_balanced():
     assert b[0] == 0 and b[-1] == 256 and all(x <= y for x, y in zip(b, b[1:]))
     sizes = [int(c[b[r]:b[r + 1]].sum()) for r in range(3)]
     assert sizes == [100, 100, 100]
+
+
+def _join_worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+    from paper_2003_01178_b200 import dist as cdist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        bk, bp, pk, pp = _join_case()
+        blo, bhi = cdist.shard_range(len(bk), rank, world)
+        plo, phi = cdist.shard_range(len(pk), rank, world)
+        cs = cdist.partitioned_join_checksum(torch.from_numpy(bk[blo:bhi].copy()), torch.from_numpy(bp[blo:bhi].copy()),
+                                             torch.from_numpy(pk[plo:phi].copy()), torch.from_numpy(pp[plo:phi].copy()),
+                                             ops=_NumpySortOps())
+        out.put((rank, cs))
+    finally:
+        dist.destroy_process_group()
+
+
+def _join_case():
+    rng = np.random.default_rng(11)
+    nb, npb = 5000, 40_000
+    bk = rng.permutation(np.arange(1, nb + 1)).astype(np.int32)
+    bp = rng.integers(0, 1000, nb).astype(np.int32)
+    pk = rng.integers(1, nb + 500, npb).astype(np.int32)  # ~9 % misses
+    pp = rng.integers(0, 1000, npb).astype(np.int32)
+    return bk, bp, pk, pp
+
+
+def test_partitioned_join_gloo():
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_join_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    bk, bp, pk, pp = _join_case()
+    m = dict(zip(bk.tolist(), bp.tolist()))
+    exp = sum(m[k] + p for k, p in zip(pk.tolist(), pp.tolist()) if k in m)
+    assert all(cs == exp for _, cs in res)

@@ -431,3 +431,28 @@ def test_project_misaligned_spans(env):
     tq.project_sigmoid_into(d1, d2, 0.75, -1.25, out)
     assert np.array_equal(out.cpu().numpy().view(np.int32),
                           orc.project(x1[1:], x2[1:], 0.75, -1.25, sigmoid=True).view(np.int32))
+
+
+def test_partitioned_join_single_rank_nccl(env):
+    """dist.partitioned_join_checksum through the device ops and NCCL (world 1;
+    the multi-rank routing is covered by the gloo test) == the A.3 checksum."""
+    import socket
+    import torch.distributed as dist
+    from paper_2003_01178_b200 import dist as cdist
+    torch, tq, orc = env
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", rank=0, world_size=1, init_method=f"tcp://127.0.0.1:{port}")
+    try:
+        P = 1 << 20
+        rec = golden("ops")["join_p2e20"][3]
+        bn = rec["build"]
+        bk = torch.arange(1, bn + 1, dtype=torch.int32, device="cuda")
+        bp = _cuda(torch, orc.random_i32(bn, 42, 4, 0, 999))
+        pk = _cuda(torch, orc.random_i32(P, 42, 5, 1, bn))
+        pp = _cuda(torch, orc.random_i32(P, 42, 3, 0, 999))
+        assert cdist.partitioned_join_checksum(bk, bp, pk, pp) == rec["checksum"]
+    finally:
+        dist.destroy_process_group()
