@@ -45,6 +45,11 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 // 1-D TMA bulk copy global -> shared, completion counted on `bar` in bytes.
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
                                             uint64_t* bar, uint64_t policy) {
@@ -52,6 +57,15 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
       " [%0], [%1], %2, [%3], %4;" ::"r"(s_addr(dst)),
       "l"(src), "r"(bytes), "r"(s_addr(bar)), "l"(policy)
+      : "memory");
+}
+
+// Same without an L2 cache hint (evict_normal).
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1], %2, [%3];" ::"r"(s_addr(dst)),
+      "l"(src), "r"(bytes), "r"(s_addr(bar))
       : "memory");
 }
 

@@ -388,7 +388,7 @@ __device__ __forceinline__ long long block_lookback(unsigned long long* status, 
     if (threadIdx.x == 0) st[0] = kPre | (unsigned long long)aggregate;
     return 0;
   }
-  if (threadIdx.x == 0) st[tile] = kAgg | (unsigned long long)aggregate;
+  if (!published && threadIdx.x == 0) st[tile] = kAgg | (unsigned long long)aggregate;
   long long excl = 0;
   long long look = tile - 1;
   while (true) {

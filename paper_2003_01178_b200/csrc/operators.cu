@@ -33,14 +33,34 @@ int sel_l2_ahead() {
   return v;
 }
 
-// A/B knob: CRYS_SEL_CFG=1 runs the single-pass look-back select instead of
-// reduce-then-scan (both produce the input-order result).
+// A/B knob for the input-order select: 0 = segmented (default), 1 = single
+// pass with a decoupled look-back, 3 = count / scan / write (all produce the
+// same result).
 int sel_cfg() {
   static const int cfg = [] {
     const char* e = getenv("CRYS_SEL_CFG");
     return e ? atoi(e) : 0;
   }();
   return cfg;
+}
+
+// CRYS_SEL_PDL=0: launch the segments without programmatic dependent launch.
+bool sel_pdl() {
+  static const bool v = [] {
+    const char* e = getenv("CRYS_SEL_PDL");
+    return !(e && atoi(e) == 0);
+  }();
+  return v;
+}
+
+// CRYS_SEL_SEG: tiles per segment of the segmented select (multiple of 64).
+long long sel_seg() {
+  static const long long v = [] {
+    const char* e = getenv("CRYS_SEL_SEG");
+    const long long x = e ? atoll(e) : 32768;
+    return std::max(64ll, x / 64 * 64);
+  }();
+  return v;
 }
 
 // Input-order selection (select_branching/predicated_into, workers=1: output
@@ -57,9 +77,21 @@ struct SelTile {
   static_assert(IPT % 4 == 0, "128-bit vectors");
 };
 
-template <int BT, int IPT>
+__device__ __forceinline__ int4 ld_hint4(const int32_t* p, uint64_t pol) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+
+// POL: 0 = default L2 policy, 1 = evict_last, 2 = evict_first
+template <int BT, int IPT, int POL = 0>
 __device__ __forceinline__ void sel_load(const int32_t* __restrict__ in, int64_t base, int valid,
                                          int4 (&v)[IPT / 4]) {
+  uint64_t pol = 0;
+  if constexpr (POL == 1) pol = pipe::policy_evict_last();
+  if constexpr (POL == 2) pol = pipe::policy_evict_first();
   const int wb = (threadIdx.x >> 5) * 32 * IPT + 4 * (int)lane_id();
   // tiles are 16 KB apart, so one check of the span's base decides the path
   const bool vec_ok = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
@@ -67,7 +99,8 @@ __device__ __forceinline__ void sel_load(const int32_t* __restrict__ in, int64_t
   for (int j = 0; j < IPT / 4; ++j) {
     const int s = wb + j * 128;
     if (vec_ok && s + 4 <= valid) {
-      v[j] = ld_stream4(in + base + s);
+      if constexpr (POL == 0) v[j] = ld_stream4(in + base + s);
+      else v[j] = ld_hint4(in + base + s, pol);
     } else {
       v[j] = make_int4(0, 0, 0, 0);
       if (s + 0 < valid) v[j].x = ld_stream1(in + base + s + 0);
@@ -278,6 +311,109 @@ __global__ void __launch_bounds__(BT) select_write_kernel(const int32_t* __restr
   sel_compact<BT, IPT>(v, valid, lo, hi, s_items, s_warp);
   __syncthreads();
   for (int i = threadIdx.x; i < total; i += BT) out[off + i] = s_items[i];
+}
+
+// Segmented select (the default input-order path).  The input is cut into
+// segments of `seg` tiles and launch s runs two roles side by side: COUNT
+// CTAs stream segment s and publish per-tile counts (plus 64-tile group sums
+// and the segment total, by atomics); WRITE CTAs re-read segment s - 1,
+// counted by the previous launch, and write each tile at its offset = the
+// segment totals before it + the group sums before it in its segment + the
+// tile counts before it in its group (one round of loads per CTA: no scan
+// kernel, no look-back).  Launches are chained with programmatic dependent
+// launch: the next launch's count CTAs start while this one drains, and only
+// its write CTAs wait (griddepcontrol.wait) for this grid.
+//
+// Measured on B200 (2^29 rows, profiles/r01_select_segmented.txt): with
+// seg = 32768 (512 MB) the mixed roles and the missing scan kernels beat
+// count / scan / write by 8-20 %.  Segments of <= 32 MB with evict_last on
+// the count read DO make the re-read an L2 hit (DRAM reads 2.15 GB instead of
+// 4.2 GB; the default policy keeps < 16 MB of a stream), but the extra
+// launches cost more than the HBM bytes saved, so they are off by default
+// (CRYS_SEL_SEG).
+constexpr int kSegGroup = 64;
+
+template <int BT, int IPT, bool HINT>
+__global__ void __launch_bounds__(BT) select_seg_kernel(const int32_t* __restrict__ in, int64_t n, int32_t lo,
+                                                        int32_t hi, int32_t* __restrict__ out, long long ntiles,
+                                                        long long seg, long long s, unsigned* counts,
+                                                        unsigned* gsum, unsigned long long* stot,
+                                                        long long* total_out) {
+  using T = SelTile<BT, IPT>;
+  __shared__ __align__(16) int32_t s_items[T::TILE];
+  __shared__ int s_warp[T::W];
+  __shared__ long long s_red[T::W];
+  const unsigned lane = lane_id();
+  // roles interleaved by CTA index so HBM (count) and L2 (write) traffic mix
+  const long long c0 = s * seg, c1 = min(ntiles, c0 + seg);  // count range
+  const long long w0 = c0 - seg, w1 = c0;                    // write range (segment s-1)
+  const long long nc = max(0ll, c1 - c0), nw = s > 0 ? w1 - w0 : 0;
+  const long long b = blockIdx.x, both = min(nc, nw);
+  bool is_count;
+  long long tile;
+  if (b < 2 * both) {
+    is_count = (b & 1) == 0;
+    tile = (is_count ? c0 : w0) + (b >> 1);
+  } else {
+    is_count = nc > nw;
+    tile = (is_count ? c0 : w0) + both + (b - 2 * both);
+  }
+  const int64_t base = tile * T::TILE;
+  const int valid = (int)min((int64_t)T::TILE, (int64_t)(n - base));
+  // programmatic dependent launch: the next launch's CTAs may start as this
+  // one drains; only its WRITE role waits for this grid to complete
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  int4 v[IPT / 4];
+  if (is_count) {
+    sel_load<BT, IPT, HINT ? 1 : 0>(in, base, valid, v);
+    const int wb = (threadIdx.x >> 5) * 32 * IPT + 4 * (int)lane;
+    int c = 0;
+#pragma unroll
+    for (int j = 0; j < IPT / 4; ++j) {
+      const int s0 = wb + j * 128;
+      c += (s0 + 0 < valid && v[j].x >= lo && v[j].x <= hi) + (s0 + 1 < valid && v[j].y >= lo && v[j].y <= hi) +
+           (s0 + 2 < valid && v[j].z >= lo && v[j].z <= hi) + (s0 + 3 < valid && v[j].w >= lo && v[j].w <= hi);
+    }
+    c = warp_sum(c);
+    if (lane == 0) s_warp[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned t = 0;
+#pragma unroll
+      for (int w = 0; w < T::W; ++w) t += (unsigned)s_warp[w];
+      counts[tile] = t;
+      if (t) {
+        atomicAdd(gsum + tile / kSegGroup, t);
+        atomicAdd(stot + s, (unsigned long long)t);
+      }
+    }
+    return;
+  }
+  // write role: offset = segments before + groups before (in segment) + tiles before (in group)
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // segment s-1 counted (and everything before)
+  const unsigned mine = counts[tile];
+  if (mine == 0) return;  // uniform; nothing to write
+  sel_load<BT, IPT, HINT ? 2 : 0>(in, base, valid, v);  // in flight while the offset is summed
+  const long long sw = s - 1, g = tile / kSegGroup, g0 = (sw * seg) / kSegGroup, j0 = g * kSegGroup;
+  long long part = 0;
+  for (long long i = threadIdx.x; i < sw; i += BT) part += (long long)stot[i];
+  for (long long i = g0 + threadIdx.x; i < g; i += BT) part += gsum[i];
+  for (long long i = j0 + threadIdx.x; i < tile; i += BT) part += counts[i];
+  part = warp_sum(part);
+  if (lane == 0) s_red[threadIdx.x >> 5] = part;
+  sel_compact<BT, IPT>(v, valid, lo, hi, s_items, s_warp);  // its barrier also publishes s_red
+  __syncthreads();  // s_items complete
+  long long off = 0;
+#pragma unroll
+  for (int w = 0; w < T::W; ++w) off += s_red[w];
+  for (int i = threadIdx.x; i < (int)mine; i += BT) __stcs(out + off + i, s_items[i]);
+}
+
+__global__ void select_seg_total_kernel(const unsigned long long* stot, long long nseg, long long* total_out) {
+  unsigned long long t = 0;
+  for (long long i = threadIdx.x; i < nseg; i += 32) t += stot[i];
+  t = warp_sum(t);
+  if (threadIdx.x == 0) *total_out = (long long)t;
 }
 
 // Crystal order for an arbitrary logical (bt, ipt) (select_tile_into,
@@ -885,15 +1021,44 @@ int64_t select_i32(crys_ctx* ctx, const int32_t* d_in, int64_t n, int32_t lo, in
     dyn = sizeof(int32_t) * (size_t)(2 * chunk + pairs);
   }
   const int64_t ntiles = (n + tile - 1) / tile;
-  ctx->status.reserve(sizeof(unsigned long long) * (size_t)(ntiles + 2));
+  ctx->status.reserve(sizeof(unsigned long long) * (size_t)(ntiles + 3));
   auto* status = ctx->status.as<unsigned long long>();
   auto* total = reinterpret_cast<long long*>(status + ntiles + 1);
-  CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(unsigned long long) * (size_t)(ntiles + 2), st));
+  CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(unsigned long long) * (size_t)(ntiles + 3), st));
   timing_kernel_begin(ctx);
   if (order == CRYS_ORDER_INPUT) {
     constexpr int BT = 128, IPT = 32;
     if (cfg == 1) {
       select_input_kernel<BT, IPT><<<(unsigned)ntiles, BT, 0, st>>>(d_in, n, lo, hi, d_out, status, ntiles, total);
+    } else if (cfg != 3) {
+      const long long seg = sel_seg();
+      const long long nseg = (ntiles + seg - 1) / seg;
+      const size_t ng = (size_t)((ntiles + kSegGroup - 1) / kSegGroup);
+      ctx->scratch2.reserve(sizeof(unsigned) * (size_t)(ntiles + ng) + sizeof(unsigned long long) * (size_t)nseg + 16);
+      auto* counts = ctx->scratch2.as<unsigned>();
+      auto* gsum = counts + ntiles;
+      auto* stot = reinterpret_cast<unsigned long long*>(
+          (reinterpret_cast<uintptr_t>(gsum + ng) + 15) & ~(uintptr_t)15);
+      CUDA_TRY(cudaMemsetAsync(gsum, 0, reinterpret_cast<char*>(stot + nseg) - reinterpret_cast<char*>(gsum), st));
+      for (long long sg = 0; sg <= nseg; ++sg) {
+        const long long nc = sg < nseg ? std::min(seg, ntiles - sg * seg) : 0;
+        const long long nw = sg > 0 ? std::min(seg, ntiles - (sg - 1) * seg) : 0;
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3((unsigned)(nc + nw));
+        lc.blockDim = dim3(BT);
+        lc.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        lc.attrs = attr;
+        lc.numAttrs = sg > 0 && sel_pdl() ? 1 : 0;  // launch 0 follows the memset normally
+        // segments small enough to stay in L2 between the two roles
+        // (<= 32 MB) keep the counted tiles with evict_last
+        CUDA_TRY(cudaLaunchKernelEx(&lc, seg <= 2048 ? select_seg_kernel<BT, IPT, true> : select_seg_kernel<BT, IPT, false>,
+                                    d_in, n, lo, hi, d_out, (long long)ntiles, seg, sg, counts, gsum, stot, total));
+      }
+      select_seg_total_kernel<<<1, 32, 0, st>>>(stot, nseg, total);
+      count_launch(ctx, (int)nseg + 1);
     } else {
       ScanBufs sb = scan_bufs(ctx, ntiles);
       const int gc = (int)std::min<int64_t>(

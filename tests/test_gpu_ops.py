@@ -52,6 +52,27 @@ def test_select_golden_all_shapes(env):
                 assert col_digest(out[:n2].cpu().numpy()) == dig, key
 
 
+def test_select_multi_segment_vs_oracle(env):
+    """Input-order select across several segmented launches (segment = 2^27
+    rows by default) with a ragged tail, against the C oracle."""
+    torch, tq, orc = env
+    n = (1 << 28) + 3 * 4096 + 77
+    xh = orc.random_i32(n, 9, 2, 0, 999)
+    x = _cuda(torch, xh)
+    out = torch.empty_like(x)
+    for lt in (1, 500, 1000):
+        pred = tq.PredicateSpec.lt(lt)
+        k = tq.select_branching_into(x, pred, out)
+        exp = orc.select(xh, "lt", pred.lo, pred.hi)
+        assert k == len(exp)
+        assert np.array_equal(out[:k].cpu().numpy(), exp), lt
+    # misaligned start (scalar loads) through the same launches
+    pred = tq.PredicateSpec.lt(500)
+    k = tq.select_branching_into(x[1:], pred, out)
+    exp = orc.select(xh[1:].copy(), "lt", pred.lo, pred.hi)
+    assert k == len(exp) and np.array_equal(out[:k].cpu().numpy(), exp)
+
+
 @pytest.mark.parametrize("n", [0, 1, 3, 4095, 4096, 4097, 100_000, 1 << 22])
 @pytest.mark.parametrize("op", ["lt", "le", "gt", "ge", "eq", "between"])
 def test_select_edges_vs_oracle(env, n, op):
