@@ -714,14 +714,56 @@ __device__ __forceinline__ double exp_table(double x) {
   return __longlong_as_double(bits);
 }
 
+// Fast sigmoid candidate for |z| <= 80 (a normal float result):
+// y ~ 1/(1+exp(-z)) with relative error < 2^-43 (degree-4 polynomial on the
+// 2^(j/64) table, |r|^5/120 < 2^-44.6; one Newton step on the hardware
+// reciprocal seed).  Returns RN_float(y) and `sure` = y lies more than
+// 2^-13 half-ulps from the nearest float rounding midpoint, so the
+// reference's double result (within ~2^-50 of the true value) rounds to the
+// same float; otherwise the caller takes the near-correctly-rounded path.
+// Rounding to an integer is the 1.5*2^52 trick (no FRND / F2I on the XU
+// pipe, which bounded the previous version).
+__device__ __forceinline__ float sigmoid_fast(double z, bool& sure) {
+  const double x = -z;
+  const double sh = fma(x, 92.33248261689366, 0x1.8p52);  // 64/ln2, rounded to an integer in the low bits
+  const int n = __double2loint(sh);
+  const double nd = sh - 0x1.8p52;
+  double r = fma(-nd, 0.010830424667801708, x);
+  r = fma(-nd, 2.8447437476627285e-11, r);
+  double p = fma(r, 1.0 / 24, 1.0 / 6);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = p * r;
+  const double t = __ldg(&kExp2Tab[n & 63].x);
+  const double e = __longlong_as_double(__double_as_longlong(fma(t, p, t)) + ((long long)(n >> 6) << 52));
+  const double den = 1.0 + e;
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(den));
+  y = fma(y, fma(-den, y, 1.0), y);
+  const float f = __double2float_rn(y);
+  const double d = y - (double)f;  // exact (Sterbenz)
+  const int fb = __float_as_int(f);
+  // half an ulp of f towards d: 2^(ef - 151), one binade lower below a power of two
+  const int ef = (fb >> 23) & 0xff;
+  const int k = ef - 151 - ((d < 0.0 && (fb & 0x7fffff) == 0) ? 1 : 0);
+  const double hu = __hiloint2double((k + 1023) << 20, 0);
+  sure = fabs(d) < fma(hu, -0x1p-13, hu);
+  return f;
+}
+
 template <bool SIGMOID>
 __device__ __forceinline__ float project_one(float u, float v, float a, float b) {
   if constexpr (!SIGMOID) {
     return __fadd_rn(__fmul_rn(a, u), __fmul_rn(b, v));
   } else {
     // float(1 / (1 + exp(-z))) with z in double (project.hpp:56-64); the
-    // products of two floats are exact in double
-    const double z = __dadd_rn(__dmul_rn((double)a, (double)u), __dmul_rn((double)b, (double)v));
+    // products of two floats are exact in double, so one fma rounds z once
+    const double z = fma((double)a, (double)u, __dmul_rn((double)b, (double)v));
+    if (fabs(z) <= 80.0) {  // the float result is a normal number
+      bool sure;
+      const float f = sigmoid_fast(z, sure);
+      if (sure) return f;
+    }
     const double e = fabs(z) <= 700.0 ? exp_table(-z) : exp(-z);
     return __double2float_rn(__drcp_rn(__dadd_rn(1.0, e)));
   }
@@ -736,9 +778,21 @@ __global__ void __launch_bounds__(256) project_kernel(const float* __restrict__ 
                         reinterpret_cast<uintptr_t>(out)) & 15) == 0;
   const int64_t n4 = vec_ok ? n / 4 : 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
-    const float4 u = ld_stream4f(x1 + 4 * i);
-    const float4 v = ld_stream4f(x2 + 4 * i);
+  // the next vector pair is loaded before this one is computed: the sigmoid
+  // is long enough per element that one pair in flight per thread leaves
+  // HBM latency exposed
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  float4 un = make_float4(0.f, 0.f, 0.f, 0.f), vn = un;
+  if (i < n4) {
+    un = ld_stream4f(x1 + 4 * i);
+    vn = ld_stream4f(x2 + 4 * i);
+  }
+  for (; i < n4; i += stride) {
+    const float4 u = un, v = vn;
+    if (i + stride < n4) {
+      un = ld_stream4f(x1 + 4 * (i + stride));
+      vn = ld_stream4f(x2 + 4 * (i + stride));
+    }
     float4 r;
     r.x = project_one<SIGMOID>(u.x, v.x, a, b);
     r.y = project_one<SIGMOID>(u.y, v.y, a, b);
