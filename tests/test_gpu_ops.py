@@ -400,6 +400,29 @@ def test_project_sigmoid_2e26_vs_reference_math(env):
     assert np.all(np.abs(got[diff].astype(np.int64) - exp[diff]) <= 1)
 
 
+def test_project_sigmoid_wide_range_vs_reference_math(env):
+    """Sigmoid over |z| up to ~2000: the fast path's range limit (|z| <= 80),
+    the subnormal / saturated float results beyond it, and zeros and
+    subnormal inputs, against the oracle's double math."""
+    torch, tq, orc = env
+    rng = np.random.default_rng(3)
+    n = 1 << 22
+    x1 = rng.uniform(-1000, 1000, n).astype(np.float32)
+    x2 = rng.uniform(-1000, 1000, n).astype(np.float32)
+    x1[:64] = 0.0
+    x2[:64] = np.float32(1e-40)  # subnormal
+    x1[64:128] = np.float32(-1e-39)
+    d1, d2 = _cuda(torch, x1), _cuda(torch, x2)
+    out = torch.empty_like(d1)
+    for a, b in ((0.75, -1.25), (0.1, 0.05), (1.0, 1.0)):
+        tq.project_sigmoid_into(d1, d2, a, b, out)
+        got = out.cpu().numpy().view(np.int32)
+        exp = orc.project(x1, x2, a, b, sigmoid=True).view(np.int32)
+        diff = np.nonzero(got != exp)[0]
+        assert len(diff) <= 1, (a, b, len(diff))
+        assert np.all(np.abs(got[diff].astype(np.int64) - exp[diff]) <= 1)
+
+
 def test_misaligned_and_ragged_inputs(env):
     """Device spans that start off a 16 B boundary (a torch slice) and lengths
     that are not multiples of the vector width: every operator must take its
