@@ -34,7 +34,11 @@
 namespace crys {
 namespace {
 
-constexpr int kOsBT = 256, kOsIPT = 16;
+#ifndef CRYS_OS_IPT
+#define CRYS_OS_IPT 16
+#endif
+constexpr int kOsBT = 256, kOsIPT = CRYS_OS_IPT;
+constexpr int kOsMinBlocks = kOsIPT <= 16 ? 4 : (kOsIPT <= 24 ? 3 : 2);
 constexpr int kOsTile = kOsBT * kOsIPT;  // 4096 pairs (256 threads, 4 CTAs per SM: measured faster than 512 x 2)
 constexpr int kOsWarps = kOsBT / 32;
 constexpr uint32_t kOsAgg = 1u << 30, kOsPre = 2u << 30, kOsVal = (1u << 30) - 1;
@@ -217,7 +221,7 @@ struct OsPass {
 // pipes work in parallel -- measured best on B200 (LSB 2^28: match-only 11.8,
 // ballots-only 7.88, 1/4 match 7.68, 1/2 match 7.69, 3/8 match 8.00 ms).
 template <int DBG, int RANK>
-__global__ void __launch_bounds__(kOsBT, 1024 / kOsBT) onesweep_kernel(OsPass a) {
+__global__ void __launch_bounds__(kOsBT, kOsMinBlocks) onesweep_kernel(OsPass a) {
   extern __shared__ __align__(128) uint32_t os_sm[];
   int32_t* s_k = reinterpret_cast<int32_t*>(os_sm);           // [kOsTile] staged -> digit-sorted keys
   int32_t* s_p = s_k + kOsTile;                                // [kOsTile] staged -> digit-sorted payloads
