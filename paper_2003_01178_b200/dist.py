@@ -267,3 +267,105 @@ def partitioned_join_checksum(build_keys, build_payloads, probe_keys, probe_payl
     t = torch.tensor([local], dtype=torch.int64, device=probe_keys.device)
     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     return int(t.item())
+
+
+# --------------------------------------------------------------- operator shards
+# the operator microbenchmarks sharded by row range.  Rank r of W
+# holds rows [r*N//W, (r+1)*N//W) of the input (``shard_range``; for the
+# Crystal order aligned to whole logical tiles, ``shard_range_aligned``).
+
+def shard_range_aligned(total_rows: int, rank: int, world: int, align: int) -> Tuple[int, int]:
+    """Row range of `rank` with interior boundaries on multiples of `align`
+    (the Crystal-order select: a shard boundary must not split a logical
+    tile, select.hpp:107-135, or the per-tile thread-major order changes)."""
+    if align < 1:
+        raise tq.ConfigError("align must be >= 1")
+    units = (total_rows + align - 1) // align
+    lo, hi = shard_range(units, rank, world)
+    return min(lo * align, total_rows), min(hi * align, total_rows)
+
+
+class DeviceOperatorOps:
+    """The device half of the sharded operators (libcrystal_b200 kernels)."""
+
+    def select(self, x, pred, order="input", config=None):
+        import torch
+        out = torch.empty(max(1, x.numel()), dtype=x.dtype, device=x.device)
+        if order == "crystal":
+            k = tq.select_tile_into(x, pred, out, config or tq.TileConfig())
+        else:
+            k = tq.select_branching_into(x, pred, out)
+        return out[:k]
+
+    def join_checksum(self, ht, pkeys, ppays):
+        return tq.join_probe_tile(pkeys, ppays, ht)
+
+    def project(self, x1, x2, a, b, sigmoid=False):
+        import torch
+        out = torch.empty_like(x1)
+        (tq.project_sigmoid_into if sigmoid else tq.project_linear_into)(x1, x2, a, b, out)
+        return out
+
+
+def sharded_select(x_shard, pred, group=None, ops=None, order="input", config=None):
+    """Select over a row-range shard with one offset exchange:
+    the local matches, an all_gather of the per-rank match counts (one int64
+    each) and this rank's exclusive offset.  The global output -- the rank
+    segments concatenated at their offsets -- equals the single-GPU output in
+    input order (select_branching_into, workers=1) and, with tile-aligned
+    shards, in Crystal order.  Returns (local matches, offset, total)."""
+    import torch
+    import torch.distributed as dist
+    ops = ops or DeviceOperatorOps()
+    local = ops.select(x_shard, pred, order, config)
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    c = torch.tensor([int(local.numel())], dtype=torch.int64, device=x_shard.device)
+    counts = [torch.empty_like(c) for _ in range(world)]
+    dist.all_gather(counts, c, group=group)
+    cs = [int(t.item()) for t in counts]
+    return local, sum(cs[:rank]), sum(cs)
+
+
+def gather_select(local, offset: int, total: int, dst: int = 0, group=None):
+    """Assemble the global select output on rank `dst` (tests / small
+    outputs): the segments in rank order.  Other ranks get None."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    n = torch.tensor([int(local.numel())], dtype=torch.int64, device=local.device)
+    ns = [torch.empty_like(n) for _ in range(world)]
+    dist.all_gather(ns, n, group=group)
+    width = max(1, max(int(t.item()) for t in ns))
+    buf = torch.zeros(width, dtype=local.dtype, device=local.device)
+    buf[:local.numel()] = local
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    if rank != dst:
+        return None
+    out = torch.cat([p[:int(k.item())] for p, k in zip(parts, ns)])
+    if out.numel() != total or offset != sum(int(k.item()) for k in ns[:rank]):
+        raise tq.ContractError("gather_select: segment sizes disagree with the offset exchange")
+    return out
+
+
+def sharded_join_checksum(ht, probe_keys_shard, probe_payloads_shard, group=None, ops=None) -> int:
+    """Join probe with the probe side sharded by row range and the hash table
+    replicated (every rank builds it): the local Q4 checksum (join.cpp:69-96)
+    and one SUM all-reduce of an int64.  Equal to the
+    single-GPU checksum."""
+    import torch
+    import torch.distributed as dist
+    ops = ops or DeviceOperatorOps()
+    local = int(ops.join_checksum(ht, probe_keys_shard, probe_payloads_shard)) if probe_keys_shard.numel() else 0
+    t = torch.tensor([local], dtype=torch.int64, device=probe_keys_shard.device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return int(t.item())
+
+
+def sharded_project(x1_shard, x2_shard, a: float, b: float, sigmoid: bool = False, ops=None):
+    """Projection of a row-range shard: element-wise, no exchange (SURVEY
+    8(e)); the global output is the rank shards in order."""
+    ops = ops or DeviceOperatorOps()
+    return ops.project(x1_shard, x2_shard, a, b, sigmoid)

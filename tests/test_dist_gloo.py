@@ -202,3 +202,116 @@ def test_partitioned_join_gloo():
     m = dict(zip(bk.tolist(), bp.tolist()))
     exp = sum(m[k] + p for k, p in zip(pk.tolist(), pp.tolist()) if k in m)
     assert all(cs == exp for _, cs in res)
+
+
+# ------------------------------------------------------ operator shards (8(e))
+class _OracleOperatorOps:
+    """Test stand-in for dist.DeviceOperatorOps on CPU tensors: the C oracle
+    computes each rank's local step (the product runs libcrystal_b200)."""
+
+    def __init__(self):
+        from oracle.oracle import Oracle
+        self.orc = Oracle()
+
+    def select(self, x, pred, order="input", config=None):
+        import torch
+        bt, ipt = (config.block_threads, config.items_per_thread) if config else (128, 4)
+        r = self.orc.select(x.numpy(), "lt", pred.lo, pred.hi, order=order, bt=bt, ipt=ipt)
+        return torch.from_numpy(np.ascontiguousarray(r, np.int32))
+
+    def join_checksum(self, ht, pk, pp):
+        sk, sp = ht
+        return self.orc.join_checksum(pk.numpy(), pp.numpy(), sk, sp)
+
+    def project(self, x1, x2, a, b, sigmoid=False):
+        import torch
+        return torch.from_numpy(self.orc.project(x1.numpy(), x2.numpy(), a, b, sigmoid=sigmoid))
+
+
+def _ops_case():
+    rng = np.random.default_rng(5)
+    n = 100_003
+    x = rng.integers(0, 1000, n).astype(np.int32)
+    x1 = rng.uniform(-4, 4, n).astype(np.float32)
+    x2 = rng.uniform(-4, 4, n).astype(np.float32)
+    return x, x1, x2
+
+
+def _ops_worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+    from paper_2003_01178_b200 import dist as cdist
+    from paper_2003_01178_b200 import tq
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ops = _OracleOperatorOps()
+        x, x1, x2 = _ops_case()
+        pred = tq.PredicateSpec.lt(300)
+        res = {}
+        # input order: plain row ranges
+        lo, hi = cdist.shard_range(len(x), rank, world)
+        local, off, total = cdist.sharded_select(torch.from_numpy(x[lo:hi].copy()), pred, ops=ops)
+        res["input"] = cdist.gather_select(local, off, total)
+        # Crystal order: shards aligned to whole logical tiles (3 x 5 = 15)
+        cfg = tq.TileConfig(3, 5)
+        lo, hi = cdist.shard_range_aligned(len(x), rank, world, 15)
+        local, off, total = cdist.sharded_select(torch.from_numpy(x[lo:hi].copy()), pred, ops=ops,
+                                                 order="crystal", config=cfg)
+        res["crystal"] = cdist.gather_select(local, off, total)
+        # join: hash table replicated, probe side sharded
+        bk, bp, pk, pp = _join_case()
+        _, sk, sp = ops.orc.ht_build(bk, bp, 16384)
+        plo, phi = cdist.shard_range(len(pk), rank, world)
+        res["join"] = cdist.sharded_join_checksum((sk, sp), torch.from_numpy(pk[plo:phi].copy()),
+                                                  torch.from_numpy(pp[plo:phi].copy()), ops=ops)
+        # project: row ranges, no exchange
+        lo, hi = cdist.shard_range(len(x1), rank, world)
+        res["project"] = (lo, cdist.sharded_project(torch.from_numpy(x1[lo:hi].copy()),
+                                                    torch.from_numpy(x2[lo:hi].copy()), 0.75, -1.25,
+                                                    sigmoid=True, ops=ops).numpy())
+        out.put((rank, {k: (v.numpy() if hasattr(v, "numpy") else v) for k, v in res.items()}))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_operators_gloo():
+    """Select (one offset exchange, input and Crystal order), replicated-table
+    join (one SUM all-reduce) and row-range project over 3 gloo ranks equal
+    the single-process oracle results."""
+    from oracle.oracle import Oracle
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ops_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    orc = Oracle()
+    x, x1, x2 = _ops_case()
+    assert np.array_equal(res[0]["input"], orc.select(x, "lt", 300, 0))
+    assert np.array_equal(res[0]["crystal"], orc.select(x, "lt", 300, 0, order="crystal", bt=3, ipt=5))
+    assert res[1]["input"] is None and res[2]["crystal"] is None
+    bk, bp, pk, pp = _join_case()
+    m = dict(zip(bk.tolist(), bp.tolist()))
+    exp = sum(m[k] + p for k, p in zip(pk.tolist(), pp.tolist()) if k in m)
+    assert all(r["join"] == exp for r in res.values())
+    proj = np.concatenate([res[r]["project"][1] for r in range(world)])
+    assert np.array_equal(proj.view(np.int32), orc.project(x1, x2, 0.75, -1.25, sigmoid=True).view(np.int32))
+
+
+def test_shard_range_aligned():
+    from paper_2003_01178_b200 import dist as cdist
+    for n, world, align in ((100_003, 3, 15), (10, 4, 4), (0, 2, 8), (64, 8, 512)):
+        prev = 0
+        for r in range(world):
+            lo, hi = cdist.shard_range_aligned(n, r, world, align)
+            assert lo == prev and lo <= hi <= n
+            assert lo % align == 0 or lo == n
+            prev = hi
+        assert prev == n
