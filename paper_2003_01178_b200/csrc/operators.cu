@@ -598,6 +598,26 @@ __global__ void __launch_bounds__(256) select_chunk_count_kernel(const int32_t* 
     const int valid = (int)min((int64_t)chunk, n - base);
     int cnt = 0;
     int i = threadIdx.x;
+    const int32_t* cb = in + base;
+    const int lead = min(valid, (int)(((16 - (reinterpret_cast<uintptr_t>(cb) & 15)) & 15) / 4));
+    if ((reinterpret_cast<uintptr_t>(cb) & 3) == 0) {
+      // 128-bit body from the first 16 B boundary (the count is order-free)
+      if ((int)threadIdx.x < lead) {
+        const int32_t a = ld_stream1(cb + threadIdx.x);
+        cnt += (a >= lo && a <= hi);
+      }
+      const int nv = (valid - lead) / 4;
+      const int32_t* vb = cb + lead;
+      for (int v = threadIdx.x; v < nv; v += 256) {
+        const int4 q = ld_stream4(vb + 4 * v);
+        cnt += (q.x >= lo && q.x <= hi) + (q.y >= lo && q.y <= hi) + (q.z >= lo && q.z <= hi) + (q.w >= lo && q.w <= hi);
+      }
+      for (int r = lead + 4 * nv + threadIdx.x; r < valid; r += 256) {
+        const int32_t a = ld_stream1(cb + r);
+        cnt += (a >= lo && a <= hi);
+      }
+      i = valid;  // done
+    }
     for (; i + 3 * 256 < valid; i += 4 * 256) {
       const int32_t a = ld_stream1(in + base + i), b = ld_stream1(in + base + i + 256);
       const int32_t e = ld_stream1(in + base + i + 512), f = ld_stream1(in + base + i + 768);
@@ -1136,25 +1156,27 @@ int64_t select_i32(crys_ctx* ctx, const int32_t* d_in, int64_t n, int32_t lo, in
       launch_scan(sb, ntiles, st);
       count_launch(ctx, 3);
     }
-    auto launch = [&](auto fn) {
-      occupancy((const void*)fn, kCrysPB, dyn2);
-      fn<<<(unsigned)ntiles, kCrysPB, dyn2, st>>>(d_in, n, lo, hi, bt, ipt, chunk, d_out, status, total, sb.local,
-                                                  sb.bases);
+    auto launch = [&](auto fn, size_t dyn_bytes) {
+      occupancy((const void*)fn, kCrysPB, dyn_bytes);
+      fn<<<(unsigned)ntiles, kCrysPB, dyn_bytes, st>>>(d_in, n, lo, hi, bt, ipt, chunk, d_out, status, total,
+                                                       sb.local, sb.bases);
     };
+    // (a TMA-staged chunk variant measured slower: 3 instead of 5 CTAs per
+    // SM, profiles/r01_select_segmented.txt)
     if (known) {
-      if (ipt <= 1) launch(select_crystal_reg_kernel<1, 4, true>);
-      else if (ipt <= 2) launch(select_crystal_reg_kernel<2, 4, true>);
-      else if (ipt <= 4) launch(select_crystal_reg_kernel<4, 4, true>);
-      else if (ipt <= 8) launch(select_crystal_reg_kernel<8, 2, true>);
-      else if (ipt <= 16) launch(select_crystal_reg_kernel<16, 1, true>);
-      else launch(select_crystal_reg_kernel<32, 1, true>);
+      if (ipt <= 1) launch(select_crystal_reg_kernel<1, 4, true>, dyn2);
+      else if (ipt <= 2) launch(select_crystal_reg_kernel<2, 4, true>, dyn2);
+      else if (ipt <= 4) launch(select_crystal_reg_kernel<4, 4, true>, dyn2);
+      else if (ipt <= 8) launch(select_crystal_reg_kernel<8, 2, true>, dyn2);
+      else if (ipt <= 16) launch(select_crystal_reg_kernel<16, 1, true>, dyn2);
+      else launch(select_crystal_reg_kernel<32, 1, true>, dyn2);
     } else {
-      if (ipt <= 1) launch(select_crystal_reg_kernel<1, 4>);
-      else if (ipt <= 2) launch(select_crystal_reg_kernel<2, 4>);
-      else if (ipt <= 4) launch(select_crystal_reg_kernel<4, 4>);
-      else if (ipt <= 8) launch(select_crystal_reg_kernel<8, 2>);
-      else if (ipt <= 16) launch(select_crystal_reg_kernel<16, 1>);
-      else launch(select_crystal_reg_kernel<32, 1>);
+      if (ipt <= 1) launch(select_crystal_reg_kernel<1, 4>, dyn2);
+      else if (ipt <= 2) launch(select_crystal_reg_kernel<2, 4>, dyn2);
+      else if (ipt <= 4) launch(select_crystal_reg_kernel<4, 4>, dyn2);
+      else if (ipt <= 8) launch(select_crystal_reg_kernel<8, 2>, dyn2);
+      else if (ipt <= 16) launch(select_crystal_reg_kernel<16, 1>, dyn2);
+      else launch(select_crystal_reg_kernel<32, 1>, dyn2);
     }
   } else {
     occupancy((const void*)select_crystal_kernel, kCrysPB, dyn);
