@@ -129,6 +129,7 @@ struct crys_ctx {
   double kernel_ms = 0, total_ms = 0;
   // generic scratch
   crys::DevBuf scratch, scratch2, status;
+  crys::DevBuf part;  // radix-partitioned join probe: the probe pairs by hash bucket
   crys::PinnedBuf pinned;
   std::unique_ptr<crys::QueryWorkspace, crys::WsDeleter> qws;
   std::unique_ptr<crys::SortWorkspace, crys::WsDeleter> sws;

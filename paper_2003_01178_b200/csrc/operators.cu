@@ -1022,6 +1022,193 @@ __global__ void __launch_bounds__((kJW + 1) * 32, 1) join_ring_kernel(
 // table is on chip (k = 2; measured 0.361 -> 0.347 ms at 8 KB).  With the table
 // probed through L2 the prefetched lines compete with it (1.07 -> 1.12 ms at
 // 4 MB), so k = 0 there.  CRYS_JOIN_L2=k overrides both.
+// ---- radix-partitioned probe for tables far beyond L2 (PAPER's radix join;
+// the checksum is order-free).  Bucket = the top k bits of the Fibonacci
+// hash = the top k bits of the home slot, so bucket p's probes start inside
+// slots [p cap/2^k, (p+1) cap/2^k): one ~8 MB slice of the table.  A
+// histogram pass and a scatter pass (per-tile bucket ranks by shared-memory
+// atomics, one global claim per bucket per tile) group the probe pairs by
+// bucket; the TMA-ring probe then streams them in bucket order, so the CTAs
+// in flight share one L2-resident slice instead of missing to HBM.
+constexpr int kHpBT = 256, kHpIPT = 16, kHpTile = kHpBT * kHpIPT;
+
+__device__ __forceinline__ uint32_t hp_bucket(int32_t key, int bshift) {
+  return (uint32_t)((uint32_t)key * kFibonacci) >> bshift;
+}
+
+// CTA c of `grid` owns the contiguous tiles [c T / grid, (c+1) T / grid) in
+// both passes, so the scatter needs no global atomics: its per-bucket
+// offsets come from the histogram pass (hp_offsets_kernel).
+__device__ __forceinline__ void hp_chunk(int64_t ntiles, int& t0, int& t1) {
+  t0 = (int)(((int64_t)blockIdx.x * ntiles) / gridDim.x);
+  t1 = (int)(((int64_t)(blockIdx.x + 1) * ntiles) / gridDim.x);
+}
+
+__global__ void __launch_bounds__(kHpBT) hp_hist_kernel(const int32_t* __restrict__ keys, int64_t n, int bshift,
+                                                        int nb, unsigned* hist, unsigned* totals) {
+  __shared__ unsigned h[kHpBT / 32][256];  // per-warp sub-histograms: less atomic contention
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < (kHpBT / 32) * 256; i += kHpBT) (&h[0][0])[i] = 0;
+  __syncthreads();
+  int t0, t1;
+  hp_chunk((n + kHpTile - 1) / kHpTile, t0, t1);
+  const int64_t v0 = (int64_t)t0 * (kHpTile / 4), v1 = min((int64_t)t1 * (kHpTile / 4), n / 4);
+  for (int64_t i = v0 + threadIdx.x; i < v1; i += kHpBT) {  // n % 4 == 0, 16 B aligned (host)
+    const int4 k = ld_stream4(keys + 4 * i);
+    atomicAdd(&h[warp][hp_bucket(k.x, bshift)], 1u);
+    atomicAdd(&h[warp][hp_bucket(k.y, bshift)], 1u);
+    atomicAdd(&h[warp][hp_bucket(k.z, bshift)], 1u);
+    atomicAdd(&h[warp][hp_bucket(k.w, bshift)], 1u);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nb; b += kHpBT) {
+    unsigned t = 0;
+#pragma unroll
+    for (int w = 0; w < kHpBT / 32; ++w) t += h[w][b];
+    hist[(size_t)blockIdx.x * nb + b] = t;
+    if (t) atomicAdd(&totals[b], t);
+  }
+}
+
+// One CTA per bucket b: off[c][b] = (sum of the totals before b) + (the
+// counts of bucket b in the CTAs before c).
+__global__ void __launch_bounds__(kHpBT) hp_offsets_kernel(const unsigned* hist, const unsigned* totals, int nb,
+                                                           int grid, unsigned* off) {
+  __shared__ unsigned s_scan[kHpBT / 32 + 1];
+  __shared__ unsigned s_base;
+  const int b = blockIdx.x;
+  {
+    unsigned v = 0;
+    for (int i = threadIdx.x; i < b; i += kHpBT) v += totals[i];
+    v = warp_sum(v);
+    if (lane_id() == 0) s_scan[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned t = 0;
+      for (int w = 0; w < kHpBT / 32; ++w) t += s_scan[w];
+      s_base = t;
+    }
+    __syncthreads();
+  }
+  unsigned run = s_base;
+  for (int c0 = 0; c0 < grid; c0 += kHpBT) {
+    const int c = c0 + (int)threadIdx.x;
+    const unsigned v = c < grid ? hist[(size_t)c * nb + b] : 0u;
+    unsigned all;
+    const unsigned ex = BlockScan<kHpBT>(v, s_scan, all);
+    if (c < grid) off[(size_t)c * nb + b] = run + ex;
+    run += all;
+    __syncthreads();  // s_scan reuse
+  }
+}
+
+__global__ void __launch_bounds__(kHpBT) hp_scatter_kernel(const int32_t* __restrict__ keys,
+                                                           const int32_t* __restrict__ pays, int64_t n, int bshift,
+                                                           int nb, const unsigned* off,
+                                                           int32_t* __restrict__ ok, int32_t* __restrict__ op) {
+  constexpr int W = kHpBT / 32;
+  __shared__ unsigned s_cur[256];
+  __shared__ long long s_dst[256];   // global position of the tile's bucket run minus its tile offset
+  __shared__ unsigned s_wc[W][256];  // per-warp bucket counters, then per-warp slots in the tile
+  __shared__ unsigned s_scan[kHpBT / 32 + 1];
+  __shared__ int32_t s_k[kHpTile], s_p[kHpTile];
+  const int warp = threadIdx.x >> 5;
+  for (int b = threadIdx.x; b < nb; b += kHpBT) s_cur[b] = off[(size_t)blockIdx.x * nb + b];
+  int t0, t1;
+  hp_chunk((n + kHpTile - 1) / kHpTile, t0, t1);
+  for (int t = t0; t < t1; ++t) {
+    for (int i = threadIdx.x; i < W * 256; i += kHpBT) (&s_wc[0][0])[i] = 0;
+    __syncthreads();
+    const int64_t base = (int64_t)t * kHpTile;
+    const int valid = (int)min((int64_t)kHpTile, n - base);
+    int4 kv[kHpIPT / 4], pv[kHpIPT / 4];
+    uint32_t rk[kHpIPT];
+#pragma unroll
+    for (int v = 0; v < kHpIPT / 4; ++v) {
+      const int64_t i = base + 4 * ((int64_t)v * kHpBT + threadIdx.x);
+      if (i < n) {  // n % 4 == 0: whole vectors
+        kv[v] = ld_stream4(keys + i);
+        pv[v] = ld_stream4(pays + i);
+      }
+    }
+    // rank inside (tile, warp, bucket) with warp-private counters (the order
+    // inside a bucket is free: the checksum does not depend on it)
+#pragma unroll
+    for (int v = 0; v < kHpIPT / 4; ++v) {
+      const int64_t i = base + 4 * ((int64_t)v * kHpBT + threadIdx.x);
+      const int32_t kk[4] = {kv[v].x, kv[v].y, kv[v].z, kv[v].w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t b = hp_bucket(kk[e], bshift);
+        rk[4 * v + e] = i < n ? (b << 16) | atomicAdd(&s_wc[warp][b], 1u) : 0xFFFFFFFFu;
+      }
+    }
+    __syncthreads();
+    {  // tile offsets of the buckets (block scan), per-warp slots, global runs
+      const int b = threadIdx.x;  // kHpBT == 256 >= nb
+      unsigned c = 0;
+      if (b < nb)
+#pragma unroll
+        for (int w = 0; w < W; ++w) c += s_wc[w][b];
+      unsigned all;
+      const unsigned ts = BlockScan<kHpBT>(c, s_scan, all);
+      if (b < nb) {
+        unsigned run = ts;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          const unsigned x = s_wc[w][b];
+          s_wc[w][b] = run;
+          run += x;
+        }
+        s_dst[b] = (long long)s_cur[b] - (long long)ts;
+        s_cur[b] += c;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int v = 0; v < kHpIPT / 4; ++v) {  // into bucket order in shared memory
+      const int32_t kk[4] = {kv[v].x, kv[v].y, kv[v].z, kv[v].w};
+      const int32_t pp[4] = {pv[v].x, pv[v].y, pv[v].z, pv[v].w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t r = rk[4 * v + e];
+        if (r != 0xFFFFFFFFu) {
+          const unsigned slot = s_wc[warp][r >> 16] + (r & 0xFFFFu);
+          s_k[slot] = kk[e];
+          s_p[slot] = pp[e];
+        }
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < valid; i += kHpBT) {  // bucket runs: coalesced stores
+      const int32_t k = s_k[i];
+      const long long dst = s_dst[hp_bucket(k, bshift)] + i;
+      ok[dst] = k;
+      op[dst] = s_p[i];
+    }
+    __syncthreads();  // s_wc / s_k / s_p reuse
+  }
+}
+
+// CRYS_JOIN_PART_SLICE_KB: table bytes per partition of the partitioned probe.
+size_t join_part_slice() {
+  static const size_t v = [] {
+    const char* e = getenv("CRYS_JOIN_PART_SLICE_KB");
+    return (size_t)(e ? atoll(e) : 16384) << 10;
+  }();
+  return v;
+}
+
+// CRYS_JOIN_PART_MB: tables of at least this many MB take the partitioned
+// probe (0 = never).
+int64_t join_part_min_bytes() {
+  static const int64_t v = [] {
+    const char* e = getenv("CRYS_JOIN_PART_MB");
+    return (int64_t)(e ? atoll(e) : 128) << 20;
+  }();
+  return v;
+}
+
 int join_l2_ahead(bool table_on_chip) {
   static const int v = [] {
     const char* e = getenv("CRYS_JOIN_L2");
@@ -1264,9 +1451,34 @@ int64_t join_probe_sum(crys_ctx* ctx, const int32_t* d_keys, const int32_t* d_pa
       fn<<<grid, (kJW + 1) * 32, ring4 + tbytes, st>>>(d_keys, d_payloads, n, ht->slots.as<int2>(), mask,
                                                        ht->shift, out, join_l2_ahead(true));
     } else {
+      const int64_t pmin = join_part_min_bytes();
+      const int logcap = 32 - ht->shift;
+      int k = 0;  // buckets of <= join_part_slice() table slices
+      while (k < 8 && k < logcap && (tbytes >> k) > join_part_slice()) ++k;
+      const int32_t* pk = d_keys;
+      const int32_t* pp = d_payloads;
+      if (pmin > 0 && (int64_t)tbytes >= pmin && k > 0 && n >= kHpTile && n < (int64_t(1) << 31)) {
+        const int nb = 1 << k, bshift = 32 - k;
+        const int64_t hp_tiles = (n + kHpTile - 1) / kHpTile;
+        const int g = (int)std::min<int64_t>(hp_tiles, (int64_t)ctx->num_sms *
+                                                         occupancy((const void*)hp_scatter_kernel, kHpBT, 0));
+        ctx->part.reserve(2 * sizeof(int32_t) * (size_t)n + (2 * (size_t)g * nb + 256) * sizeof(unsigned) + 64);
+        int32_t* ok = ctx->part.as<int32_t>();
+        int32_t* op = ok + n;
+        unsigned* totals = reinterpret_cast<unsigned*>(op + n);
+        unsigned* hist = totals + 256;
+        unsigned* offs = hist + (size_t)g * nb;
+        CUDA_TRY(cudaMemsetAsync(totals, 0, 256 * sizeof(unsigned), st));
+        hp_hist_kernel<<<g, kHpBT, 0, st>>>(d_keys, n, bshift, nb, hist, totals);
+        hp_offsets_kernel<<<nb, kHpBT, 0, st>>>(hist, totals, nb, g, offs);
+        hp_scatter_kernel<<<g, kHpBT, 0, st>>>(d_keys, d_payloads, n, bshift, nb, offs, ok, op);
+        count_launch(ctx, 3);
+        pk = ok;
+        pp = op;
+      }
       auto fn = join_ring_kernel<6, false>;
       ensure_dyn_smem((const void*)fn, ring6);
-      fn<<<grid, (kJW + 1) * 32, ring6, st>>>(d_keys, d_payloads, n, ht->slots.as<int2>(), mask, ht->shift,
+      fn<<<grid, (kJW + 1) * 32, ring6, st>>>(pk, pp, n, ht->slots.as<int2>(), mask, ht->shift,
                                               out, join_l2_ahead(false));
     }
     timing_kernel_end(ctx);
