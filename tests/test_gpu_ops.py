@@ -224,6 +224,27 @@ def test_hash_build_errors(env):
         tq.HashTable.build(s, s, 4)
 
 
+def test_join_partitioned_path_vs_numpy(env):
+    """A 128 MB table takes the radix-partitioned probe (hash-bucket scatter,
+    then the ring probe per L2-resident slice): probes with misses, negative
+    keys and a size that is not a multiple of the tile, against numpy."""
+    torch, tq, orc = env
+    cap = 1 << 24  # 16 M slots x 8 B = 128 MB
+    bn = 6_000_000
+    rng = np.random.default_rng(21)
+    bkh = np.arange(1, bn + 1, dtype=np.int32)
+    bph = rng.integers(0, 1000, bn).astype(np.int32)
+    P = 3 * (1 << 20) + 4 * 1001
+    pkh = rng.integers(-1000, bn + 200_000, P).astype(np.int32)
+    pph = rng.integers(0, 1000, P).astype(np.int32)
+    ht = tq.HashTable.build(_cuda(torch, bkh), _cuda(torch, bph), cap)
+    got = tq.join_probe_tile(_cuda(torch, pkh), _cuda(torch, pph), ht)
+    ht.free()
+    hit = (pkh >= 1) & (pkh <= bn)
+    exp = int(bph[pkh[hit] - 1].astype(np.int64).sum() + pph[hit].astype(np.int64).sum())
+    assert got == exp
+
+
 @pytest.mark.slow
 def test_join_golden_p2e28(env):
     torch, tq, orc = env
