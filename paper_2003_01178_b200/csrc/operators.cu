@@ -1102,7 +1102,7 @@ __global__ void __launch_bounds__(kHpBT) hp_offsets_kernel(const unsigned* hist,
   }
 }
 
-__global__ void __launch_bounds__(kHpBT) hp_scatter_kernel(const int32_t* __restrict__ keys,
+__global__ void __launch_bounds__(kHpBT, 4) hp_scatter_kernel(const int32_t* __restrict__ keys,
                                                            const int32_t* __restrict__ pays, int64_t n, int bshift,
                                                            int nb, const unsigned* off,
                                                            int32_t* __restrict__ ok, int32_t* __restrict__ op) {
