@@ -34,6 +34,9 @@
 namespace crys {
 namespace {
 
+#ifndef CRYS_OS_MATCH_EVERY
+#define CRYS_OS_MATCH_EVERY 5  // mixed ranking: every n-th item on match.any, the rest on ballots (sweep: profiles/r01_sort_tile_size.txt)
+#endif
 #ifndef CRYS_OS_IPT
 #define CRYS_OS_IPT 16
 #endif
@@ -301,8 +304,8 @@ __global__ void __launch_bounds__(kOsBT, kOsMinBlocks) onesweep_kernel(OsPass a)
     const uint32_t d = sl < valid ? digit_of(key[k], a.start, mask) : 256u;
     if constexpr (RANK == 0) {
       rd[k] = __match_any_sync(0xffffffffu, d);
-    } else if (RANK == 2 && (k & 3) == 0) {
-      // mixed: every 4th item on the ADU (match.any), the rest on the vote
+    } else if (RANK == 2 && (k % CRYS_OS_MATCH_EVERY) == 0) {
+      // mixed: every CRYS_OS_MATCH_EVERY-th item on the ADU (match.any), the rest on the vote
       // path, so the two pipes work in parallel
       rd[k] = __match_any_sync(0xffffffffu, d);
     } else {
