@@ -37,6 +37,9 @@ namespace {
 #ifndef CRYS_OS_MATCH_EVERY
 #define CRYS_OS_MATCH_EVERY 5  // mixed ranking: every n-th item on match.any, the rest on ballots (sweep: profiles/r01_sort_tile_size.txt)
 #endif
+#ifndef CRYS_OS_LB
+#define CRYS_OS_LB 4  // look-back window: predecessors read per round trip
+#endif
 #ifndef CRYS_OS_IPT
 #define CRYS_OS_IPT 16
 #endif
@@ -384,7 +387,7 @@ __global__ void __launch_bounds__(kOsBT, kOsMinBlocks) onesweep_kernel(OsPass a)
       // closest inclusive prefix ends the walk; a not-yet-published word is
       // re-polled on its own (the one-at-a-time walk spent 22 % of the
       // kernel's stall samples in this loop)
-      constexpr int kLB = 4;  // measured: 1 -> 7.45, 2 -> 7.03, 4 -> 6.96, 8 -> 7.15, 16 -> 7.52 ms (LSB 2^28)
+      constexpr int kLB = CRYS_OS_LB;  // measured: 1 -> 7.45, 2 -> 7.03, 4 -> 6.96, 8 -> 7.15, 16 -> 7.52 ms (LSB 2^28)
       for (int t0 = tile - 1; t0 >= first; t0 -= kLB) {
         uint32_t w[kLB];
 #pragma unroll
