@@ -513,29 +513,12 @@ __global__ void __launch_bounds__(kCrysPB) select_crystal_kernel(
 // chunk.  IPTM >= ipt is the unrolled item bound (items stay in registers).
 // KNOWN: the chunk offsets come from a count pass + scan (offsets[c]) instead
 // of the look-back (the reduce-then-scan form, as for the input-order select).
-template <int IPTM, int G, bool KNOWN = false>
-__global__ void __launch_bounds__(kCrysPB) select_crystal_reg_kernel(
-    const int32_t* __restrict__ in, int64_t n, int32_t lo, int32_t hi, int bt, int ipt, int chunk,
-    int32_t* __restrict__ out, unsigned long long* status, long long* total_out,
-    const long long* local = nullptr, const long long* bases = nullptr) {
-  // ceil(2^32 / bt) (bt = 1 would need 2^32: handled without the multiply)
-  const unsigned bt_magic = bt > 1 ? (unsigned)((0x100000000ull + (unsigned)bt - 1) / (unsigned)bt) : 0u;
-  static_assert(G >= 1 && G <= 4, "four 16-bit count fields per scan word");
-  extern __shared__ int32_t s_dyn[];
-  int32_t* s_out = s_dyn;  // [chunk]
-  __shared__ unsigned long long s_scan[kCrysPB / 32 + 1];
-  __shared__ long long s_red[kCrysPB / 32 + kCrysPB / 64 + 1];
-  const long long c = blockIdx.x;
-  const int64_t base = c * (int64_t)chunk;
-  const int valid = (int)min((int64_t)chunk, n - base);
-  const long long nchunks = (n + chunk - 1) / chunk;
-  if constexpr (KNOWN) {
-    const long long o = sel_offset(local, bases, c, nchunks);
-    if (sel_offset(local, bases, c + 1, nchunks) == o) {  // no match in this chunk (uniform exit)
-      if (threadIdx.x == 0 && base + chunk >= n) *total_out = o;
-      return;
-    }
-  }
+// One chunk of whole logical tiles compacted into s_out in Crystal order
+// (thread-major per logical tile, tiles in order); returns the match count.
+template <int IPTM, int G>
+__device__ __forceinline__ int crystal_compact(const int32_t* __restrict__ in, int64_t base, int valid, int32_t lo,
+                                               int32_t hi, int bt, int ipt, unsigned bt_magic, int32_t* s_out,
+                                               unsigned long long* s_scan) {
   const int S = bt * ipt;
   const int pairs = ((valid + S - 1) / S) * bt;
   const int32_t* src = in + base;
@@ -576,6 +559,33 @@ __global__ void __launch_bounds__(kCrysPB) select_crystal_reg_kernel(
     }
     run = before;
   }
+  return run;
+}
+
+template <int IPTM, int G, bool KNOWN = false>
+__global__ void __launch_bounds__(kCrysPB) select_crystal_reg_kernel(
+    const int32_t* __restrict__ in, int64_t n, int32_t lo, int32_t hi, int bt, int ipt, int chunk,
+    int32_t* __restrict__ out, unsigned long long* status, long long* total_out,
+    const long long* local = nullptr, const long long* bases = nullptr) {
+  // ceil(2^32 / bt) (bt = 1 would need 2^32: handled without the multiply)
+  const unsigned bt_magic = bt > 1 ? (unsigned)((0x100000000ull + (unsigned)bt - 1) / (unsigned)bt) : 0u;
+  static_assert(G >= 1 && G <= 4, "four 16-bit count fields per scan word");
+  extern __shared__ int32_t s_dyn[];
+  int32_t* s_out = s_dyn;  // [chunk]
+  __shared__ unsigned long long s_scan[kCrysPB / 32 + 1];
+  __shared__ long long s_red[kCrysPB / 32 + kCrysPB / 64 + 1];
+  const long long c = blockIdx.x;
+  const int64_t base = c * (int64_t)chunk;
+  const int valid = (int)min((int64_t)chunk, n - base);
+  const long long nchunks = (n + chunk - 1) / chunk;
+  if constexpr (KNOWN) {
+    const long long o = sel_offset(local, bases, c, nchunks);
+    if (sel_offset(local, bases, c + 1, nchunks) == o) {  // no match in this chunk (uniform exit)
+      if (threadIdx.x == 0 && base + chunk >= n) *total_out = o;
+      return;
+    }
+  }
+  const int run = crystal_compact<IPTM, G>(in, base, valid, lo, hi, bt, ipt, bt_magic, s_out, s_scan);
   __syncthreads();  // s_out complete (the look-back's barriers would also order it)
   long long off;
   if constexpr (KNOWN) {
