@@ -110,6 +110,10 @@ class ClockSampler:
             h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
             mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
             self.nvml = (pynvml, h, mx)
+            # the suite loop holds the GIL between its C calls: a short switch
+            # interval lets the 5 ms poller in during the timed region
+            self._switch = sys.getswitchinterval()
+            sys.setswitchinterval(0.0005)
             self.t = threading.Thread(target=self._poll_nvml, daemon=True)
             self.t.start()
             return self
@@ -127,13 +131,9 @@ class ClockSampler:
         return self
 
     def _poll_nvml(self):
-        pynvml, h, mx = self.nvml
         while not self._stop.is_set():
             try:
-                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-                r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                active = {nm for nm, attr in self.REASONS if r & getattr(pynvml, attr, 0)}
-                self.samples.append((float(sm), float(mx), active))
+                self._sample_nvml()
             except Exception:
                 pass
             self._stop.wait(self.period)
@@ -142,10 +142,22 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def _sample_nvml(self):
+        pynvml, h, mx = self.nvml
+        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+        active = {nm for nm, attr in self.REASONS if r & getattr(pynvml, attr, 0)}
+        self.samples.append((float(sm), float(mx), active))
+
     def __exit__(self, *a):
         self._stop.set()
         if self.nvml:
             self.t.join(timeout=1)
+            sys.setswitchinterval(self._switch)
+            try:
+                self._sample_nvml()  # the clocks right at the end of the timed region
+            except Exception:
+                pass
         if self.proc:
             self.proc.terminate()
             try:
