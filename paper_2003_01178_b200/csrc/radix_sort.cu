@@ -419,11 +419,21 @@ __global__ void __launch_bounds__(kOsBT, kOsMinBlocks) onesweep_kernel(OsPass a)
     s_dst[d] = (long long)sbeg + (long long)gb + (long long)excl - (long long)s_start[d];
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < valid; i += kOsBT) {
-    const int32_t kk = s_k[i];
-    const long long dst = s_dst[digit_of(kk, a.start, mask)] + i;
-    a.kout[dst] = kk;
-    a.pout[dst] = s_p[i];
+  if (a.n < (int64_t(1) << 31)) {  // 32-bit destinations (fewer instructions per item)
+#pragma unroll 4
+    for (int i = threadIdx.x; i < valid; i += kOsBT) {
+      const int32_t kk = s_k[i];
+      const int dst = (int)s_dst[digit_of(kk, a.start, mask)] + i;
+      a.kout[dst] = kk;
+      a.pout[dst] = s_p[i];
+    }
+  } else {
+    for (int i = threadIdx.x; i < valid; i += kOsBT) {
+      const int32_t kk = s_k[i];
+      const long long dst = s_dst[digit_of(kk, a.start, mask)] + i;
+      a.kout[dst] = kk;
+      a.pout[dst] = s_p[i];
+    }
   }
 }
 
