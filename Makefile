@@ -27,7 +27,7 @@ $(BUILD)/%.o: $(CSRC)/%.cpp $(HDRS)
 	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@ 2> $(BUILD)/$*.ptxas.txt || (cat $(BUILD)/$*.ptxas.txt; false)
 
 $(LIB): $(OBJS)
-	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS)
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS) -ldl
 
 oracle:
 	$(MAKE) -C oracle

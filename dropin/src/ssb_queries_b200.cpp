@@ -1,9 +1,11 @@
 // ssb_queries_b200.cpp -- B200 drop-in for P:src/ssb_queries.cpp.
 //
-// Defines everything P:include/tq/ssb_queries.hpp declares.  run_query hands
-// the host database's columns to crys_run_query_host (the plan's referenced
-// columns are copied to HBM inside the call, then dimension builds, ONE
-// fused lineorder pass and the group compaction run on the GPU); the
+// Defines everything P:include/tq/ssb_queries.hpp declares.  run_query maps
+// `workers` to a device group (b200::group_context: lineorder row-range
+// shards, one per GPU, one NCCL reduce per query), uploads the host database
+// ONCE into that group's HBM (b200::cached_database, keyed by identity +
+// content fingerprint) and runs crys_run_query: dimension builds, ONE fused
+// lineorder pass per shard and the group compaction on the GPUs; the
 // AggregateTable / sort_result / diff_results helpers are host utilities with
 // the reference's semantics (ssb_queries.cpp:15-88).
 #include <algorithm>
@@ -108,17 +110,25 @@ QueryResult run_query(const SsbDatabase& db, QueryId id, const TileConfig& confi
   }
   TQ_CHECK(!cols.empty(), "run_query: empty database");
 
+  // `workers` -> a device group of lineorder shards (one NCCL reduce per
+  // query); the host database is uploaded once and cached by identity
+  crys_ctx* group = b200::group_context(workers);
+  crys_db* hbm = b200::cached_database(group, &db, cols);
+
   int64_t cells = 0;
   int32_t ngroup = 0, njoins = 0;
   b200::check(crys_query_shape(static_cast<int>(id), &cells, &ngroup, &njoins));
   const int64_t max_rows = std::max<int64_t>(cells, 1);
-  std::vector<int32_t> groups(static_cast<size_t>(3 * max_rows));
-  std::vector<int64_t> sums(static_cast<size_t>(max_rows));
+  thread_local std::vector<int32_t> groups;
+  thread_local std::vector<int64_t> sums;
+  if ((int64_t)sums.size() < max_rows) {
+    groups.resize(static_cast<size_t>(3 * max_rows));
+    sums.resize(static_cast<size_t>(max_rows));
+  }
   int64_t survivors[4] = {0, 0, 0, 0};
   int64_t nrows = 0;
-  b200::check(crys_run_query_host(b200::context(), cols.data(), static_cast<int>(cols.size()),
-                                  static_cast<int>(id), config.block_threads, config.items_per_thread,
-                                  groups.data(), sums.data(), max_rows, &nrows, survivors));
+  b200::check(crys_run_query(group, hbm, static_cast<int>(id), config.block_threads, config.items_per_thread,
+                             groups.data(), sums.data(), max_rows, &nrows, survivors));
 
   QueryResult result;
   for (const GroupPart& g : plan.group) result.group_labels.push_back(g.label);

@@ -34,7 +34,8 @@ typedef enum {
   CRYS_EBUILD = 3,    /* tq::BuildError    (common.hpp:27)  */
   CRYS_EIO = 4,       /* tq::IoError       (common.hpp:32)  */
   CRYS_ECUDA = 5,     /* CUDA runtime failure (no reference analogue) */
-  CRYS_ENOTBUILT = 6  /* kernel shape not compiled for sm_100a */
+  CRYS_ENOTBUILT = 6, /* kernel shape not compiled for sm_100a */
+  CRYS_ENCCL = 7      /* NCCL missing or failed (device groups, SURVEY 8(b) C ABI) */
 } crys_status;
 
 /* PredOp (tile.hpp:92): comparison against lo (or inclusive [lo,hi]). */
@@ -64,11 +65,38 @@ typedef struct crys_ht crys_ht;
 const char* crys_last_error(void);
 /* Library / build identification ("sm_100a ..."). */
 const char* crys_version(void);
+/* Visible CUDA devices (0 when there is no usable driver/device). */
+int crys_device_count(void);
 
 /* Bind to CUDA device `device`, create a stream and scratch.  Replaces the
  * per-call std::thread pool of parallel_for_blocks (kernel.cpp:60-103). */
 crys_status crys_init(int device, crys_ctx** out);
 void crys_destroy(crys_ctx* ctx);
+/* A DEVICE GROUP: one host thread drives `nshards` lineorder row-range shards
+ * placed on devices[0..nshards) (the reference's `workers`
+ * fan-out, kernel.cpp:60-103, ssb_queries.cpp:265-266).  Every distinct device
+ * gets a member context; the members share one NCCL communicator
+ * (ncclCommInitAll, libnccl.so.2 loaded on first use) and each query ends in
+ * ONE ncclReduce(int64, sum) of the members' packed partial aggregates to
+ * devices[0], grouped with ncclGroupStart/End.  Several shards on one device
+ * (devices[] repeating an ordinal: the emulation of an N-GPU box on fewer GPUs)
+ * accumulate into that device's aggregate before the reduce.  Dimension tables
+ * are replicated and built once per device.  ENCCL when NCCL cannot be loaded
+ * and the group spans more than one device (a one-device group does not need
+ * it; CRYS_GROUP_NCCL=1 forces the NCCL path anyway, =0 disables it).
+ * Databases created on a group (crys_db_generate / crys_db_create +
+ * crys_db_upload_host / crys_db_upload_column) are sharded; crys_run_query
+ * on them runs the whole group.  Every other entry point treats a group
+ * context as a context on devices[0]. */
+crys_status crys_init_group(int nshards, const int* devices, crys_ctx** out);
+/* Shards / distinct devices of a context (1 / 1 for crys_init). */
+int crys_group_shards(const crys_ctx* ctx);
+int crys_group_devices(const crys_ctx* ctx);
+/* 1 when the group reduces through NCCL. */
+int crys_group_uses_nccl(const crys_ctx* ctx);
+/* "libnccl <version code>" once libnccl.so.2 loads (dlopen), else why not. */
+const char* crys_nccl_version(void);
+
 /* Run subsequent work on `cuda_stream` (a cudaStream_t; NULL = the ctx's own
  * stream).  The legacy default stream (handle 0, e.g. torch's default stream)
  * is CRYS_STREAM_LEGACY -- passing 0 would select the ctx's own non-blocking
@@ -170,19 +198,57 @@ crys_status crys_run_query_host(crys_ctx* ctx, const crys_host_column* cols, int
                                 int bt, int ipt, int32_t* h_groups, int64_t* h_sums,
                                 int64_t max_rows, int64_t* nrows, int64_t* h_survivors);
 
-/* Multi-GPU building blocks (lineorder row-range shards):
- * the shard's dense partial aggregate -> d_agg = int64[2*cells] laid out as
- * [sums | counts] (the payload of the one NCCL reduce), survivors accumulated
- * into d_survivors (int64[4]).  Asynchronous on the ctx stream. */
+/* Multi-GPU building blocks (lineorder row-range shards), dense
+ * form: the shard's partial aggregate ADDS into d_agg = int64[2*cells] laid
+ * out as [sums | counts], and its survivors and error words add into d_hdr =
+ * int64[CRYS_PARTIAL_HEADER] (layout below) -- both caller-zeroed, so several
+ * shards can accumulate into one buffer.  Asynchronous on the ctx stream. */
 crys_status crys_query_partial(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt,
-                               int64_t* d_agg, int64_t* d_survivors);
-/* Compact a (reduced) dense aggregate on the device into result rows. */
-crys_status crys_query_finalize(crys_ctx* ctx, int qid, const int64_t* d_agg,
+                               int64_t* d_agg, int64_t* d_hdr);
+/* The packed partial (the payload of the ONE collective per query): the
+ * dense sub-box of the group-by domain the query can occupy, computed on the
+ * device from the dimension builds (identical on every shard because the
+ * dimensions are replicated).  Layout, int64:
+ *   [0..3]    survivors per join (QueryStats.survivors)
+ *   [4]       shards whose rows hit a group value outside its domain
+ *             (ContractError, ssb_queries.cpp:32-33)
+ *   [8+4j+c-1] shards whose build of join j failed with code c: 1 sentinel
+ *             key, 2 duplicate key, 3 capacity (BuildError,
+ *             hash_table.cpp:51-93), 4 key outside the column statistics
+ *   [32 .. 32+cells)          sums of the box cells
+ *   [32+cells .. 32+2*cells)  occupancy counts
+ * Element-wise SUM over shards is the merge (AggregateTable::merge,
+ * ssb_queries.cpp:38-47). */
+#define CRYS_PARTIAL_HEADER 32
+typedef struct {
+  int32_t nparts;  /* group parts of the plan (0..3) */
+  int32_t lo[3];   /* first group VALUE of the box per part */
+  int32_t card[3]; /* extent per part */
+  int32_t pad;
+  int64_t cells;   /* product of card (1 for flight 1; 0: nothing can match) */
+} crys_group_box;
+/* Enqueue the shard's query and pack its partial into d_buf (capacity
+ * `cap` int64); *len = CRYS_PARTIAL_HEADER + 2*box->cells.  Returns once the
+ * dimension builds have fixed the box (the fused pass is still running on
+ * the ctx stream), so the caller can size the collective right away. */
+crys_status crys_query_partial_box(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt,
+                                   int64_t* d_buf, int64_t cap, int64_t* len, crys_group_box* box);
+/* Rows of a (reduced) packed partial; raises the errors its header carries. */
+crys_status crys_query_finalize_box(crys_ctx* ctx, int qid, const crys_group_box* box,
+                                    const int64_t* d_buf, int32_t* h_groups, int64_t* h_sums,
+                                    int64_t max_rows, int64_t* nrows, int64_t* h_survivors);
+
+/* Compact a (reduced) dense aggregate [sums | counts] on the device into
+ * result rows; d_hdr (nullable) is the matching reduced header: its survivors
+ * go to h_survivors[4] (nullable) and its error words raise EBUILD /
+ * ECONTRACT exactly as crys_run_query does. */
+crys_status crys_query_finalize(crys_ctx* ctx, int qid, const int64_t* d_agg, const int64_t* d_hdr,
                                 int32_t* h_groups, int64_t* h_sums, int64_t max_rows,
-                                int64_t* nrows);
+                                int64_t* nrows, int64_t* h_survivors);
 /* Same compaction on the host (pure CPU; no device needed). */
-crys_status crys_query_finalize_host(int qid, const int64_t* h_agg, int32_t* h_groups,
-                                     int64_t* h_sums, int64_t max_rows, int64_t* nrows);
+crys_status crys_query_finalize_host(int qid, const int64_t* h_agg, const int64_t* h_hdr,
+                                     int32_t* h_groups, int64_t* h_sums, int64_t max_rows,
+                                     int64_t* nrows, int64_t* h_survivors);
 
 /* ------------------------------------------------------------ operators */
 

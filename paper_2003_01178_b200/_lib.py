@@ -12,7 +12,8 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libcrystal_b200.so")
 
-CRYS_OK, CRYS_ECONFIG, CRYS_ECONTRACT, CRYS_EBUILD, CRYS_EIO, CRYS_ECUDA, CRYS_ENOTBUILT = range(7)
+CRYS_OK, CRYS_ECONFIG, CRYS_ECONTRACT, CRYS_EBUILD, CRYS_EIO, CRYS_ECUDA, CRYS_ENOTBUILT, CRYS_ENCCL = range(8)
+CRYS_PARTIAL_HEADER = 32
 CRYS_LT, CRYS_LE, CRYS_GT, CRYS_GE, CRYS_EQ, CRYS_BETWEEN = range(6)
 CRYS_ORDER_INPUT, CRYS_ORDER_CRYSTAL = 0, 1
 CRYS_SORT_LSB, CRYS_SORT_MSB = 0, 1
@@ -21,6 +22,11 @@ CRYS_STREAM_LEGACY = 0x1  # cudaStreamLegacy
 
 class crys_pred(C.Structure):
     _fields_ = [("op", C.c_int32), ("lo", C.c_int32), ("hi", C.c_int32)]
+
+
+class crys_group_box(C.Structure):
+    _fields_ = [("nparts", C.c_int32), ("lo", C.c_int32 * 3), ("card", C.c_int32 * 3), ("pad", C.c_int32),
+                ("cells", C.c_int64)]
 
 
 class crys_host_column(C.Structure):
@@ -36,6 +42,12 @@ SIGNATURES = [
     ("crys_last_error", C.c_char_p, []),
     ("crys_version", C.c_char_p, []),
     ("crys_init", C.c_int, [C.c_int, C.POINTER(_P)]),
+    ("crys_init_group", C.c_int, [C.c_int, _I32P, C.POINTER(_P)]),
+    ("crys_group_shards", C.c_int, [_P]),
+    ("crys_group_devices", C.c_int, [_P]),
+    ("crys_group_uses_nccl", C.c_int, [_P]),
+    ("crys_nccl_version", C.c_char_p, []),
+    ("crys_device_count", C.c_int, []),
     ("crys_destroy", None, [_P]),
     ("crys_set_stream", C.c_int, [_P, _P]),
     ("crys_synchronize", C.c_int, [_P]),
@@ -62,8 +74,12 @@ SIGNATURES = [
     ("crys_run_query_host", C.c_int, [_P, C.POINTER(crys_host_column), C.c_int, C.c_int, C.c_int,
                                       C.c_int, _P, _P, C.c_int64, _I64P, _P]),
     ("crys_query_partial", C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, _P, _P]),
-    ("crys_query_finalize", C.c_int, [_P, C.c_int, _P, _P, _P, C.c_int64, _I64P]),
-    ("crys_query_finalize_host", C.c_int, [C.c_int, _P, _P, _P, C.c_int64, _I64P]),
+    ("crys_query_partial_box", C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, _P, C.c_int64, _I64P,
+                                         C.POINTER(crys_group_box)]),
+    ("crys_query_finalize_box", C.c_int, [_P, C.c_int, C.POINTER(crys_group_box), _P, _P, _P, C.c_int64,
+                                          _I64P, _P]),
+    ("crys_query_finalize", C.c_int, [_P, C.c_int, _P, _P, _P, _P, C.c_int64, _I64P, _P]),
+    ("crys_query_finalize_host", C.c_int, [C.c_int, _P, _P, _P, _P, C.c_int64, _I64P, _P]),
     ("crys_select_i32", C.c_int, [_P, _P, C.c_int64, crys_pred, _P, _I64P, C.c_int, C.c_int, C.c_int]),
     ("crys_project_f32", C.c_int, [_P, _P, _P, C.c_int64, C.c_float, C.c_float, _P, C.c_int,
                                    C.c_int, C.c_int]),
@@ -81,7 +97,28 @@ SIGNATURES = [
 ]
 
 
+def _torch_nccl():
+    """The libnccl.so.2 of the nvidia-nccl wheel torch links against (found
+    without importing torch).  The library dlopens NCCL lazily; pointing it
+    here keeps ONE NCCL per process whichever of torch / this library loads
+    it first (a second, older libnccl.so.2 would break torch's import)."""
+    import importlib.util
+    try:
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return None
+    for d in (spec.submodule_search_locations or []) if spec else []:
+        p = os.path.join(d, "lib", "libnccl.so.2")
+        if os.path.exists(p):
+            return p
+    return None
+
+
 def _load() -> C.CDLL:
+    if "CRYS_NCCL_LIBRARY" not in os.environ:
+        p = _torch_nccl()
+        if p:
+            os.environ["CRYS_NCCL_LIBRARY"] = p
     if not os.path.exists(LIB_PATH):
         raise ImportError(
             f"{LIB_PATH} is missing: the B200 kernels are not built "

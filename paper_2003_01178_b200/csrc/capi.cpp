@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -56,9 +57,15 @@ crys_ctx::~crys_ctx() {
   if (own_stream) cudaStreamDestroy(own_stream);
 }
 
+crys_db::crys_db() {
+  static std::atomic<uint64_t> next{1};
+  uid = next.fetch_add(1);
+}
+
 crys_db::~crys_db() {
   for (auto& kv : cols)
     if (kv.second.ready) cudaEventDestroy(kv.second.ready);
+  for (crys_db* s : shards) delete s;
 }
 
 const int32_t* crys_db::col(const std::string& table, const std::string& column, int64_t* rows) const {
@@ -109,10 +116,12 @@ namespace crys {
 
 void ensure_dyn_smem(const void* fn, size_t bytes) {
   static std::mutex mu;
-  static std::map<const void*, size_t> set_to;
+  static std::map<std::pair<int, const void*>, size_t> set_to;
   if (bytes <= 48 * 1024) return;
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lk(mu);
-  size_t& cur = set_to[fn];
+  size_t& cur = set_to[{dev, fn}];
   if (bytes <= cur) return;
   CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   cur = bytes;
@@ -163,38 +172,91 @@ void emit_rows(int qid, const std::vector<int64_t>& cell, const std::vector<int6
 
 }  // namespace crys
 
+namespace crys {
+crys_ctx* new_context(int device) {
+  int n = 0;
+  CUDA_TRY(cudaGetDeviceCount(&n));
+  CRYS_CHECK(device >= 0 && device < n, CRYS_ECONFIG, "no such CUDA device");
+  CUDA_TRY(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  CRYS_CHECK(prop.major == 10, CRYS_ENOTBUILT,
+             std::string("library is compiled for sm_100a only; device is ") + prop.name);
+  auto* ctx = new crys_ctx();
+  ctx->device = device;
+  ctx->num_sms = prop.multiProcessorCount;
+  cudaError_t e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete ctx;
+    crys::fail(CRYS_ECUDA, cudaGetErrorString(e));
+  }
+  ctx->stream = ctx->own_stream;
+  for (auto& ev : ctx->ev) {
+    e = cudaEventCreate(&ev);
+    if (e != cudaSuccess) {
+      delete ctx;
+      crys::fail(CRYS_ECUDA, cudaGetErrorString(e));
+    }
+  }
+  return ctx;
+}
+}  // namespace crys
+
+namespace crys {
+// Header words of a reduced partial -> the reference's exceptions (the same
+// messages as the device finalize, ssb_query.cu finalize_host_part).
+void raise_partial_errors(int qid, const int64_t* h_hdr) {
+  if (!h_hdr) return;
+  for (int j = 0; j < 4; ++j)
+    for (int c = 1; c <= 4; ++c)
+      if (h_hdr[8 + 4 * j + (c - 1)]) {
+        static const char* kMsg[5] = {"", "HashTable: key equals empty sentinel", "HashTable: duplicate key",
+                                      "HashTable: capacity overflow", "dimension key outside its column statistics"};
+        fail(c == 4 ? CRYS_ECONTRACT : CRYS_EBUILD,
+             std::string(kMsg[c]) + " (join " + std::to_string(j) + " of " + plan_for(qid).name + ")");
+      }
+  if (h_hdr[4]) fail(CRYS_ECONTRACT, "group value outside its declared domain");
+}
+}  // namespace crys
+
 extern "C" {
 
 const char* crys_last_error(void) { return g_last_error.c_str(); }
 
 const char* crys_version(void) {
-  return "crystal_b200 1.0 (sm_100a; fused SSB q1.1-q4.3, select/project, hash join, radix sort)";
+  return "crystal_b200 2.0 (sm_100a; fused SSB q1.1-q4.3, device groups + NCCL reduce, select/project, "
+         "hash join, radix sort)";
 }
+
+const char* crys_nccl_version(void) { return crys::nccl_status(); }
+
+int crys_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
 
 crys_status crys_init(int device, crys_ctx** out) {
   return guarded([&] {
     CRYS_CHECK(out != nullptr, CRYS_ECONFIG, "null output handle");
-    int n = 0;
-    CUDA_TRY(cudaGetDeviceCount(&n));
-    CRYS_CHECK(device >= 0 && device < n, CRYS_ECONFIG, "no such CUDA device");
-    CUDA_TRY(cudaSetDevice(device));
-    cudaDeviceProp prop;
-    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
-    CRYS_CHECK(prop.major == 10, CRYS_ENOTBUILT,
-               std::string("library is compiled for sm_100a only; device is ") + prop.name);
-    auto* ctx = new crys_ctx();
-    ctx->device = device;
-    ctx->num_sms = prop.multiProcessorCount;
-    cudaError_t e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
-    if (e != cudaSuccess) {
-      delete ctx;
-      crys::fail(CRYS_ECUDA, cudaGetErrorString(e));
-    }
-    ctx->stream = ctx->own_stream;
-    for (auto& ev : ctx->ev) CUDA_TRY(cudaEventCreate(&ev));
-    *out = ctx;
+    *out = crys::new_context(device);
   });
 }
+
+crys_status crys_init_group(int nshards, const int* devices, crys_ctx** out) {
+  return guarded([&] {
+    CRYS_CHECK(out != nullptr, CRYS_ECONFIG, "null output handle");
+    *out = crys::new_group(nshards, devices);
+  });
+}
+
+int crys_group_shards(const crys_ctx* ctx) { return ctx ? crys::group_shards(ctx) : 0; }
+int crys_group_devices(const crys_ctx* ctx) { return ctx ? crys::group_devices(ctx) : 0; }
+int crys_group_uses_nccl(const crys_ctx* ctx) { return ctx && crys::group_nccl(ctx) ? 1 : 0; }
 
 void crys_destroy(crys_ctx* ctx) {
   if (!ctx) return;
@@ -310,7 +372,26 @@ crys_status crys_db_generate(crys_ctx* ctx, int64_t sf, uint64_t seed, int64_t l
     db->lo_begin = lo_begin;
     db->lo_end = lo_end;
     try {
-      crys::ssb_generate(ctx, db);
+      if (ctx->group) {  // every shard generates its row range + the dimensions on its device
+        const int64_t rows = 6000000LL * sf;  // ssb_gen.cpp:179
+        if (db->lo_end < 0 || db->lo_end > rows) db->lo_end = rows;
+        CRYS_CHECK(db->lo_begin >= 0 && db->lo_begin <= db->lo_end, CRYS_ECONFIG, "bad lineorder shard range");
+        const int S = crys::group_shards(ctx);
+        for (int sh = 0; sh < S; ++sh) {
+          crys_ctx* m = crys::group_member_of_shard(ctx, sh);
+          CUDA_TRY(cudaSetDevice(m->device));
+          auto* part = new crys_db();
+          db->shards.push_back(part);
+          part->ctx = m;
+          part->sf = sf;
+          part->seed = seed;
+          crys::shard_range(db->lo_begin, db->lo_end, sh, S, &part->lo_begin, &part->lo_end);
+          crys::ssb_generate(m, part);
+        }
+        CUDA_TRY(cudaSetDevice(ctx->device));
+      } else {
+        crys::ssb_generate(ctx, db);
+      }
     } catch (...) {
       delete db;
       throw;
@@ -345,12 +426,40 @@ crys_status crys_db_create(crys_ctx* ctx, int64_t sf, uint64_t seed, crys_db** o
     db->ctx = ctx;
     db->sf = sf;
     db->seed = seed;
+    for (int sh = 0; ctx->group && sh < crys::group_shards(ctx); ++sh) {
+      auto* part = new crys_db();
+      db->shards.push_back(part);
+      part->ctx = crys::group_member_of_shard(ctx, sh);
+      part->sf = sf;
+      part->seed = seed;
+    }
     *out = db;
   });
 }
 
 crys_status crys_db_upload_column(crys_db* db, const char* table, const char* column,
                                   const int32_t* h_data, int64_t rows) {
+  if (db && db->is_group()) {  // lineorder: row-range slices; dimensions: every shard
+    const bool fact = table && std::string(table) == "lineorder";
+    const int S = (int)db->shards.size();
+    for (int sh = 0; sh < S; ++sh) {
+      int64_t b = 0, e = rows;
+      if (fact) crys::shard_range(0, rows, sh, S, &b, &e);
+      const crys_status st = crys_db_upload_column(db->shards[(size_t)sh], table, column,
+                                                   h_data ? h_data + b : nullptr, e - b);
+      if (st != CRYS_OK) return st;
+      if (fact) {
+        db->shards[(size_t)sh]->lo_begin = b;
+        db->shards[(size_t)sh]->lo_end = e;
+      }
+    }
+    if (fact) {
+      db->lo_begin = 0;
+      db->lo_end = rows;
+    }
+    cudaSetDevice(db->ctx->device);
+    return CRYS_OK;
+  }
   return guarded([&] {
     CRYS_CHECK(db && table && column, CRYS_ECONFIG, "null argument");
     bind(db->ctx);
@@ -372,6 +481,49 @@ crys_status crys_db_upload_column(crys_db* db, const char* table, const char* co
 }
 
 crys_status crys_db_upload_host(crys_db* db, const crys_host_column* cols, int ncols) {
+  if (db && db->is_group()) {
+    // lineorder columns are cut into the shards' row ranges; dimension columns
+    // go to the first shard of every device (the one that builds its tables)
+    int64_t lo_rows = -1;
+    for (int i = 0; i < ncols && cols; ++i)
+      if (cols[i].table && std::string(cols[i].table) == "lineorder") {
+        if (lo_rows >= 0 && cols[i].rows != lo_rows) {
+          g_last_error = "lineorder columns of different length";
+          return CRYS_ECONTRACT;
+        }
+        lo_rows = cols[i].rows;
+      }
+    const int S = (int)db->shards.size();
+    for (int sh = 0; sh < S; ++sh) {
+      crys_db* part = db->shards[(size_t)sh];
+      const bool dims = crys::shard_holds_dims(db->ctx, sh);
+      int64_t b = 0, e = 0;
+      if (lo_rows >= 0) crys::shard_range(0, lo_rows, sh, S, &b, &e);
+      std::vector<crys_host_column> mine;
+      for (int i = 0; i < ncols; ++i) {
+        crys_host_column c = cols[i];
+        if (c.table && std::string(c.table) == "lineorder") {
+          c.h_data = c.h_data ? c.h_data + b : nullptr;
+          c.rows = e - b;
+        } else if (!dims) {
+          continue;
+        }
+        mine.push_back(c);
+      }
+      const crys_status st = crys_db_upload_host(part, mine.data(), (int)mine.size());
+      if (st != CRYS_OK) return st;
+      if (lo_rows >= 0) {
+        part->lo_begin = b;
+        part->lo_end = e;
+      }
+    }
+    if (lo_rows >= 0) {
+      db->lo_begin = 0;
+      db->lo_end = lo_rows;
+    }
+    cudaSetDevice(db->ctx->device);
+    return CRYS_OK;
+  }
   return guarded([&] {
     CRYS_CHECK(db && (ncols == 0 || cols), CRYS_ECONFIG, "null argument");
     crys_ctx* ctx = db->ctx;
@@ -440,6 +592,8 @@ void io_ready(crys_ctx* ctx) {
 
 crys_status crys_db_load_column_file(crys_db* db, const char* table, const char* column, const char* path) {
   return guarded([&] {
+    CRYS_CHECK(!(db && db->is_group()), CRYS_ECONFIG,
+               "a device-group database has one column per shard (use a shard's context)");
     CRYS_CHECK(db && table && column && path, CRYS_ECONFIG, "null argument");
     crys_ctx* ctx = db->ctx;
     bind(ctx);
@@ -503,6 +657,8 @@ crys_status crys_db_load_column_file(crys_db* db, const char* table, const char*
 
 crys_status crys_db_save_column_file(const crys_db* db, const char* table, const char* column, const char* path) {
   return guarded([&] {
+    CRYS_CHECK(!(db && db->is_group()), CRYS_ECONFIG,
+               "a device-group database has one column per shard (use a shard's context)");
     CRYS_CHECK(db && table && column && path, CRYS_ECONFIG, "null argument");
     crys_ctx* ctx = db->ctx;
     bind(ctx);
@@ -529,6 +685,8 @@ crys_status crys_db_save_column_file(const crys_db* db, const char* table, const
 crys_status crys_db_column(const crys_db* db, const char* table, const char* column,
                            const int32_t** d_data, int64_t* rows) {
   return guarded([&] {
+    CRYS_CHECK(!(db && db->is_group()), CRYS_ECONFIG,
+               "a device-group database has one column per shard (use a shard's context)");
     CRYS_CHECK(db && table && column && d_data, CRYS_ECONFIG, "null argument");
     *d_data = db->col(table, column, rows);
   });
@@ -536,6 +694,30 @@ crys_status crys_db_column(const crys_db* db, const char* table, const char* col
 
 crys_status crys_db_download_column(const crys_db* db, const char* table, const char* column,
                                     int32_t* h_out, int64_t rows) {
+  if (db && db->is_group()) {  // lineorder: the shards in row order; dimensions: shard 0
+    const bool fact = table && std::string(table) == "lineorder";
+    int64_t off = 0;
+    for (const crys_db* part : db->shards) {
+      int64_t n = 0;
+      const int32_t* d = nullptr;
+      const crys_status st0 = crys_db_column(part, table, column, &d, &n);
+      if (st0 != CRYS_OK) return st0;
+      if (!fact) return crys_db_download_column(part, table, column, h_out, rows);
+      if (off + n > rows) {
+        g_last_error = "row count mismatch";
+        return CRYS_ECONTRACT;
+      }
+      const crys_status st = crys_db_download_column(part, table, column, h_out + off, n);
+      if (st != CRYS_OK) return st;
+      off += n;
+    }
+    cudaSetDevice(db->ctx->device);
+    if (off != rows) {
+      g_last_error = "row count mismatch";
+      return CRYS_ECONTRACT;
+    }
+    return CRYS_OK;
+  }
   return guarded([&] {
     CRYS_CHECK(db && table && column && h_out, CRYS_ECONFIG, "null argument");
     bind(db->ctx);
@@ -551,8 +733,14 @@ crys_status crys_db_download_column(const crys_db* db, const char* table, const 
 
 void crys_db_free(crys_db* db) {
   if (!db) return;
+  for (crys_db* part : db->shards) {
+    cudaSetDevice(part->ctx->device);
+    cudaStreamSynchronize(part->ctx->stream);
+    crys::forget_db(part->ctx, part->uid);
+  }
   cudaSetDevice(db->ctx->device);
   cudaStreamSynchronize(db->ctx->stream);
+  crys::forget_db(db->ctx, db->uid);
   delete db;
 }
 
@@ -581,8 +769,15 @@ crys_status crys_run_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, in
     bind(ctx);
     CRYS_CHECK(db != nullptr && nrows != nullptr, CRYS_ECONFIG, "null argument");
     CRYS_CHECK(bt > 0 && ipt > 0, CRYS_ECONFIG, "TileConfig: block_threads/items_per_thread must be positive");
+    crys::plan_for(qid);  // ConfigError for an unknown id
     crys::ResultRows r;
-    crys::ssb_run_query(ctx, db, qid, bt, ipt, &r);
+    if (db->is_group()) {
+      CRYS_CHECK(db->ctx == ctx, CRYS_ECONFIG, "device-group database belongs to another context");
+      crys::ssb_run_group(ctx, db, qid, bt, ipt, &r);
+    } else {
+      CRYS_CHECK(db->ctx->device == ctx->device, CRYS_ECONFIG, "database lives on another device");
+      crys::ssb_run_query(ctx, db, qid, bt, ipt, &r);
+    }
     fill_survivors(qid, r, h_survivors);
     crys::emit_rows(qid, r.cell, r.sum, h_groups, h_sums, max_rows, nrows);
   });
@@ -643,31 +838,58 @@ crys_status crys_run_query_host(crys_ctx* ctx, const crys_host_column* cols, int
 }
 
 crys_status crys_query_partial(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt,
-                               int64_t* d_agg, int64_t* d_survivors) {
+                               int64_t* d_agg, int64_t* d_hdr) {
   return guarded([&] {
     bind(ctx);
-    CRYS_CHECK(db && d_agg && d_survivors, CRYS_ECONFIG, "null argument");
-    ctx->scratch2.reserve(64);
-    int32_t* err = ctx->scratch2.as<int32_t>();
-    CUDA_TRY(cudaMemsetAsync(err, 0, sizeof(int32_t), ctx->stream));
+    CRYS_CHECK(db && d_agg && d_hdr, CRYS_ECONFIG, "null argument");
+    CRYS_CHECK(!db->is_group() && db->ctx->device == ctx->device, CRYS_ECONFIG,
+               "partial: a single-device database on this context's device");
     crys::ssb_query_partial(ctx, db, qid, bt, ipt, reinterpret_cast<unsigned long long*>(d_agg),
-                            reinterpret_cast<unsigned long long*>(d_survivors), err);
+                            reinterpret_cast<long long*>(d_hdr));
   });
 }
 
-crys_status crys_query_finalize(crys_ctx* ctx, int qid, const int64_t* d_agg, int32_t* h_groups,
-                                int64_t* h_sums, int64_t max_rows, int64_t* nrows) {
+crys_status crys_query_partial_box(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt,
+                                   int64_t* d_buf, int64_t cap, int64_t* len, crys_group_box* box) {
   return guarded([&] {
     bind(ctx);
-    CRYS_CHECK(d_agg && nrows, CRYS_ECONFIG, "null argument");
+    CRYS_CHECK(db && d_buf && len && box, CRYS_ECONFIG, "null argument");
+    CRYS_CHECK(!db->is_group() && db->ctx->device == ctx->device, CRYS_ECONFIG,
+               "partial: a single-device database on this context's device");
+    crys::ssb_partial_box(ctx, {db}, qid, bt, ipt, reinterpret_cast<long long*>(d_buf), cap, box, len, false);
+  });
+}
+
+crys_status crys_query_finalize_box(crys_ctx* ctx, int qid, const crys_group_box* box, const int64_t* d_buf,
+                                    int32_t* h_groups, int64_t* h_sums, int64_t max_rows, int64_t* nrows,
+                                    int64_t* h_survivors) {
+  return guarded([&] {
+    bind(ctx);
+    CRYS_CHECK(box && d_buf && nrows, CRYS_ECONFIG, "null argument");
     crys::ResultRows r;
-    crys::ssb_finalize_device(ctx, qid, reinterpret_cast<const unsigned long long*>(d_agg), &r);
+    crys::ssb_finalize_packed(ctx, qid, *box, reinterpret_cast<const long long*>(d_buf), &r);
+    fill_survivors(qid, r, h_survivors);
     crys::emit_rows(qid, r.cell, r.sum, h_groups, h_sums, max_rows, nrows);
   });
 }
 
-crys_status crys_query_finalize_host(int qid, const int64_t* h_agg, int32_t* h_groups,
-                                     int64_t* h_sums, int64_t max_rows, int64_t* nrows) {
+crys_status crys_query_finalize(crys_ctx* ctx, int qid, const int64_t* d_agg, const int64_t* d_hdr,
+                                int32_t* h_groups, int64_t* h_sums, int64_t max_rows, int64_t* nrows,
+                                int64_t* h_survivors) {
+  return guarded([&] {
+    bind(ctx);
+    CRYS_CHECK(d_agg && nrows, CRYS_ECONFIG, "null argument");
+    crys::ResultRows r;
+    crys::ssb_finalize_device(ctx, qid, reinterpret_cast<const unsigned long long*>(d_agg),
+                              reinterpret_cast<const long long*>(d_hdr), &r);
+    fill_survivors(qid, r, h_survivors);
+    crys::emit_rows(qid, r.cell, r.sum, h_groups, h_sums, max_rows, nrows);
+  });
+}
+
+
+crys_status crys_query_finalize_host(int qid, const int64_t* h_agg, const int64_t* h_hdr, int32_t* h_groups,
+                                     int64_t* h_sums, int64_t max_rows, int64_t* nrows, int64_t* h_survivors) {
   return guarded([&] {
     CRYS_CHECK(h_agg && nrows, CRYS_ECONFIG, "null argument");
     const crys::QueryPlan& plan = crys::plan_for(qid);
@@ -679,7 +901,12 @@ crys_status crys_query_finalize_host(int qid, const int64_t* h_agg, int32_t* h_g
         sums.push_back(h_agg[c]);
       }
     }
+    if (h_survivors) {
+      const int ns = plan.joins.empty() ? 1 : (int)plan.joins.size();
+      for (int j = 0; j < 4; ++j) h_survivors[j] = (h_hdr && j < ns) ? h_hdr[j] : 0;
+    }
     crys::emit_rows(qid, cell, sums, h_groups, h_sums, max_rows, nrows);
+    crys::raise_partial_errors(qid, h_hdr);
   });
 }
 

@@ -53,7 +53,12 @@ struct HtMeta {
   int32_t count;  // filtered build rows
   uint32_t mask;  // capacity - 1
   int32_t shift;  // 32 - log2(capacity)   (hash_table.cpp:12-16)
-  int32_t err;    // 1 sentinel key, 2 duplicate key (BuildError)
+  int32_t err;    // 1 sentinel key, 2 duplicate key, 3 capacity (BuildError), 4 key outside stats
+  // group digits (payload - lo) of the rows that passed the filters: the
+  // extent of the group-by sub-box a query can occupy (identical on every
+  // shard, since dimensions are replicated).  dmin > dmax: no digit.
+  int32_t dmin, dmax;
+  int32_t pad[2];
 };
 
 // Packs a {key, payload} slot into the 64-bit word atomicCAS operates on

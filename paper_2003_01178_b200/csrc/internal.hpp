@@ -110,10 +110,12 @@ void lower_pred(const crys_pred& p, int32_t* lo, int32_t* hi);
 // ------------------------------------------------------------ runtime
 struct QueryWorkspace;
 struct SortWorkspace;
+struct Group;
 // Workspaces are complete only in their own .cu file.
 struct WsDeleter {
   void operator()(QueryWorkspace* p) const;
   void operator()(SortWorkspace* p) const;
+  void operator()(Group* p) const;
 };
 
 }  // namespace crys
@@ -139,11 +141,20 @@ struct crys_ctx {
   cudaStream_t graph_stream = nullptr; // query graphs are captured/replayed here (lazy)
   cudaEvent_t graph_fence = nullptr;
   cudaEvent_t io_ev[2] = {nullptr, nullptr};
+  // non-null: a device group (crys_init_group); this ctx then acts on the
+  // root device and the members do the per-device work
+  std::unique_ptr<crys::Group, crys::WsDeleter> group;
   ~crys_ctx();
 };
 
 struct crys_db {
   crys_ctx* ctx = nullptr;
+  uint64_t uid = 0;  // unique for the process lifetime (graph / tuning cache keys)
+  // a database on a device group: one complete database per shard (its
+  // lineorder row range + replicated dimensions) on the shard's member ctx
+  std::vector<crys_db*> shards;
+  bool is_group() const { return !shards.empty(); }
+  crys_db();
   int64_t sf = 0;
   uint64_t seed = 0;
   int64_t lo_begin = 0, lo_end = 0;  // shard of the full lineorder
@@ -178,9 +189,21 @@ struct crys_ht {
 
 namespace crys {
 
+// Contexts and device groups (capi.cpp, group.cpp).
+crys_ctx* new_context(int device);
+crys_ctx* new_group(int nshards, const int* devices);
+int group_shards(const crys_ctx* ctx);
+int group_devices(const crys_ctx* ctx);
+bool group_nccl(const crys_ctx* ctx);
+crys_ctx* group_member_of_shard(const crys_ctx* gctx, int shard);
+bool shard_holds_dims(const crys_ctx* gctx, int shard);
+void shard_range(int64_t lo, int64_t hi, int s, int S, int64_t* b, int64_t* e);
+const char* nccl_status();
+
 // Raise (never lower) a kernel's dynamic shared-memory limit; the attribute
 // is per function, so one kernel shared by plans of different sizes must keep
-// the largest value it has ever been launched with.
+// the largest value it has ever been launched with.  The attribute is also per
+// device, so the bookkeeping is keyed by (current device, function).
 void ensure_dyn_smem(const void* fn, size_t bytes);
 
 // Launch accounting + event timing helpers.
@@ -197,7 +220,7 @@ void fill_uniform_i32(crys_ctx* ctx, int32_t* out, int64_t n, uint64_t seed, uin
 void fill_float_pairs(crys_ctx* ctx, float* x1, float* x2, int64_t n, uint64_t seed, uint64_t stream,
                       float lo, float hi);
 void ssb_query_partial(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt,
-                       unsigned long long* d_agg, unsigned long long* d_surv, int32_t* d_err);
+                       unsigned long long* d_agg, long long* d_hdr);
 struct ResultRows {
   std::vector<int64_t> cell;
   std::vector<int64_t> sum;
@@ -205,8 +228,17 @@ struct ResultRows {
   int32_t err = 0;
 };
 void ssb_run_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt, ResultRows* out);
-void ssb_finalize_device(crys_ctx* ctx, int qid, const unsigned long long* d_agg,
+void ssb_finalize_device(crys_ctx* ctx, int qid, const unsigned long long* d_agg, const long long* d_hdr,
                          ResultRows* out);
+void ssb_finalize_packed(crys_ctx* ctx, int qid, const crys_group_box& box, const long long* d_buf,
+                         ResultRows* out);
+// One device's packed partial over its fact shards (dimensions from facts[0]).
+void ssb_partial_box(crys_ctx* ctx, const std::vector<const crys_db*>& facts, int qid, int bt, int ipt,
+                     long long* d_out, int64_t cap, crys_group_box* box, int64_t* len, bool defer_tune);
+void ssb_tune_done(crys_ctx* ctx);               // completes a deferred autotuning measurement
+long long* ssb_group_buffer(crys_ctx* ctx, int64_t n);  // member workspace for the packed partial
+void forget_db(crys_ctx* ctx, uint64_t uid);     // drop a freed database's graphs / tuning
+void ssb_run_group(crys_ctx* gctx, const crys_db* gdb, int qid, int bt, int ipt, ResultRows* out);
 void emit_rows(int qid, const std::vector<int64_t>& cell, const std::vector<int64_t>& sums,
                int32_t* h_groups, int64_t* h_sums, int64_t max_rows, int64_t* nrows);
 

@@ -13,6 +13,7 @@
 //                          probed L2/HBM-resident
 #include <algorithm>
 #include <map>
+#include <tuple>
 #include <mutex>
 
 #include "async.cuh"
@@ -1229,9 +1230,11 @@ int join_l2_ahead(bool table_on_chip) {
 
 int occupancy(const void* fn, int bt, size_t smem) {
   static std::mutex mu;
-  static std::map<std::pair<const void*, size_t>, int> cache;
+  static std::map<std::tuple<int, const void*, size_t>, int> cache;
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lk(mu);
-  auto key = std::make_pair(fn, smem);
+  auto key = std::make_tuple(dev, fn, smem);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   ensure_dyn_smem(fn, smem);

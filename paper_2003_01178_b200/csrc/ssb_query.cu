@@ -28,6 +28,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <tuple>
 
 #include "crystal.cuh"
 #include "internal.hpp"
@@ -96,11 +97,62 @@ struct Flight1Args {
 struct ResultHeader {
   unsigned long long nrows;
   unsigned long long surv[4];
-  int32_t err;
-  int32_t ht_err;
+  int32_t err;     // rows that reached the aggregate with a group value outside its domain
+  int32_t ht_err;  // first join (plan order) whose build failed: (join << 8) | code
   int32_t pad[4];
 };
 static_assert(sizeof(ResultHeader) == 64, "header is one 64 B line");
+
+// The group-by sub-box a query can occupy (host-built plan part + the device
+// digit extents in HtMeta): part g is fed by join `join[g]`, its full domain
+// has fcard[g] values and mixed-radix stride fstride[g] (last part fastest).
+enum BoxMode : int32_t { kBoxFull = 0, kBoxMeta = 1, kBoxExplicit = 2 };
+struct BoxPlan {
+  int32_t nparts;
+  int32_t join[3];
+  int32_t fcard[3];
+  int32_t mode;            // BoxMode: whole domain / digit extents in HtMeta / xmin+xcard
+  int32_t xmin[3], xcard[3];
+  int64_t fstride[3];
+};
+struct BoxD {
+  int32_t dmin[3], card[3];
+  int64_t cells;
+};
+
+__device__ __forceinline__ BoxD box_of(const BoxPlan& p, const HtMeta* meta) {
+  BoxD b;
+  b.cells = 1;
+  for (int g = 0; g < 3; ++g) {
+    b.dmin[g] = 0;
+    b.card[g] = 1;
+    if (g >= p.nparts) continue;
+    int32_t lo = 0, hi = p.fcard[g] - 1;
+    if (p.mode == kBoxMeta) {
+      const HtMeta& m = meta[p.join[g]];
+      lo = max(lo, m.dmin);
+      hi = min(hi, m.dmax);
+    } else if (p.mode == kBoxExplicit) {
+      lo = max(lo, p.xmin[g]);
+      hi = min(hi, p.xmin[g] + p.xcard[g] - 1);
+    }
+    b.dmin[g] = lo;
+    b.card[g] = hi >= lo ? hi - lo + 1 : 0;
+    b.cells *= b.card[g];
+  }
+  return b;
+}
+
+// box cell -> full mixed-radix cell index
+__device__ __forceinline__ int64_t box_to_full(const BoxPlan& p, const BoxD& b, int64_t i) {
+  int64_t full = 0;
+  for (int g = p.nparts - 1; g >= 0; --g) {
+    const int64_t d = i % b.card[g];
+    i /= b.card[g];
+    full += (b.dmin[g] + d) * p.fstride[g];
+  }
+  return full;
+}
 
 struct RowOut {
   long long cell;
@@ -126,7 +178,7 @@ __global__ void query_prologue_kernel(const PrologueArgs a) {
   }
   for (int64_t i = tid; i < a.zero64_n; i += stride) a.zero64[i] = 0;
   for (int64_t i = tid; i < a.zero64b_n; i += stride) a.zero64b[i] = 0;
-  if (tid < kMaxJoins) a.meta[tid] = HtMeta{0, 0u, 0, 0};
+  if (tid < kMaxJoins) a.meta[tid] = HtMeta{0, 0u, 0, 0, INT_MAX, INT_MIN, {0, 0}};
 }
 
 // ---------------------------------------------------------- dimension builds
@@ -165,9 +217,14 @@ __global__ void __launch_bounds__(256) dim_filter_kernel(const DimBuildArgs a) {
   // build size: per-warp atomics only where the compaction needs positions
   // (kTabHash); direct tables count in shared memory, one global add per CTA
   // (a per-warp add to one address serialised ~30 us on the 1 M-row part table)
-  __shared__ int s_count;
-  if (threadIdx.x == 0) s_count = 0;
+  __shared__ int s_count, s_dmin, s_dmax;
+  if (threadIdx.x == 0) {
+    s_count = 0;
+    s_dmin = INT_MAX;
+    s_dmax = INT_MIN;
+  }
   __syncthreads();
+  int32_t dmin = INT_MAX, dmax = INT_MIN;  // digits of this thread's passing rows
   const bool hashed = d.kind == kTabHash;
   const int64_t span = (int64_t)blockDim.x * kDimU;
   for (int64_t base = (int64_t)blockIdx.x * span; base < d.rows; base += (int64_t)gridDim.x * span) {
@@ -205,6 +262,10 @@ __global__ void __launch_bounds__(256) dim_filter_kernel(const DimBuildArgs a) {
       }
       if (!pass) continue;
       const int32_t dig = digit_of(d, pay[u]);
+      if (dig >= 0) {
+        dmin = min(dmin, dig);
+        dmax = max(dmax, dig);
+      }
       if (hashed) {
         d.compact[pos0 + __popc(bal & lanemask_lt())] = make_int2(key[u], dig);
         continue;
@@ -226,8 +287,25 @@ __global__ void __launch_bounds__(256) dim_filter_kernel(const DimBuildArgs a) {
       if (!ok) atomicCAS(&m->err, 0, 2);  // duplicate key (BuildError)
     }
   }
+  if (d.gcard) {  // warp, then CTA, then one global min/max per CTA
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      dmin = min(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+      dmax = max(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    }
+    if (lane == 0 && dmin <= dmax) {
+      atomicMin(&s_dmin, dmin);
+      atomicMax(&s_dmax, dmax);
+    }
+  }
   __syncthreads();
-  if (threadIdx.x == 0 && !hashed && s_count) atomicAdd(&m->count, s_count);
+  if (threadIdx.x == 0) {
+    if (!hashed && s_count) atomicAdd(&m->count, s_count);
+    if (s_dmin <= s_dmax) {
+      atomicMin(&m->dmin, s_dmin);
+      atomicMax(&m->dmax, s_dmax);
+    }
+  }
 }
 
 __global__ void dim_init_kernel(const DimBuildArgs a) {
@@ -333,24 +411,33 @@ __global__ void __launch_bounds__(BT) ssb_flight1_kernel(const Flight1Args a) {
 }
 
 // Occupied cells -> (cell, sum) rows (grouped_result, ssb_queries.cpp:145-155).
-// Flight 1 always yields its single row (ssb_queries.cpp:207-209).
+// Flight 1 always yields its single row (ssb_queries.cpp:207-209).  Only the
+// group-by sub-box the dimension builds allow is scanned (q4.3: 800 of 1.75 M
+// cells); `packed` sources hold exactly the box cells (a reduced partial),
+// otherwise they are the full dense aggregate.
 __global__ void finalize_kernel(const unsigned long long* sums, const unsigned long long* cnts,
-                                int64_t cells, int flight1, ResultHeader* hdr, RowOut* rows,
+                                BoxPlan bp, int packed, int flight1, ResultHeader* hdr, RowOut* rows,
                                 const unsigned long long* surv, const int32_t* err,
                                 const HtMeta* meta, int nj) {
   const unsigned lane = lane_id();
+  const BoxD box = box_of(bp, meta);
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // QueryStats + error words ride in the header
     for (int j = 0; j < 4; ++j) hdr->surv[j] = surv ? surv[j] : 0;
     hdr->err = err ? *err : 0;
     int e = 0;
-    for (int j = 0; j < nj; ++j)
-      if (meta[j].err) e = meta[j].err;
+    for (int j = nj - 1; j >= 0; --j)  // the first failing build in plan order wins
+      if (meta[j].err) e = (j << 8) | meta[j].err;
     hdr->ht_err = e;
   }
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < cells;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < box.cells;
        base += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = base + threadIdx.x;
-    const bool take = c < cells && (cnts[c] != 0 || (flight1 && c == 0));
+    const int64_t b = base + threadIdx.x;
+    int64_t c = 0, src = 0;
+    if (b < box.cells) {
+      c = box_to_full(bp, box, b);
+      src = packed ? b : c;
+    }
+    const bool take = b < box.cells && (cnts[src] != 0 || (flight1 && c == 0));
     const unsigned bal = __ballot_sync(0xffffffffu, take);
     if (!bal) continue;
     const int leader = __ffs(bal) - 1;
@@ -360,9 +447,70 @@ __global__ void finalize_kernel(const unsigned long long* sums, const unsigned l
     if (take) {
       RowOut r;
       r.cell = c;
-      r.sum = (long long)sums[c];
+      r.sum = (long long)sums[src];
       rows[p0 + __popc(bal & lanemask_lt())] = r;
     }
+  }
+}
+
+// The dimension builds' digit extents -> host-mapped memory (the host sizes
+// the collective from them while the fused pass runs), then a ready flag.
+struct HostBox {
+  int32_t dmin[kMaxJoins], dmax[kMaxJoins];
+  volatile int32_t ready;
+  int32_t pad[7];
+};
+__global__ void box_publish_kernel(const HtMeta* meta, int nj, HostBox* hb) {
+  if (threadIdx.x == 0) {
+    for (int j = 0; j < nj; ++j) {
+      hb->dmin[j] = meta[j].dmin;
+      hb->dmax[j] = meta[j].dmax;
+    }
+    __threadfence_system();
+    hb->ready = 1;
+  }
+}
+
+// Packs this device's dense aggregate into the partial layout of
+// crystal_b200.h (CRYS_PARTIAL_HEADER int64 header, then the box's sums and
+// counts) -- the payload of the one NCCL reduce.  Header words ADD into
+// `out` (several shards of one device accumulate before the pack).
+__global__ void pack_partial_kernel(const unsigned long long* sums, const unsigned long long* cnts,
+                                    BoxPlan bp, const HtMeta* meta, int nj,
+                                    const unsigned long long* surv, const int32_t* err,
+                                    long long* out, int64_t cap) {
+  const BoxD box = box_of(bp, meta);
+  if (CRYS_PARTIAL_HEADER + 2 * box.cells > cap) return;  // the host raises ContractError
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    for (int j = 0; j < 4; ++j) out[j] = surv ? (long long)surv[j] : 0;
+    out[4] = (err && *err) ? 1 : 0;
+    for (int i = 5; i < CRYS_PARTIAL_HEADER; ++i) out[i] = 0;
+    for (int j = 0; j < nj; ++j) {
+      const int e = meta[j].err;
+      if (e >= 1 && e <= 4) out[8 + 4 * j + (e - 1)] = 1;
+    }
+  }
+  long long* ps = out + CRYS_PARTIAL_HEADER;
+  long long* pc = ps + box.cells;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < box.cells;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = box_to_full(bp, box, b);
+    ps[b] = (long long)sums[c];
+    pc[b] = (long long)cnts[c];
+  }
+}
+
+// The header words of a packed partial -> the ResultHeader error fields
+// (finalize of a reduced buffer; survivors are copied by finalize_kernel).
+__global__ void unpack_errors_kernel(const long long* hdr_in, ResultHeader* hdr) {
+  if (threadIdx.x == 0) {
+    // every finalize_kernel thread reads err / meta errors through here
+    int e = 0;
+    for (int j = 3; j >= 0; --j)
+      for (int c = 4; c >= 1; --c)
+        if (hdr_in[8 + 4 * j + (c - 1)]) e = (j << 8) | c;
+    hdr->err = hdr_in[4] ? 1 : 0;
+    hdr->ht_err = e;
   }
 }
 
@@ -398,9 +546,11 @@ F1Launch select_flight1() {
 
 int blocks_per_sm(const void* fn, int bt, size_t smem) {
   static std::mutex mu;
-  static std::map<std::pair<const void*, size_t>, int> cache;
+  static std::map<std::tuple<int, const void*, size_t>, int> cache;
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lk(mu);
-  auto key = std::make_pair(fn, smem);
+  auto key = std::make_tuple(dev, fn, smem);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   ensure_dyn_smem(fn, smem);
@@ -559,6 +709,11 @@ struct PipeTune {
   bool in_flight = false;  // the query in flight carries the measurements
 };
 
+// Graph / tuning caches are keyed by the database's unique id (never reused,
+// unlike its address), the query and the kind of sequence.
+enum SeqKind { kSeqQuery = 0, kSeqPartial = 1 };
+using SeqKey = std::tuple<uint64_t, int, int>;
+
 struct QueryWorkspace {
   DevBuf agg;      // u64 [2*cells] + counters: surv[4] + err
   DevBuf meta;     // HtMeta[4]
@@ -566,18 +721,23 @@ struct QueryWorkspace {
   DevBuf compact[kMaxJoins];
   DevBuf tables;   // every join's direct probe table, contiguous, 16 B aligned
   DevBuf result;   // ResultHeader + RowOut[cells]
+  DevBuf packed;   // the packed partial of a device group member (NCCL payload)
   PinnedBuf host;
-  std::map<std::pair<const crys_db*, int>, QueryGraph> graphs;
-  std::map<std::pair<const crys_db*, int>, PipeTune> tune;
+  HostBox* hbox = nullptr;  // host-mapped digit extents (box_publish_kernel)
+  std::map<SeqKey, QueryGraph> graphs;
+  std::map<std::pair<uint64_t, int>, PipeTune> tune;
   PipeTune* measuring = nullptr;  // set by enqueue_query, completed after the sync
   ~QueryWorkspace() {
     for (auto& kv : graphs)
       if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
-    for (auto& kv : tune)
-      for (int k = 0; k < kTuneN; ++k) {
-        if (kv.second.e0[k]) cudaEventDestroy(kv.second.e0[k]);
-        if (kv.second.e1[k]) cudaEventDestroy(kv.second.e1[k]);
-      }
+    for (auto& kv : tune) destroy_events(kv.second);
+    if (hbox) cudaFreeHost(hbox);
+  }
+  static void destroy_events(PipeTune& t) {
+    for (int k = 0; k < kTuneN; ++k) {
+      if (t.e0[k]) cudaEventDestroy(t.e0[k]);
+      if (t.e1[k]) cudaEventDestroy(t.e1[k]);
+    }
   }
 };
 
@@ -588,31 +748,75 @@ static QueryWorkspace& ws_of(crys_ctx* ctx) {
   return *ctx->qws;
 }
 
+// crys_db_free: drop every graph / tuning entry of that database.
+void forget_db(crys_ctx* ctx, uint64_t uid) {
+  if (!ctx || !ctx->qws) return;
+  QueryWorkspace& ws = *ctx->qws;
+  for (auto it = ws.graphs.begin(); it != ws.graphs.end();) {
+    if (std::get<0>(it->first) == uid) {
+      if (it->second.exec) cudaGraphExecDestroy(it->second.exec);
+      it = ws.graphs.erase(it);
+    } else {
+      ++it;
+    }
+  }
+  for (auto it = ws.tune.begin(); it != ws.tune.end();) {
+    if (it->first.first == uid) {
+      if (ws.measuring == &it->second) ws.measuring = nullptr;
+      QueryWorkspace::destroy_events(it->second);
+      it = ws.tune.erase(it);
+    } else {
+      ++it;
+    }
+  }
+}
+
 static int64_t bit_ceil64(int64_t v) {
   int64_t c = 1;
   while (c < v) c <<= 1;
   return c;
 }
 
-// Enqueues dimension builds + the fused lineorder pass of `qid` over this
-// shard, accumulating into d_agg = [sums | counts] (cells each), d_surv[4] and
-// d_err.  `prologue_zero` additionally zeroes those buffers and the result
-// header in the same prologue launch (single-GPU path); the multi-GPU path
-// hands in caller-zeroed buffers.
-static void enqueue_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt,
-                          unsigned long long* d_agg, unsigned long long* d_surv, int32_t* d_err,
-                          unsigned long long* zero_extra, int64_t zero_extra_n, bool prologue_zero,
-                          bool tune_ok = false) {
+// The plan's group parts as a box plan (mixed radix, last part fastest).
+static BoxPlan box_plan(const QueryPlan& plan, BoxMode mode) {
+  BoxPlan bp;
+  std::memset(&bp, 0, sizeof(bp));
+  bp.nparts = (int32_t)plan.group.size();
+  CRYS_CHECK(bp.nparts <= 3, CRYS_ENOTBUILT, "at most three group parts");
+  bp.mode = plan.joins.empty() ? kBoxFull : mode;
+  int64_t stride = 1;
+  for (int g = bp.nparts - 1; g >= 0; --g) {
+    bp.join[g] = plan.group[g].join_index;
+    bp.fcard[g] = plan.group[g].hi - plan.group[g].lo + 1;
+    bp.fstride[g] = stride;
+    stride *= bp.fcard[g];
+  }
+  return bp;
+}
+
+// Enqueues dimension builds (from `dimdb`) + the fused lineorder pass of `qid`
+// over every fact shard in `facts` (lineorder columns; several shards of one
+// device accumulate into the same aggregate), into d_agg = [sums | counts]
+// (cells each), d_surv[4] and d_err.  `prologue_zero` additionally zeroes
+// those buffers and the result header in the same prologue launch; the
+// accumulating partial API hands in caller-zeroed buffers.  `hbox`: publish
+// the builds' digit extents to host-mapped memory right after the builds.
+static void enqueue_query(crys_ctx* ctx, const crys_db* dimdb, const std::vector<const crys_db*>& facts,
+                          int qid, int bt, int ipt, unsigned long long* d_agg,
+                          unsigned long long* d_surv, int32_t* d_err, unsigned long long* zero_extra,
+                          int64_t zero_extra_n, bool prologue_zero, bool tune_ok, HostBox* hbox) {
   const QueryPlan& plan = plan_for(qid);
   CRYS_CHECK(bt > 0 && ipt > 0, CRYS_ECONFIG, "TileConfig: block_threads/items_per_thread must be positive");
+  CRYS_CHECK(!facts.empty(), CRYS_ECONFIG, "no lineorder shard");
   QueryWorkspace& ws = ws_of(ctx);
   cudaStream_t st = ctx->stream;
   const int nj = (int)plan.joins.size();
   const int64_t cells = plan.cells();
 
-  int64_t n = 0;
+  // rows of every fact shard
   const std::string& first_col = nj ? plan.joins[0].fact_key : plan.fact_filters[0].column;
-  db->col("lineorder", first_col, &n);
+  std::vector<int64_t> nrows(facts.size());
+  for (size_t f = 0; f < facts.size(); ++f) facts[f]->col("lineorder", first_col, &nrows[f]);
 
   ws.meta.reserve(sizeof(HtMeta) * kMaxJoins);
   PrologueArgs pro;
@@ -652,13 +856,13 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int
       const DimJoin& dj = plan.joins[j];
       DimBuildDesc& d = da.d[j];
       int64_t rows = 0;
-      d.key = db->col(dj.dim_table, dj.dim_key, &rows);
+      d.key = dimdb->col(dj.dim_table, dj.dim_key, &rows);
       d.rows = rows;
-      d.payload = dj.payload.empty() ? nullptr : db->col(dj.dim_table, dj.payload, &rows);
+      d.payload = dj.payload.empty() ? nullptr : dimdb->col(dj.dim_table, dj.payload, &rows);
       CRYS_CHECK((int)dj.filters.size() <= 2, CRYS_ENOTBUILT, "at most two filters per join");
       d.nf = (int)dj.filters.size();
       for (int f = 0; f < d.nf; ++f) {
-        d.fcol[f] = db->col(dj.dim_table, dj.filters[f].column, &rows);
+        d.fcol[f] = dimdb->col(dj.dim_table, dj.filters[f].column, &rows);
         CRYS_CHECK(dj.filters[f].ranges.size() <= 2, CRYS_ENOTBUILT, "at most two ranges per filter");
         d.nranges[f] = (int)dj.filters[f].ranges.size();
         for (int r = 0; r < d.nranges[f]; ++r) {
@@ -673,7 +877,7 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int
       // table layout: a perfect hash over the dense key range when the key
       // column's statistics allow it, else the linear-probing table
       int32_t lo = 0, hi = -1;
-      const bool direct = db->col_range(dj.dim_table, dj.dim_key, &lo, &hi) &&
+      const bool direct = dimdb->col_range(dj.dim_table, dj.dim_key, &lo, &hi) &&
                           (int64_t)hi - lo + 1 <= kMaxDirect;
       if (direct) {
         d.kmin = (uint32_t)lo;
@@ -709,8 +913,6 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int
       t.meta = j;
       t.g = d.kind == kTabHash ? (const void*)d.slots : nullptr;
       if (d.kind != kTabHash) pipe::set_decode(t);
-      pa.col[j] = db->col("lineorder", dj.fact_key, &rows);
-      CRYS_CHECK(rows == n, CRYS_ECONTRACT, "lineorder columns of different length");
     }
     if (tbl_total) ws.tables.reserve(tbl_total);
     for (int j = 0; j < nj; ++j) {
@@ -746,12 +948,16 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int
       CRYS_LAUNCHED("dim_insert_kernel");
       count_launch(ctx, 2);
     }
+    if (hbox) {
+      box_publish_kernel<<<1, 32, 0, st>>>(ws.meta.as<HtMeta>(), nj, hbox);
+      CRYS_LAUNCHED("box_publish_kernel");
+      count_launch(ctx);
+    }
   }
 
-  // ---- the fused lineorder pass
+  // ---- the fused lineorder pass, once per fact shard
   int64_t rows = 0;
   if (nj) {
-    pa.n = n;
     pa.meta = ws.meta.as<HtMeta>();
     pa.l2_ahead = l2_ahead();
     pa.cells = (int32_t)cells;
@@ -760,23 +966,35 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int
     pa.surv = d_surv;
     pa.err = d_err;
     CRYS_CHECK(plan.agg != kAggExtPriceTimesDiscount, CRYS_ENOTBUILT, "join flights aggregate revenue");
-    pa.col[nj] = db->col("lineorder", "lo_revenue", &rows);
-    if (plan.agg == kAggRevenueMinusSupplyCost) pa.col[nj + 1] = db->col("lineorder", "lo_supplycost", &rows);
-    int cfg = pipe_cfg();  // CRYS_PIPE_CFG > 0 forces an instantiation
     auto launch = [&](TuneCand c) {
       pa.l2_ahead = c.l2;
-      if (nj == 3 && plan.agg == kAggRevenue)
-        launch_pipeline_cfg<3, 4>(ctx, pa, cells, plan.name, c.cfg);
-      else if (nj == 4 && plan.agg == kAggRevenueMinusSupplyCost)
-        launch_pipeline_cfg<4, 6>(ctx, pa, cells, plan.name, c.cfg);
-      else
-        fail(CRYS_ENOTBUILT, "no fused pipeline for this plan shape");
+      for (size_t f = 0; f < facts.size(); ++f) {
+        pa.n = nrows[f];
+        for (int j = 0; j < nj; ++j) {
+          pa.col[j] = facts[f]->col("lineorder", plan.joins[j].fact_key, &rows);
+          CRYS_CHECK(rows == pa.n, CRYS_ECONTRACT, "lineorder columns of different length");
+        }
+        pa.col[nj] = facts[f]->col("lineorder", "lo_revenue", &rows);
+        CRYS_CHECK(rows == pa.n, CRYS_ECONTRACT, "lineorder columns of different length");
+        if (plan.agg == kAggRevenueMinusSupplyCost) {
+          pa.col[nj + 1] = facts[f]->col("lineorder", "lo_supplycost", &rows);
+          CRYS_CHECK(rows == pa.n, CRYS_ECONTRACT, "lineorder columns of different length");
+        }
+        if (nj == 3 && plan.agg == kAggRevenue)
+          launch_pipeline_cfg<3, 4>(ctx, pa, cells, plan.name, c.cfg);
+        else if (nj == 4 && plan.agg == kAggRevenueMinusSupplyCost)
+          launch_pipeline_cfg<4, 6>(ctx, pa, cells, plan.name, c.cfg);
+        else
+          fail(CRYS_ENOTBUILT, "no fused pipeline for this plan shape");
+        count_launch(ctx);
+      }
     };
+    const int cfg = pipe_cfg();  // CRYS_PIPE_CFG > 0 forces an instantiation
     TuneCand run{cfg, l2_ahead()};
     const TuneCand* cands = nj == 3 ? kTune4 : kTune6;
     const int ncand = nj == 3 ? kTuneN : kTuneN6;
     if (cfg == 0 && l2_ahead() == 0 && (nj == 3 || nj == 4) && tune_enabled() && tune_ok) {
-      PipeTune& tn = ws.tune[{db, qid}];
+      PipeTune& tn = ws.tune[{dimdb->uid, qid}];
       if (tn.chosen >= 0) {
         run = cands[tn.chosen];
       } else {  // every candidate twice, the second run timed; the last run's result is kept
@@ -792,7 +1010,6 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int
             if (rep == 1) CUDA_TRY(cudaEventRecord(tn.e0[k], st));
             launch(cands[k]);
             if (rep == 1) CUDA_TRY(cudaEventRecord(tn.e1[k], st));
-            count_launch(ctx);
           }
         }
         tn.in_flight = true;
@@ -803,46 +1020,72 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int
     timing_kernel_begin(ctx);
     launch(run);
     timing_kernel_end(ctx);
-    count_launch(ctx);
     return;
   }
   Flight1Args fa;
   std::memset(&fa, 0, sizeof(fa));
-  fa.n = n;
   fa.g_sum = d_agg;
   fa.g_cnt = d_agg + cells;
   fa.surv = d_surv;
-  for (int f = 0; f < 3; ++f) {
-    fa.fcol[f] = db->col("lineorder", plan.fact_filters[f].column, &rows);
-    CRYS_CHECK(rows == n, CRYS_ECONTRACT, "lineorder columns of different length");
-    fa.flo[f] = plan.fact_filters[f].lo;
-    fa.fhi[f] = plan.fact_filters[f].hi;
-  }
-  // aggregate columns (agg_fact_columns, ssb_plans.cpp:287-299)
-  fa.agg_a = db->col("lineorder", "lo_extendedprice", &rows);
-  fa.agg_b = db->col("lineorder", "lo_discount", &rows);
-  fa.agg_b_is_f1 = plan.fact_filters.size() > 1 && plan.fact_filters[1].column == "lo_discount";
   F1Launch L = select_flight1();
   const int nb = blocks_per_sm((const void*)L.fn, L.bt, 0);
-  const int64_t ntiles = (n + (int64_t)L.bt * L.ipt - 1) / ((int64_t)L.bt * L.ipt);
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)nb * ctx->num_sms));
   timing_kernel_begin(ctx);
-  L.fn<<<grid, L.bt, 0, st>>>(fa);
-  CRYS_LAUNCHED(std::string("fused ") + plan.name + " bt=" + std::to_string(L.bt) + " ipt=" +
-                std::to_string(L.ipt) + " grid=" + std::to_string(grid));
+  for (size_t f = 0; f < facts.size(); ++f) {
+    const int64_t n = nrows[f];
+    fa.n = n;
+    for (int k = 0; k < 3; ++k) {
+      fa.fcol[k] = facts[f]->col("lineorder", plan.fact_filters[k].column, &rows);
+      CRYS_CHECK(rows == n, CRYS_ECONTRACT, "lineorder columns of different length");
+      fa.flo[k] = plan.fact_filters[k].lo;
+      fa.fhi[k] = plan.fact_filters[k].hi;
+    }
+    // aggregate columns (agg_fact_columns, ssb_plans.cpp:287-299)
+    fa.agg_a = facts[f]->col("lineorder", "lo_extendedprice", &rows);
+    fa.agg_b = facts[f]->col("lineorder", "lo_discount", &rows);
+    fa.agg_b_is_f1 = plan.fact_filters.size() > 1 && plan.fact_filters[1].column == "lo_discount";
+    const int64_t ntiles = (n + (int64_t)L.bt * L.ipt - 1) / ((int64_t)L.bt * L.ipt);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)nb * ctx->num_sms));
+    L.fn<<<grid, L.bt, 0, st>>>(fa);
+    CRYS_LAUNCHED(std::string("fused ") + plan.name + " bt=" + std::to_string(L.bt) + " ipt=" +
+                  std::to_string(L.ipt) + " grid=" + std::to_string(grid));
+    count_launch(ctx);
+  }
   timing_kernel_end(ctx);
-  count_launch(ctx);
+}
+
+// Adds this call's error words into a partial header (accumulating API).
+__global__ void partial_errors_kernel(const HtMeta* meta, int nj, const int32_t* err, long long* hdr) {
+  if (threadIdx.x == 0) {
+    if (*err) atomicAdd(reinterpret_cast<unsigned long long*>(hdr + 4), 1ull);
+    for (int j = 0; j < nj; ++j) {
+      const int e = meta[j].err;
+      if (e >= 1 && e <= 4) atomicAdd(reinterpret_cast<unsigned long long*>(hdr + 8 + 4 * j + (e - 1)), 1ull);
+    }
+  }
 }
 
 void ssb_query_partial(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt,
-                       unsigned long long* d_agg, unsigned long long* d_surv, int32_t* d_err) {
-  enqueue_query(ctx, db, qid, bt, ipt, d_agg, d_surv, d_err, nullptr, 0, false);
+                       unsigned long long* d_agg, long long* d_hdr) {
+  const QueryPlan& plan = plan_for(qid);
+  ctx->scratch2.reserve(64);
+  int32_t* err = ctx->scratch2.as<int32_t>();
+  CUDA_TRY(cudaMemsetAsync(err, 0, sizeof(int32_t), ctx->stream));
+  enqueue_query(ctx, db, {db}, qid, bt, ipt, d_agg, reinterpret_cast<unsigned long long*>(d_hdr), err,
+                nullptr, 0, false, false, nullptr);
+  partial_errors_kernel<<<1, 32, 0, ctx->stream>>>(ws_of(ctx).meta.as<HtMeta>(), (int)plan.joins.size(),
+                                                   err, d_hdr);
+  CRYS_LAUNCHED("partial_errors_kernel");
+  count_launch(ctx);
 }
 
 // Compaction kernel + the copy of the header and the first 2048 rows (stream
-// work only, so it can be captured into a query graph).
-static void finalize_enqueue(crys_ctx* ctx, int qid, const unsigned long long* d_agg,
-                             const unsigned long long* d_surv, const int32_t* d_err, bool hdr_zeroed) {
+// work only, so it can be captured into a query graph).  `src` is the dense
+// aggregate (packed = false) or a packed partial's box cells; with
+// `hdr_in` (a packed partial's header) the survivors and errors come from it.
+static void finalize_enqueue(crys_ctx* ctx, int qid, const unsigned long long* d_sums,
+                             const unsigned long long* d_cnts, const BoxPlan& bp, bool packed,
+                             const unsigned long long* d_surv, const int32_t* d_err,
+                             const long long* hdr_in, bool hdr_zeroed) {
   const QueryPlan& plan = plan_for(qid);
   QueryWorkspace& ws = ws_of(ctx);
   cudaStream_t st = ctx->stream;
@@ -852,11 +1095,17 @@ static void finalize_enqueue(crys_ctx* ctx, int qid, const unsigned long long* d
   if (!hdr_zeroed) CUDA_TRY(cudaMemsetAsync(hdr, 0, sizeof(ResultHeader), st));
   const int tpb = 256;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((cells + tpb - 1) / tpb, (int64_t)ctx->num_sms * 8));
-  finalize_kernel<<<grid, tpb, 0, st>>>(d_agg, d_agg + cells, cells, plan.joins.empty() ? 1 : 0, hdr,
-                                        rows, d_surv, d_err, ws.meta.as<HtMeta>(),
-                                        d_surv ? (int)plan.joins.size() : 0);
+  const int nj = d_err ? (int)plan.joins.size() : 0;  // build errors of this ctx's own dimension builds
+  finalize_kernel<<<grid, tpb, 0, st>>>(d_sums, d_cnts, bp, packed ? 1 : 0, plan.joins.empty() ? 1 : 0, hdr,
+                                        rows, hdr_in ? reinterpret_cast<const unsigned long long*>(hdr_in) : d_surv,
+                                        d_err, ws.meta.as<HtMeta>(), nj);
   CRYS_LAUNCHED("finalize_kernel");
   count_launch(ctx);
+  if (hdr_in) {
+    unpack_errors_kernel<<<1, 32, 0, st>>>(hdr_in, hdr);
+    CRYS_LAUNCHED("unpack_errors_kernel");
+    count_launch(ctx);
+  }
   const int64_t first = std::min<int64_t>(cells, 2048);
   const size_t first_bytes = sizeof(ResultHeader) + sizeof(RowOut) * (size_t)first;
   CUDA_TRY(cudaMemcpyAsync(ws.host.p, hdr, first_bytes, cudaMemcpyDeviceToHost, st));
@@ -866,6 +1115,16 @@ static void finalize_reserve(crys_ctx* ctx, int64_t cells) {
   QueryWorkspace& ws = ws_of(ctx);
   ws.result.reserve(sizeof(ResultHeader) + sizeof(RowOut) * (size_t)cells);
   ws.host.reserve(sizeof(ResultHeader) + sizeof(RowOut) * (size_t)cells);
+  ws.meta.reserve(sizeof(HtMeta) * kMaxJoins);
+}
+
+static const char* ht_error_message(int code) {
+  switch (code) {
+    case 1: return "HashTable: key equals empty sentinel";
+    case 2: return "HashTable: duplicate key";
+    case 3: return "HashTable: capacity overflow";
+    default: return "dimension key outside its column statistics";
+  }
 }
 
 // Host side after the stream work: wait, fetch any rows past the first 2048,
@@ -899,25 +1158,45 @@ static void finalize_host_part(crys_ctx* ctx, int qid, ResultRows* out) {
     out->cell[(size_t)i] = v[(size_t)i].first;
     out->sum[(size_t)i] = v[(size_t)i].second;
   }
-  if (ht_err == 1) fail(CRYS_EBUILD, "HashTable: key equals empty sentinel");
-  if (ht_err == 2) fail(CRYS_EBUILD, "HashTable: duplicate key");
-  if (ht_err == 3) fail(CRYS_EBUILD, "HashTable: capacity overflow");
-  if (ht_err == 4) fail(CRYS_ECONTRACT, "dimension key outside its column statistics");
+  // the build errors of the first failing join in plan order (the reference
+  // builds the dimension tables in plan order and throws at the first)
+  if (ht_err) {
+    const int code = ht_err & 0xFF;
+    fail(code == 4 ? CRYS_ECONTRACT : CRYS_EBUILD,
+         std::string(ht_error_message(code)) + " (join " + std::to_string(ht_err >> 8) + " of " + plan.name + ")");
+  }
   if (out->err) fail(CRYS_ECONTRACT, "group value outside its declared domain");
 }
 
-static void finalize_impl(crys_ctx* ctx, int qid, const unsigned long long* d_agg,
-                          const unsigned long long* d_surv, const int32_t* d_err, ResultRows* out,
-                          bool hdr_zeroed) {
-  finalize_reserve(ctx, plan_for(qid).cells());
-  finalize_enqueue(ctx, qid, d_agg, d_surv, d_err, hdr_zeroed);
+// Finalize of a caller's dense [sums | counts] (+ optional partial header).
+void ssb_finalize_device(crys_ctx* ctx, int qid, const unsigned long long* d_agg, const long long* d_hdr,
+                         ResultRows* out) {
+  const int64_t cells = plan_for(qid).cells();
+  finalize_reserve(ctx, cells);
+  const BoxPlan bp = box_plan(plan_for(qid), kBoxFull);
+  finalize_enqueue(ctx, qid, d_agg, d_agg + cells, bp, false, nullptr, nullptr, d_hdr, false);
   finalize_host_part(ctx, qid, out);
 }
 
-void ssb_finalize_device(crys_ctx* ctx, int qid, const unsigned long long* d_agg,
+// Finalize of a (reduced) packed partial whose box the caller knows.
+void ssb_finalize_packed(crys_ctx* ctx, int qid, const crys_group_box& box, const long long* d_buf,
                          ResultRows* out) {
-  ws_of(ctx).meta.reserve(sizeof(HtMeta) * kMaxJoins);
-  finalize_impl(ctx, qid, d_agg, nullptr, nullptr, out, false);
+  const QueryPlan& plan = plan_for(qid);
+  finalize_reserve(ctx, plan.cells());
+  BoxPlan bp = box_plan(plan, kBoxExplicit);
+  CRYS_CHECK(box.nparts == bp.nparts, CRYS_ECONTRACT, "group box does not match the query's group parts");
+  int64_t cells = 1;
+  for (int g = 0; g < bp.nparts; ++g) {
+    bp.xmin[g] = box.lo[g] - plan.group[g].lo;
+    bp.xcard[g] = box.card[g];
+    CRYS_CHECK(box.card[g] >= 0 && bp.xmin[g] >= 0 && bp.xmin[g] + box.card[g] <= bp.fcard[g],
+               CRYS_ECONTRACT, "group box outside the query's group domain");
+    cells *= box.card[g];
+  }
+  CRYS_CHECK(cells == box.cells, CRYS_ECONTRACT, "group box cell count mismatch");
+  const unsigned long long* s = reinterpret_cast<const unsigned long long*>(d_buf + CRYS_PARTIAL_HEADER);
+  finalize_enqueue(ctx, qid, s, s + cells, bp, true, nullptr, nullptr, d_buf, false);
+  finalize_host_part(ctx, qid, out);
 }
 
 // CRYS_GRAPHS=0 disables the per-query graph replay (A/B).
@@ -929,15 +1208,8 @@ static bool graphs_enabled() {
   return on;
 }
 
-static std::vector<uintptr_t> query_signature(crys_ctx* ctx, const crys_db* db) {
-  QueryWorkspace& ws = ws_of(ctx);
-  std::vector<uintptr_t> sig = {(uintptr_t)ctx->stream, (uintptr_t)ws.agg.p, ws.agg.bytes,
-                                (uintptr_t)ws.meta.p, (uintptr_t)ws.tables.p, ws.tables.bytes,
-                                (uintptr_t)ws.result.p, ws.result.bytes, (uintptr_t)ws.host.p, ws.host.bytes};
-  for (int j = 0; j < kMaxJoins; ++j) {
-    sig.push_back((uintptr_t)ws.slots[j].p);
-    sig.push_back((uintptr_t)ws.compact[j].p);
-  }
+static void db_signature(const crys_db* db, std::vector<uintptr_t>& sig) {
+  sig.push_back((uintptr_t)db->uid);
   for (const auto& kv : db->cols) {
     sig.push_back((uintptr_t)kv.second.buf->p);
     sig.push_back((uintptr_t)kv.second.rows);
@@ -946,88 +1218,105 @@ static std::vector<uintptr_t> query_signature(crys_ctx* ctx, const crys_db* db) 
   }
   sig.push_back((uintptr_t)db->lo_begin);
   sig.push_back((uintptr_t)db->lo_end);
+}
+
+static std::vector<uintptr_t> query_signature(crys_ctx* ctx, const std::vector<const crys_db*>& dbs) {
+  QueryWorkspace& ws = ws_of(ctx);
+  std::vector<uintptr_t> sig = {(uintptr_t)ctx->stream, (uintptr_t)ws.agg.p, ws.agg.bytes,
+                                (uintptr_t)ws.meta.p, (uintptr_t)ws.tables.p, ws.tables.bytes,
+                                (uintptr_t)ws.result.p, ws.result.bytes, (uintptr_t)ws.host.p, ws.host.bytes,
+                                (uintptr_t)ws.packed.p, ws.packed.bytes, (uintptr_t)ws.hbox};
+  for (int j = 0; j < kMaxJoins; ++j) {
+    sig.push_back((uintptr_t)ws.slots[j].p);
+    sig.push_back((uintptr_t)ws.compact[j].p);
+  }
+  for (const crys_db* db : dbs) db_signature(db, sig);
   return sig;
 }
 
-void ssb_run_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt, ResultRows* out) {
+static bool any_pending(const std::vector<const crys_db*>& dbs) {
+  bool pending = false;
+  for (const crys_db* db : dbs)
+    for (const auto& kv : db->cols) pending = pending || kv.second.pending;
+  return pending;
+}
+
+// after the host part (stream synchronised): pick the fastest candidate
+static void tune_done(crys_ctx* ctx) {
+  QueryWorkspace& ws = ws_of(ctx);
+  PipeTune* tn = ws.measuring;
+  ws.measuring = nullptr;
+  if (!tn || !tn->in_flight) return;
+  tn->in_flight = false;
+  float best = 1e30f;
+  for (int k = 0; k < tn->ncand; ++k) {
+    float ms = 0;
+    CUDA_TRY(cudaEventElapsedTime(&ms, tn->e0[k], tn->e1[k]));
+    if (ms < best) {
+      best = ms;
+      tn->chosen = k;
+    }
+  }
+}
+
+static bool still_tuning(crys_ctx* ctx, const crys_db* dimdb, int qid) {
   const QueryPlan& plan = plan_for(qid);
   QueryWorkspace& ws = ws_of(ctx);
-  const int64_t cells = plan.cells();
-  CRYS_CHECK(bt > 0 && ipt > 0, CRYS_ECONFIG, "TileConfig: block_threads/items_per_thread must be positive");
-  ws.agg.reserve(sizeof(unsigned long long) * (2 * (size_t)cells + 5));
-  finalize_reserve(ctx, cells);
-  auto* agg = ws.agg.as<unsigned long long>();
-  auto* surv = agg + 2 * cells;
-  auto* err = reinterpret_cast<int32_t*>(surv + 4);
-  auto enqueue = [&] {
-    ws.measuring = nullptr;
-    enqueue_query(ctx, db, qid, bt, ipt, agg, surv, err, ws.result.as<unsigned long long>(),
-                  sizeof(ResultHeader) / 8, true, true);
-    finalize_enqueue(ctx, qid, agg, surv, err, true);
-  };
-  // after the host part (stream synchronised): pick the fastest candidate
-  auto tune_done = [&] {
-    PipeTune* tn = ws.measuring;
-    ws.measuring = nullptr;
-    if (!tn || !tn->in_flight) return;
-    tn->in_flight = false;
-    float best = 1e30f;
-    for (int k = 0; k < tn->ncand; ++k) {
-      float ms = 0;
-      CUDA_TRY(cudaEventElapsedTime(&ms, tn->e0[k], tn->e1[k]));
-      if (ms < best) {
-        best = ms;
-        tn->chosen = k;
-      }
-    }
-  };
-  bool pending = false;
-  for (const auto& kv : db->cols) pending = pending || kv.second.pending;
-  {  // still autotuning this (db, query): direct runs, no graph
-    auto it = ws.tune.find({db, qid});
-    const bool tunable = (plan.joins.size() == 3 || plan.joins.size() == 4) && tune_enabled() &&
-                         pipe_cfg() == 0 && l2_ahead() == 0;
-    if (tunable && (it == ws.tune.end() || it->second.chosen < 0)) pending = true;
-  }
-  // Graph replay: the launch sequence of a query is fixed for a given database
-  // and workspace, so after one direct run (which sizes every buffer) it is
-  // captured once and then replayed with ONE launch.  Not with per-query
-  // timing (events) or columns still in flight from an async upload.
-  if (!graphs_enabled() || ctx->timing || pending) {
+  const bool tunable = (plan.joins.size() == 3 || plan.joins.size() == 4) && tune_enabled() &&
+                       pipe_cfg() == 0 && l2_ahead() == 0;
+  if (!tunable) return false;
+  auto it = ws.tune.find({dimdb->uid, qid});
+  return it == ws.tune.end() || it->second.chosen < 0;
+}
+
+// Runs `enqueue` (stream work only) either directly or through a CUDA graph
+// keyed by `key`: the launch sequence of a query is fixed for a given database
+// and workspace, so after one direct run (which sizes every buffer) it is
+// captured once and then replayed with ONE launch.  Not with per-query timing
+// (events), columns still in flight from an async upload, or while the
+// pipeline is being autotuned.  Graphs run on the context's own graph stream,
+// fenced after the caller's earlier work; the caller's stream is fenced after
+// them again when the scope ends.  `after` (host work that waits on the
+// stream, e.g. the result copy) runs inside the scope.
+template <class Enq, class After>
+static void run_sequence(crys_ctx* ctx, SeqKey key, const std::vector<const crys_db*>& dbs, bool direct,
+                         Enq&& enqueue, After&& after) {
+  QueryWorkspace& ws = ws_of(ctx);
+  if (!graphs_enabled() || ctx->timing || direct || any_pending(dbs)) {
     timing_begin(ctx);
     enqueue();
-    finalize_host_part(ctx, qid, out);
-    tune_done();
+    after();
     timing_end(ctx);
     return;
   }
-  QueryGraph& g = ws.graphs[{db, qid}];
-  // Graphs are captured and replayed on the context's own (non-blocking)
-  // stream -- the caller's stream may be the legacy default stream, which
-  // cannot be captured -- ordered after the caller's earlier work by an event.
-  struct StreamSwap {
-    crys_ctx* c;
-    cudaStream_t saved;
-    ~StreamSwap() { c->stream = saved; }
-  };
+  QueryGraph& g = ws.graphs[key];
   if (!ctx->graph_stream) {
     CUDA_TRY(cudaStreamCreateWithFlags(&ctx->graph_stream, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(&ctx->graph_fence, cudaEventDisableTiming));
   }
+  struct StreamSwap {
+    crys_ctx* c;
+    cudaStream_t saved;
+    ~StreamSwap() {
+      // the caller's later work orders after everything this scope enqueued
+      cudaEventRecord(c->graph_fence, c->stream);
+      c->stream = saved;
+      cudaStreamWaitEvent(saved, c->graph_fence, 0);
+    }
+  };
   CUDA_TRY(cudaEventRecord(ctx->graph_fence, ctx->stream));
   CUDA_TRY(cudaStreamWaitEvent(ctx->graph_stream, ctx->graph_fence, 0));
   StreamSwap swap{ctx, ctx->stream};
   ctx->stream = ctx->graph_stream;
-  const std::vector<uintptr_t> sig = query_signature(ctx, db);
+  const std::vector<uintptr_t> sig = query_signature(ctx, dbs);
   if (g.sig != sig) {  // first run (or a changed layout): direct, then remember the layout
     if (g.exec) {
       cudaGraphExecDestroy(g.exec);
       g.exec = nullptr;
     }
     enqueue();
-    finalize_host_part(ctx, qid, out);
-    tune_done();
-    g.sig = query_signature(ctx, db);
+    after();
+    g.sig = query_signature(ctx, dbs);
     return;
   }
   if (!g.exec) {
@@ -1049,7 +1338,139 @@ void ssb_run_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt, R
   }
   CUDA_TRY(cudaGraphLaunch(g.exec, ctx->stream));
   ctx->launches += g.kernels;
-  finalize_host_part(ctx, qid, out);
+  after();
+}
+
+void ssb_run_query(crys_ctx* ctx, const crys_db* db, int qid, int bt, int ipt, ResultRows* out) {
+  const QueryPlan& plan = plan_for(qid);
+  QueryWorkspace& ws = ws_of(ctx);
+  const int64_t cells = plan.cells();
+  CRYS_CHECK(bt > 0 && ipt > 0, CRYS_ECONFIG, "TileConfig: block_threads/items_per_thread must be positive");
+  ws.agg.reserve(sizeof(unsigned long long) * (2 * (size_t)cells + 5));
+  finalize_reserve(ctx, cells);
+  auto* agg = ws.agg.as<unsigned long long>();
+  auto* surv = agg + 2 * cells;
+  auto* err = reinterpret_cast<int32_t*>(surv + 4);
+  const std::vector<const crys_db*> dbs = {db};
+  const BoxPlan bp = box_plan(plan, kBoxMeta);
+  auto enqueue = [&] {
+    ws.measuring = nullptr;
+    enqueue_query(ctx, db, dbs, qid, bt, ipt, agg, surv, err, ws.result.as<unsigned long long>(),
+                  sizeof(ResultHeader) / 8, true, true, nullptr);
+    finalize_enqueue(ctx, qid, agg, agg + cells, bp, false, surv, err, nullptr, true);
+  };
+  auto after = [&] {
+    finalize_host_part(ctx, qid, out);
+    tune_done(ctx);
+  };
+  run_sequence(ctx, SeqKey{db->uid, qid, kSeqQuery}, dbs, still_tuning(ctx, db, qid), enqueue, after);
+}
+
+// ---------------------------------------------------------- packed partials
+
+// Host view of the box published by box_publish_kernel.
+static crys_group_box host_box(const QueryPlan& plan, const HostBox* hb) {
+  crys_group_box b;
+  std::memset(&b, 0, sizeof(b));
+  b.nparts = (int32_t)plan.group.size();
+  b.cells = 1;
+  for (int g = 0; g < b.nparts; ++g) {
+    const GroupPart& gp = plan.group[g];
+    const int32_t full = gp.hi - gp.lo + 1;
+    const int32_t lo = std::max(0, hb->dmin[gp.join_index]);
+    const int32_t hi = std::min(full - 1, hb->dmax[gp.join_index]);
+    b.lo[g] = gp.lo + lo;
+    b.card[g] = hi >= lo ? hi - lo + 1 : 0;
+    b.cells *= b.card[g];
+  }
+  return b;
+}
+
+static HostBox* host_box_buffer(QueryWorkspace& ws) {
+  if (!ws.hbox) {
+    void* p = nullptr;
+    CUDA_TRY(cudaHostAlloc(&p, sizeof(HostBox), cudaHostAllocMapped | cudaHostAllocPortable));
+    ws.hbox = static_cast<HostBox*>(p);
+    std::memset(p, 0, sizeof(HostBox));
+  }
+  return ws.hbox;
+}
+
+// Waits for box_publish_kernel (spin on host-mapped memory; the stream keeps
+// running the fused pass meanwhile).
+static void wait_box(crys_ctx* ctx, HostBox* hb) {
+  for (uint64_t spins = 0; hb->ready == 0; ++spins) {
+    if ((spins & 1023) == 1023) {
+      const cudaError_t e = cudaStreamQuery(ctx->stream);
+      if (e != cudaSuccess && e != cudaErrorNotReady)
+        fail(CRYS_ECUDA, std::string("waiting for the dimension builds: ") + cudaGetErrorString(e));
+      if (e == cudaSuccess && hb->ready == 0) fail(CRYS_ECUDA, "dimension builds finished without a box");
+    }
+  }
+}
+
+// One shard group's partial on this device (dimensions from facts[0]):
+// prologue + builds + box publish + fused passes over every fact shard +
+// pack into d_out (capacity `cap` int64).  Returns with *box / *len set while
+// the fused pass may still run.  Graph-replayed like a query.
+void ssb_partial_box(crys_ctx* ctx, const std::vector<const crys_db*>& facts, int qid, int bt, int ipt,
+                     long long* d_out, int64_t cap, crys_group_box* box, int64_t* len, bool defer_tune) {
+  const QueryPlan& plan = plan_for(qid);
+  QueryWorkspace& ws = ws_of(ctx);
+  const int64_t cells = plan.cells();
+  const int nj = (int)plan.joins.size();
+  CRYS_CHECK(bt > 0 && ipt > 0, CRYS_ECONFIG, "TileConfig: block_threads/items_per_thread must be positive");
+  CRYS_CHECK(d_out != nullptr, CRYS_ECONFIG, "null partial buffer");
+  ws.agg.reserve(sizeof(unsigned long long) * (2 * (size_t)cells + 5));
+  ws.meta.reserve(sizeof(HtMeta) * kMaxJoins);
+  HostBox* hb = nj ? host_box_buffer(ws) : nullptr;
+  auto* agg = ws.agg.as<unsigned long long>();
+  auto* surv = agg + 2 * cells;
+  auto* err = reinterpret_cast<int32_t*>(surv + 4);
+  const BoxPlan bp = box_plan(plan, kBoxMeta);
+  if (hb) hb->ready = 0;
+  auto enqueue = [&] {
+    ws.measuring = nullptr;
+    enqueue_query(ctx, facts[0], facts, qid, bt, ipt, agg, surv, err, nullptr, 0, true, true, hb);
+    const int tpb = 256;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((cells + tpb - 1) / tpb, (int64_t)ctx->num_sms * 8));
+    pack_partial_kernel<<<grid, tpb, 0, ctx->stream>>>(agg, agg + cells, bp, ws.meta.as<HtMeta>(), nj, surv,
+                                                       err, d_out, cap);
+    CRYS_LAUNCHED("pack_partial_kernel");
+    count_launch(ctx);
+  };
+  auto after = [&] {
+    if (hb) {
+      wait_box(ctx, hb);
+      *box = host_box(plan, hb);
+    } else {
+      std::memset(box, 0, sizeof(*box));
+      box->cells = 1;
+    }
+    *len = CRYS_PARTIAL_HEADER + 2 * box->cells;
+    CRYS_CHECK(*len <= cap, CRYS_ECONTRACT,
+               "partial buffer too small: need " + std::to_string(*len) + " int64");
+    if (!defer_tune) {
+      if (ws.measuring) CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+      tune_done(ctx);
+    }
+  };
+  std::vector<const crys_db*> dbs(facts.begin(), facts.end());
+  run_sequence(ctx, SeqKey{facts[0]->uid, qid, kSeqPartial}, dbs, still_tuning(ctx, facts[0], qid), enqueue,
+               after);
+}
+
+void ssb_tune_done(crys_ctx* ctx) {
+  if (ctx->qws && ctx->qws->measuring) {
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    tune_done(ctx);
+  }
+}
+
+long long* ssb_group_buffer(crys_ctx* ctx, int64_t n) {
+  QueryWorkspace& ws = ws_of(ctx);
+  ws.packed.reserve(sizeof(long long) * (size_t)n);
+  return ws.packed.as<long long>();
 }
 
 }  // namespace crys

@@ -19,6 +19,7 @@ from typing import Optional, Tuple
 import numpy as np
 
 from . import tq
+from . import _lib
 from ._lib import LIB
 
 
@@ -33,43 +34,132 @@ def lineorder_rows(sf: int) -> int:
     return 6_000_000 * sf  # ssb_gen.cpp:179
 
 
-def agg_buffer_len(qid) -> int:
+HEADER = _lib.CRYS_PARTIAL_HEADER
+
+
+def dense_buffer_len(qid) -> int:
+    """Dense partial: [sums[cells] | counts[cells] | header[CRYS_PARTIAL_HEADER]]."""
     cells, _, _ = tq.query_shape(qid)
-    return 2 * cells + 4
+    return 2 * cells + HEADER
 
 
-def reduce_and_finalize(buf, qid, dst: int = 0, group=None) -> Optional[tq.QueryResult]:
-    """One collective: SUM-reduce the [sums|counts|survivors] buffer to `dst`,
-    then compact there (device kernel for CUDA tensors, host otherwise)."""
+agg_buffer_len = dense_buffer_len
+
+
+def _global_rank(group, r: int) -> int:
+    import torch.distributed as dist
+    return r if group is None else dist.get_global_rank(group, r)
+
+
+def _box_from(box) -> "_lib.crys_group_box":
+    if isinstance(box, _lib.crys_group_box):
+        return box
+    b = _lib.crys_group_box()
+    b.nparts = len(box["lo"])
+    for g, (lo, card) in enumerate(zip(box["lo"], box["card"])):
+        b.lo[g], b.card[g] = lo, card
+    b.cells = int(np.prod(box["card"], dtype=np.int64)) if box["lo"] else 1
+    return b
+
+
+def expand_packed_host(qid, box, packed: np.ndarray):
+    """A packed partial [header | box sums | box counts] -> (dense [sums |
+    counts], header) on the host (the mixed-radix box -> full cell map of
+    crystal_b200.h; last group part fastest)."""
+    box = _box_from(box)
+    cells, ng, _ = tq.query_shape(qid)
+    labels = tq._GROUP_LABELS[int(qid)]
+    packed = np.asarray(packed, np.int64)
+    n = int(box.cells)
+    hdr = packed[:HEADER].copy()
+    dense = np.zeros(2 * cells, np.int64)
+    if n:
+        # full strides and group lows of the plan's parts
+        lo_full, card_full = _GROUP_DOMAINS[int(qid)]
+        idx = np.arange(n, dtype=np.int64)
+        full = np.zeros(n, np.int64)
+        stride = 1
+        fstride = [0] * ng
+        for g in range(ng - 1, -1, -1):
+            fstride[g] = stride
+            stride *= card_full[g]
+        rem = idx.copy()
+        for g in range(ng - 1, -1, -1):
+            d = rem % box.card[g]
+            rem //= box.card[g]
+            full += (box.lo[g] - lo_full[g] + d) * fstride[g]
+        dense[full] = packed[HEADER:HEADER + n]
+        dense[cells + full] = packed[HEADER + n:HEADER + 2 * n]
+    assert len(labels) == ng
+    return dense, hdr
+
+
+# group-part domains (lo, cardinality) per plan (ssb_plans.cpp:110-275)
+_GROUP_DOMAINS = {
+    0: ([], []), 1: ([], []), 2: ([], []),
+    3: ([1992, 0], [7, 1000]), 4: ([1992, 0], [7, 1000]), 5: ([1992, 0], [7, 1000]),
+    6: ([0, 0, 1992], [25, 25, 7]), 7: ([0, 0, 1992], [250, 250, 7]),
+    8: ([0, 0, 1992], [250, 250, 7]), 9: ([0, 0, 1992], [250, 250, 7]),
+    10: ([1992, 0], [7, 25]), 11: ([1992, 0, 0], [7, 25, 25]),
+    12: ([1992, 0, 0], [7, 250, 1000]),
+}
+
+
+def reduce_and_finalize(buf, qid, dst: int = 0, group=None, box=None) -> Optional[tq.QueryResult]:
+    """One collective: SUM-reduce this rank's partial to group rank `dst`,
+    then compact there (device kernels for CUDA tensors, host otherwise).
+
+    ``box`` given: ``buf`` is a PACKED partial [header | box sums | box
+    counts] (crys_query_partial_box; every rank has the same box because the
+    dimensions are replicated).  Otherwise ``buf`` is the dense form [sums |
+    counts | header].  The header's build / group-domain errors raise the
+    reference's exceptions on `dst` (BuildError / ContractError)."""
     import torch
     import torch.distributed as dist
-    dist.reduce(buf, dst=dst, op=dist.ReduceOp.SUM, group=group)
+    dist.reduce(buf, dst=_global_rank(group, dst), op=dist.ReduceOp.SUM, group=group)
     if dist.get_rank(group) != dst:
         return None
-    cells, _, nj = tq.query_shape(qid)
     if buf.is_cuda:
-        torch.cuda.current_stream(buf.device).synchronize()
         ctx = tq.Context.default(buf.device.index)
-        ctx.bind_torch_stream()
-        maxr = max(cells, 1)
-        groups = np.zeros(3 * maxr, np.int32)
-        sums = np.zeros(maxr, np.int64)
-        n = C.c_int64()
-        tq.check(LIB.crys_query_finalize(ctx.h, int(qid), C.c_void_p(buf.data_ptr()),
-                                         groups.ctypes.data_as(C.c_void_p),
-                                         sums.ctypes.data_as(C.c_void_p), maxr, C.byref(n)))
-        res = tq._rows_from_buffers(qid, groups, sums, n.value)
-        surv = buf[2 * cells:2 * cells + 4].cpu().numpy()
+        return finalize_device(buf, qid, ctx, box)
+    host = buf.numpy()
+    cells, _, _ = tq.query_shape(qid)
+    if box is not None:
+        dense, hdr = expand_packed_host(qid, box, host)
+        return tq.finalize_host(qid, dense, hdr)
+    return tq.finalize_host(qid, host[:2 * cells], host[2 * cells:2 * cells + HEADER])
+
+
+def finalize_device(buf, qid, ctx: tq.Context, box=None) -> tq.QueryResult:
+    """Compact a (reduced) partial on the device: packed when ``box`` is given
+    (crys_query_finalize_box), else dense [sums | counts | header]
+    (crys_query_finalize)."""
+    cells, _, nj = tq.query_shape(qid)
+    maxr = max(cells, 1)
+    groups = np.zeros(3 * maxr, np.int32)
+    sums = np.zeros(maxr, np.int64)
+    surv = np.zeros(4, np.int64)
+    n = C.c_int64()
+    ctx.bind_torch_stream()
+    if box is not None:
+        b = _box_from(box)
+        tq.check(LIB.crys_query_finalize_box(ctx.h, int(qid), C.byref(b), C.c_void_p(buf.data_ptr()),
+                                             groups.ctypes.data_as(C.c_void_p), sums.ctypes.data_as(C.c_void_p),
+                                             maxr, C.byref(n), surv.ctypes.data_as(C.c_void_p)))
     else:
-        host = buf.numpy()
-        res = tq.finalize_host(qid, host[:2 * cells])
-        surv = host[2 * cells:2 * cells + 4]
+        tq.check(LIB.crys_query_finalize(ctx.h, int(qid), C.c_void_p(buf.data_ptr()),
+                                         C.c_void_p(buf.data_ptr() + 8 * 2 * cells),
+                                         groups.ctypes.data_as(C.c_void_p), sums.ctypes.data_as(C.c_void_p),
+                                         maxr, C.byref(n), surv.ctypes.data_as(C.c_void_p)))
+    res = tq._rows_from_buffers(qid, groups, sums, n.value)
     res.survivors = [int(x) for x in surv[:max(nj, 1)]]
     return res
 
 
 class ShardedSSB:
-    """This rank's shard of an SSB database in HBM plus the query driver."""
+    """This rank's shard of an SSB database in HBM plus the query driver
+    (one process per GPU; the in-library alternative with one host thread
+    driving every GPU is ``tq.Context.group``)."""
 
     def __init__(self, sf: int, seed: int = 42, group=None, device: Optional[int] = None):
         import torch
@@ -103,16 +193,36 @@ class ShardedSSB:
         self._bufs = {}
         return self
 
+    def _buffer(self, qid, n):
+        import torch
+        buf = self._bufs.get(qid)
+        if buf is None or buf.numel() < n:
+            buf = self._bufs[qid] = torch.empty(n, dtype=torch.int64, device=f"cuda:{self.device}")
+        return buf
+
     def partial(self, qid, config: tq.TileConfig = tq.TileConfig()):
-        """This shard's dense partial aggregate (async on torch's current stream)."""
+        """This shard's PACKED partial (async on torch's current stream) and
+        its group box: (buffer view of CRYS_PARTIAL_HEADER + 2*box.cells
+        int64, crys_group_box).  Returns once the dimension builds fixed the
+        box; the fused pass is still in flight."""
+        qid = int(qid)
+        cells, _, _ = tq.query_shape(qid)
+        cap = HEADER + 2 * cells
+        buf = self._buffer(qid, cap)
+        self.ctx.bind_torch_stream()
+        n = C.c_int64()
+        box = _lib.crys_group_box()
+        tq.check(LIB.crys_query_partial_box(self.ctx.h, self.db.h, qid, config.block_threads,
+                                            config.items_per_thread, C.c_void_p(buf.data_ptr()), cap,
+                                            C.byref(n), C.byref(box)))
+        return buf[:n.value], box
+
+    def partial_dense(self, qid, config: tq.TileConfig = tq.TileConfig()):
+        """This shard's DENSE partial [sums | counts | header] (crys_query_partial)."""
         import torch
         qid = int(qid)
         cells, _, _ = tq.query_shape(qid)
-        buf = self._bufs.get(qid)
-        if buf is None:
-            buf = self._bufs[qid] = torch.empty(2 * cells + 4, dtype=torch.int64,
-                                                device=f"cuda:{self.device}")
-        buf.zero_()
+        buf = torch.zeros(2 * cells + HEADER, dtype=torch.int64, device=f"cuda:{self.device}")
         self.ctx.bind_torch_stream()
         tq.check(LIB.crys_query_partial(self.ctx.h, self.db.h, qid, config.block_threads,
                                         config.items_per_thread, C.c_void_p(buf.data_ptr()),
@@ -121,28 +231,15 @@ class ShardedSSB:
 
     def run_query(self, qid, config: tq.TileConfig = tq.TileConfig()) -> Optional[tq.QueryResult]:
         """Every rank scans its shard; rank 0 returns the merged result."""
-        buf = self.partial(qid, config)
+        buf, box = self.partial(qid, config)
         if self.world == 1:
-            return reduce_local(buf, qid, self.ctx)
-        return reduce_and_finalize(buf, qid, 0, self.group)
+            return finalize_device(buf, qid, self.ctx, box)
+        return reduce_and_finalize(buf, qid, 0, self.group, box)
 
 
 def reduce_local(buf, qid, ctx: tq.Context) -> tq.QueryResult:
-    """World size 1: compact on the device without a collective."""
-    import torch
-    cells, _, nj = tq.query_shape(qid)
-    maxr = max(cells, 1)
-    groups = np.zeros(3 * maxr, np.int32)
-    sums = np.zeros(maxr, np.int64)
-    n = C.c_int64()
-    ctx.bind_torch_stream()
-    tq.check(LIB.crys_query_finalize(ctx.h, int(qid), C.c_void_p(buf.data_ptr()),
-                                     groups.ctypes.data_as(C.c_void_p),
-                                     sums.ctypes.data_as(C.c_void_p), maxr, C.byref(n)))
-    res = tq._rows_from_buffers(qid, groups, sums, n.value)
-    torch.cuda.current_stream(buf.device).synchronize()
-    res.survivors = [int(x) for x in buf[2 * cells:2 * cells + 4].cpu().numpy()[:max(nj, 1)]]
-    return res
+    """World size 1, dense form [sums | counts | header]: compact on the device."""
+    return finalize_device(buf, qid, ctx, None)
 
 
 # ----------------------------------------------------------------- sharded sort

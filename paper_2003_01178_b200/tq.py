@@ -60,9 +60,13 @@ class NotBuiltError(RuntimeError):
     """The requested kernel shape is not compiled for sm_100a."""
 
 
+class NcclError(RuntimeError):
+    """NCCL missing or failed (device groups; no reference analogue)."""
+
+
 _ERRORS = {_lib.CRYS_ECONFIG: ConfigError, _lib.CRYS_ECONTRACT: ContractError,
            _lib.CRYS_EBUILD: BuildError, _lib.CRYS_EIO: IoError, _lib.CRYS_ECUDA: CudaError,
-           _lib.CRYS_ENOTBUILT: NotBuiltError}
+           _lib.CRYS_ENOTBUILT: NotBuiltError, _lib.CRYS_ENCCL: NcclError}
 
 
 def check(status: int) -> None:
@@ -157,24 +161,52 @@ class PredicateSpec:
 
 class Context:
     """One CUDA device + stream + scratch (replaces the per-call thread pool of
-    parallel_for_blocks, kernel.cpp:60-103).  One context per host thread."""
+    parallel_for_blocks, kernel.cpp:60-103).  A context is not thread-safe:
+    ``Context.default`` hands every host thread its own context per device.
 
-    _default: Dict[int, "Context"] = {}
+    ``Context.group(devices)`` is a DEVICE GROUP (crys_init_group): one
+    lineorder shard per entry of ``devices`` (an ordinal may repeat: several
+    shards on one GPU), dimensions replicated per device, and each query merged
+    by ONE NCCL reduce inside the library -- the reference's ``workers``
+    fan-out driven from one host thread."""
 
-    def __init__(self, device: int = 0):
+    _default = threading.local()
+
+    def __init__(self, device: int = 0, _handle=None):
         self.device = device
-        h = C.c_void_p()
-        check(LIB.crys_init(device, C.byref(h)))
-        self.h = h
+        if _handle is None:
+            h = C.c_void_p()
+            check(LIB.crys_init(device, C.byref(h)))
+            _handle = h
+        self.h = _handle
 
     @classmethod
     def default(cls, device: Optional[int] = None) -> "Context":
         if device is None:
             import torch
             device = torch.cuda.current_device()
-        if device not in cls._default:
-            cls._default[device] = Context(device)
-        return cls._default[device]
+        per_thread = getattr(cls._default, "ctxs", None)
+        if per_thread is None:
+            per_thread = cls._default.ctxs = {}
+        if device not in per_thread:
+            per_thread[device] = Context(device)
+        return per_thread[device]
+
+    @classmethod
+    def group(cls, devices: Sequence[int]) -> "Context":
+        devs = (C.c_int32 * len(devices))(*[int(d) for d in devices])
+        h = C.c_void_p()
+        check(LIB.crys_init_group(len(devices), devs, C.byref(h)))
+        return cls(int(devices[0]), h)
+
+    def shards(self) -> int:
+        return LIB.crys_group_shards(self.h)
+
+    def devices(self) -> int:
+        return LIB.crys_group_devices(self.h)
+
+    def uses_nccl(self) -> bool:
+        return bool(LIB.crys_group_uses_nccl(self.h))
 
     def bind_torch_stream(self) -> None:
         """Run subsequent calls on torch's current stream (ordering with torch ops)."""
@@ -583,21 +615,33 @@ def run_query(db, qid, config: TileConfig = TileConfig(), workers: int = 1,
     return _rows_from_buffers(qid, groups, sums, n.value)
 
 
-def finalize_host(qid, agg: np.ndarray) -> QueryResult:
-    """Dense [sums | counts] int64 aggregate -> QueryResult, on the host."""
+def finalize_host(qid, agg: np.ndarray, header: Optional[np.ndarray] = None) -> QueryResult:
+    """Dense [sums | counts] int64 aggregate -> QueryResult, on the host.
+    ``header`` (int64[CRYS_PARTIAL_HEADER], a reduced partial header) supplies
+    the survivors and raises the build / group-domain errors it carries."""
     qid = int(qid)
-    cells, _, _ = query_shape(qid)
+    cells, _, nj = query_shape(qid)
     agg = np.ascontiguousarray(agg, dtype=np.int64)
     if agg.size != 2 * cells:
         raise ContractError("aggregate buffer has the wrong shape")
+    hp = None
+    if header is not None:
+        header = np.ascontiguousarray(header, dtype=np.int64)
+        if header.size != _lib.CRYS_PARTIAL_HEADER:
+            raise ContractError("partial header has the wrong shape")
+        hp = header.ctypes.data_as(C.c_void_p)
     maxr = max(cells, 1)
     groups = np.zeros(3 * maxr, np.int32)
     sums = np.zeros(maxr, np.int64)
+    surv = np.zeros(4, np.int64)
     n = C.c_int64()
-    check(LIB.crys_query_finalize_host(qid, agg.ctypes.data_as(C.c_void_p),
+    check(LIB.crys_query_finalize_host(qid, agg.ctypes.data_as(C.c_void_p), hp,
                                        groups.ctypes.data_as(C.c_void_p),
-                                       sums.ctypes.data_as(C.c_void_p), maxr, C.byref(n)))
-    return _rows_from_buffers(qid, groups, sums, n.value)
+                                       sums.ctypes.data_as(C.c_void_p), maxr, C.byref(n),
+                                       surv.ctypes.data_as(C.c_void_p)))
+    res = _rows_from_buffers(qid, groups, sums, n.value)
+    res.survivors = [int(x) for x in surv[:max(nj, 1)]]
+    return res
 
 
 # ----------------------------------------------------------------- spans

@@ -1,7 +1,9 @@
 """Multi-rank host path on CPU (gloo, world_size 2): row-range shards, one
-SUM reduce of the [sums|counts|survivors] buffer, rank-0 compaction by the
-product code.  Per-shard partials come from the oracle here (no GPU); on the
-box the same buffer is produced by crys_query_partial."""
+SUM reduce of the partial buffer (dense [sums|counts|header] and packed
+[header|box sums|box counts]), rank-0 compaction by the product code, and the
+build / group-domain errors of any shard surfacing on rank 0.  Per-shard
+partials come from the oracle here (no GPU); on the box the same buffers are
+produced by crys_query_partial / crys_query_partial_box."""
 import os
 import socket
 
@@ -35,19 +37,71 @@ def _worker(rank, world, port, queries, out):
         db = orc.generate(1, 42, lo_begin=lo, lo_end=hi, nthreads=2)
         n = hi - lo
         res = {}
+        H = cdist.HEADER
         for q in queries:
             s, c, v = orc.partial(db, q, 0, n)
-            buf = torch.from_numpy(np.concatenate([s, c, v]).astype(np.int64))
-            assert buf.numel() == cdist.agg_buffer_len(q)
+            hdr = np.zeros(H, np.int64)
+            hdr[:4] = v
+            buf = torch.from_numpy(np.concatenate([s, c, hdr]).astype(np.int64))
+            assert buf.numel() == cdist.dense_buffer_len(q)
             r = cdist.reduce_and_finalize(buf, q)
+            # packed form over a sub-box that holds every occupied cell
+            lo, card = cdist._GROUP_DOMAINS[q]
+            box = {"lo": list(lo), "card": list(card)}
+            if q == 12:  # q4.3: years 1997-1998 only (d_year filter), the whole domain otherwise
+                box = {"lo": [1997, 0, 0], "card": [2, 250, 1000]}
+            pk = _pack(q, box, s, c, hdr)
+            r2 = cdist.reduce_and_finalize(torch.from_numpy(pk), q, box=box)
             if rank == 0:
-                res[q] = (r.as_tuples(), r.survivors)
+                res[q] = (r.as_tuples(), r.survivors, r2.as_tuples(), r2.survivors)
             else:
-                assert r is None
+                assert r is None and r2 is None
+        # a build error on ONE shard (duplicate key in join 1) surfaces on rank 0
+        q = 3
+        s, c, v = orc.partial(db, q, 0, n)
+        hdr = np.zeros(H, np.int64)
+        if rank == 1:
+            hdr[8 + 4 * 1 + (2 - 1)] = 1
+        buf = torch.from_numpy(np.concatenate([s, c, hdr]).astype(np.int64))
+        try:
+            cdist.reduce_and_finalize(buf, q)
+            err1 = None
+        except tq.BuildError as e:
+            err1 = str(e)
+        hdr = np.zeros(H, np.int64)
+        if rank == 1:
+            hdr[4] = 1  # a row reached the aggregate with a group value outside its domain
+        buf = torch.from_numpy(np.concatenate([s, c, hdr]).astype(np.int64))
+        try:
+            cdist.reduce_and_finalize(buf, q)
+            err2 = None
+        except tq.ContractError as e:
+            err2 = str(e)
         if rank == 0:
+            res["errors"] = (err1, err2)
             out.put(res)
     finally:
         dist.destroy_process_group()
+
+
+def _pack(q, box, s, c, hdr):
+    """Host restatement of pack_partial_kernel: the box cells of a dense partial."""
+    from paper_2003_01178_b200 import dist as cdist
+    lo_full, card_full = cdist._GROUP_DOMAINS[q]
+    ng = len(lo_full)
+    fstride, st = [0] * ng, 1
+    for g in range(ng - 1, -1, -1):
+        fstride[g] = st
+        st *= card_full[g]
+    n = int(np.prod(box["card"], dtype=np.int64)) if ng else 1
+    full = np.zeros(n, np.int64)
+    rem = np.arange(n, dtype=np.int64)
+    for g in range(ng - 1, -1, -1):
+        d = rem % box["card"][g]
+        rem //= box["card"][g]
+        full += (box["lo"][g] - lo_full[g] + d) * fstride[g]
+    assert c.sum() == c[full].sum(), "the box must hold every occupied cell"
+    return np.concatenate([hdr, s[full], c[full]]).astype(np.int64)
 
 
 @pytest.mark.parametrize("world", [2])
@@ -65,9 +119,13 @@ def test_sharded_ssb_gloo(world):
         assert p.exitcode == 0
     for qid in queries:
         rec = golden("sf1")["queries"][QUERY_NAMES[qid]]
-        rows, surv = res[qid]
+        rows, surv, rows2, surv2 = res[qid]
         assert rows == golden_rows(rec)
         assert surv == rec["survivors"]
+        assert rows2 == golden_rows(rec) and surv2 == rec["survivors"]
+    err1, err2 = res["errors"]
+    assert err1 is not None and "duplicate key" in err1 and "join 1" in err1
+    assert err2 is not None and "outside its declared domain" in err2
 
 
 # ---------------------------------------------------------------- sharded sort

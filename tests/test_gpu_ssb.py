@@ -133,18 +133,29 @@ def test_ssb_sf1_vs_oracle_on_shard(tq):
     db = tq.DeviceDatabase.generate(1, 42, lo, hi)
     for c in ("lo_orderdate", "lo_revenue", "lo_partkey"):
         assert np.array_equal(db.download("lineorder", c), host["lineorder"][c])
-    sh = cdist.ShardedSSB.__new__(cdist.ShardedSSB)
-    sh.ctx, sh.db, sh.device, sh._bufs, sh.world = db.ctx, db, torch.cuda.current_device(), {}, 1
+    sh = cdist.ShardedSSB.over(db)
     for q in range(13):
         s, c, v = orc.partial(host, q, 0, hi - lo)
-        buf = sh.partial(q)
+        buf = sh.partial_dense(q)
         torch.cuda.synchronize()
         got = buf.cpu().numpy()
         cells = len(s)
         assert np.array_equal(got[:cells], s), QUERY_NAMES[q]
         assert np.array_equal(got[cells:2 * cells], c), QUERY_NAMES[q]
+        nj = max(1, tq.query_shape(q)[2])
+        assert np.array_equal(got[2 * cells:2 * cells + nj], v[:nj]), QUERY_NAMES[q]
+        assert not got[2 * cells + 4:].any(), QUERY_NAMES[q]  # no error words
         res = cdist.reduce_local(buf, q, db.ctx)
-        assert res.as_tuples() == orc.query(host, q)[0], QUERY_NAMES[q]
+        exp_rows, exp_surv = orc.query(host, q)
+        assert res.as_tuples() == exp_rows, QUERY_NAMES[q]
+        assert res.survivors == exp_surv, QUERY_NAMES[q]
+        # the packed partial (the NCCL payload): its box holds every row
+        pbuf, box = sh.partial(q)
+        dense, hdr = cdist.expand_packed_host(q, box, pbuf.cpu().numpy())
+        assert np.array_equal(dense[:cells], s) and np.array_equal(dense[cells:], c), QUERY_NAMES[q]
+        assert box.cells <= max(cells, 1)
+        res2 = cdist.finalize_device(pbuf, q, db.ctx, box)
+        assert res2.as_tuples() == exp_rows and res2.survivors == exp_surv, QUERY_NAMES[q]
     db.free()
 
 
@@ -234,27 +245,22 @@ def test_ssb_sf100_matches_reference(tq):
 
 @pytest.mark.slow
 def test_ssb_sf100_eight_shards_merged(tq):
-    """The 8-GPU decomposition of SF=100 run shard by shard on one GPU: each
-    row-range shard generated in HBM, its dense partial from the same kernel
-    the multi-GPU path uses (crys_query_partial), the eight partials summed
-    (what the NCCL reduce does) and compacted on the device."""
+    """The 8-GPU decomposition of SF=100 through the device-group entry point
+    (crys_init_group with eight shards placed on this one GPU: the emulation
+    of an 8 x B200 box): every shard generated in HBM, dimension tables built
+    once, the eight fused passes summed on the device, then the same packed
+    finalize the NCCL reduce feeds."""
     import torch
-    from paper_2003_01178_b200 import dist as cdist
-    world = 8
-    total = cdist.lineorder_rows(100)
-    acc = {}
-    for r in range(world):
-        lo, hi = cdist.shard_range(total, r, world)
-        db = tq.DeviceDatabase.generate(100, 42, lo, hi)
-        sh = cdist.ShardedSSB.over(db)
+    g = tq.Context.group([torch.cuda.current_device()] * 8)
+    assert g.shards() == 8 and g.devices() == 1
+    db = tq.DeviceDatabase.generate(100, 42, ctx=g)
+    try:
         for q in range(13):
-            buf = sh.partial(q)
-            acc[q] = buf.clone() if q not in acc else acc[q] + buf
-        torch.cuda.synchronize()
+            rec = golden("sf100")["queries"][QUERY_NAMES[q]]
+            st = tq.QueryStats()
+            res = tq.run_query(db, q, tq.TileConfig(), 8, st)
+            assert res.as_tuples() == golden_rows(rec), QUERY_NAMES[q]
+            assert st.survivors == rec["survivors"][:len(st.survivors)], QUERY_NAMES[q]
+    finally:
         db.free()
-    ctx = tq.Context.default(torch.cuda.current_device())
-    for q in range(13):
-        rec = golden("sf100")["queries"][QUERY_NAMES[q]]
-        res = cdist.reduce_local(acc[q], q, ctx)
-        assert res.as_tuples() == golden_rows(rec), QUERY_NAMES[q]
-        assert res.survivors == rec["survivors"][:len(res.survivors)], QUERY_NAMES[q]
+        g.close()

@@ -136,3 +136,17 @@ def test_shard_ranges_cover():
                 assert b == c and b >= a
             sizes = [b - a for a, b in r]
             assert max(sizes) - min(sizes) <= 1
+
+
+def test_nccl_loads_without_breaking_torch():
+    """Device groups dlopen NCCL lazily; the package points the library at the
+    libnccl torch ships, so loading it first must not break `import torch`
+    (a second, older libnccl.so.2 in the process would)."""
+    import subprocess
+    import sys
+    code = ("from paper_2003_01178_b200._lib import LIB; v = LIB.crys_nccl_version().decode(); "
+            "import torch; print(v)")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.strip().startswith("libnccl "), r.stdout
