@@ -15,11 +15,6 @@
 namespace tq::b200 {
 
 namespace {
-struct ThreadContext {
-  crys_ctx* ctx = nullptr;
-  std::map<int, crys_ctx*> groups;  // shard count -> group
-  ~ThreadContext();
-};
 
 int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
@@ -41,10 +36,39 @@ std::vector<int> visible_devices() {
   return devs;
 }
 
+}  // namespace
+
+// ------------------------------------------------------------ upload cache
+
+struct CacheEntry {
+  std::vector<uint64_t> sig;
+  crys_db* db = nullptr;
+};
+struct SsbDatabaseCache {
+  std::map<std::pair<const crys_ctx*, const void*>, CacheEntry> entries;
+  long long uploads = 0;
+};
+
+namespace {
+// Everything one host thread owns, torn down in dependency order: cached
+// databases before the groups / context they live on.
+struct ThreadContext {
+  crys_ctx* ctx = nullptr;
+  std::map<int, crys_ctx*> groups;  // shard count -> group
+  SsbDatabaseCache cache;
+  ~ThreadContext() {
+    for (auto& kv : cache.entries) crys_db_free(kv.second.db);
+    cache.entries.clear();
+    for (auto& kv : groups) crys_destroy(kv.second);
+    if (ctx) crys_destroy(ctx);
+  }
+};
+
 ThreadContext& tc() {
   thread_local ThreadContext t;
   return t;
 }
+SsbDatabaseCache& cache() { return tc().cache; }
 }  // namespace
 
 crys_ctx* context() {
@@ -67,35 +91,6 @@ crys_ctx* group_context(int workers) {
   check(crys_init_group(shards, place.data(), &g));
   t.groups[shards] = g;
   return g;
-}
-
-// ------------------------------------------------------------ upload cache
-
-struct CacheEntry {
-  std::vector<uint64_t> sig;
-  crys_db* db = nullptr;
-};
-struct SsbDatabaseCache {
-  std::map<std::pair<const crys_ctx*, const void*>, CacheEntry> entries;
-  long long uploads = 0;
-  ~SsbDatabaseCache() {
-    for (auto& kv : entries) crys_db_free(kv.second.db);
-  }
-};
-
-namespace {
-SsbDatabaseCache& cache() {
-  thread_local SsbDatabaseCache c;
-  return c;
-}
-}  // namespace
-
-ThreadContext::~ThreadContext() {
-  // databases before the contexts they live on
-  for (auto& kv : cache().entries) crys_db_free(kv.second.db);
-  cache().entries.clear();
-  for (auto& kv : groups) crys_destroy(kv.second);
-  if (ctx) crys_destroy(ctx);
 }
 
 void invalidate(const void* db) {

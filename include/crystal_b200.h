@@ -158,7 +158,11 @@ crys_status crys_db_save_column_file(const crys_db* db, const char* table, const
 /* Device pointer + rows of a column (borrowed; valid until the db is freed). */
 crys_status crys_db_column(const crys_db* db, const char* table, const char* column,
                            const int32_t** d_data, int64_t* rows);
-/* Copy a column back to the host (h_out must hold `rows` values). */
+/* Rows of a column (a device-group database: lineorder summed over its
+ * shards, a dimension as replicated). */
+crys_status crys_db_column_rows(const crys_db* db, const char* table, const char* column, int64_t* rows);
+/* Copy a column back to the host (h_out must hold `rows` values; a group's
+ * lineorder comes back whole, shards in row order). */
 crys_status crys_db_download_column(const crys_db* db, const char* table, const char* column,
                                     int32_t* h_out, int64_t rows);
 void crys_db_free(crys_db* db);
@@ -300,6 +304,19 @@ crys_status crys_radix_histogram(crys_ctx* ctx, const int32_t* d_keys, int64_t n
 crys_status crys_radix_partition(crys_ctx* ctx, const int32_t* d_keys, const int32_t* d_payloads,
                                  int64_t n, int start_bit, int num_bits, int32_t* d_out_keys,
                                  int32_t* d_out_payloads);
+
+/* The Crystal device primitives (PAPER Table 1; block_ops.hpp:23-173), one
+ * logical tile of bt*ipt slots per CTA with the reference's striped ownership
+ * (slot t + k*bt): BlockLoad -> BlockPred(pred) -> per-thread counts ->
+ * BlockScan -> BlockShuffle -> BlockStore, plus BlockAggregate.  Per tile b:
+ * d_out[b*bt*ipt ..) = the compacted tile (thread-major, block_shuffle order),
+ * d_counts / d_prefix[b*bt + t] = block_thread_counts / block_scan prefix,
+ * d_totals[b] = matches, d_aggs[b*8 + 0..3] = SUM, COUNT, MIN, MAX over the
+ * matches and [4..7] over all valid slots (identities 0, 0, INT32_MAX,
+ * INT32_MIN on empty input).  1 <= bt <= 1024, 1 <= ipt <= 16.  Synchronous. */
+crys_status crys_block_ops_run(crys_ctx* ctx, const int32_t* d_in, int64_t n, int bt, int ipt,
+                               crys_pred pred, int32_t* d_out, int64_t* d_counts, int64_t* d_prefix,
+                               int64_t* d_totals, int64_t* d_aggs);
 
 /* ------------------------------------------------------------ timing hooks
  * Device-timed (CUDA events on the ctx stream) duration of the last call's

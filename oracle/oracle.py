@@ -349,6 +349,45 @@ class RefImpl:
             raise RuntimeError(self.error())
 
 
+def block_ops(column, bt, ipt, lo, hi):
+    """Restatement of the reference's block primitives for every tile of
+    `column` (P:include/tq/block_ops.hpp): block_load (:23-32), block_pred
+    with an inclusive [lo, hi] predicate (:54-69), block_thread_counts +
+    block_scan (:73-96), block_shuffle (:101-122) and block_aggregate
+    SUM/COUNT/MIN/MAX (:141-173; i64 accumulation, identities 0/0/INT32_MAX/
+    INT32_MIN), masked by the flags and over all valid slots.  Same layout as
+    tq.block_ops_run.  Pure Python loops: small inputs only."""
+    x = np.asarray(column, np.int64)
+    n = len(x)
+    S = bt * ipt
+    tiles = (n + S - 1) // S
+    out = np.zeros((tiles, S), np.int32)
+    counts = np.zeros((tiles, bt), np.int64)
+    prefix = np.zeros((tiles, bt), np.int64)
+    totals = np.zeros(tiles, np.int64)
+    aggs = np.zeros((tiles, 8), np.int64)
+    imax, imin = 2 ** 31 - 1, -2 ** 31
+    for b in range(tiles):
+        tile = x[b * S:min(n, (b + 1) * S)]
+        valid = len(tile)
+        flags = (tile >= lo) & (tile <= hi)
+        for t in range(bt):
+            counts[b, t] = int(flags[t:valid:bt].sum())
+        prefix[b] = np.concatenate([[0], np.cumsum(counts[b])[:-1]])
+        totals[b] = counts[b].sum()
+        pos = 0
+        for t in range(bt):
+            for i in range(t, valid, bt):
+                if flags[i]:
+                    out[b, pos] = tile[i]
+                    pos += 1
+        for j, m in enumerate((flags, np.ones(valid, bool))):
+            v = tile[m]
+            aggs[b, 4 * j:4 * j + 4] = [int(v.sum()), len(v), int(v.min()) if len(v) else imax,
+                                        int(v.max()) if len(v) else imin]
+    return {"out": out, "counts": counts, "prefix": prefix, "totals": totals, "aggs": aggs}
+
+
 def fnv_rows(rows):
     """FNV-1a-64 over result rows (SURVEY.md Appendix A definition)."""
     h = 1469598103934665603

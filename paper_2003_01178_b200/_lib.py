@@ -68,6 +68,7 @@ SIGNATURES = [
     ("crys_db_save_column_file", C.c_int, [_P, C.c_char_p, C.c_char_p, C.c_char_p]),
     ("crys_db_column", C.c_int, [_P, C.c_char_p, C.c_char_p, C.POINTER(_P), _I64P]),
     ("crys_db_download_column", C.c_int, [_P, C.c_char_p, C.c_char_p, _P, C.c_int64]),
+    ("crys_db_column_rows", C.c_int, [_P, C.c_char_p, C.c_char_p, _I64P]),
     ("crys_db_free", None, [_P]),
     ("crys_query_shape", C.c_int, [C.c_int, _I64P, _I32P, _I32P]),
     ("crys_run_query", C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, _P, _P, C.c_int64, _I64P, _P]),
@@ -81,6 +82,7 @@ SIGNATURES = [
     ("crys_query_finalize", C.c_int, [_P, C.c_int, _P, _P, _P, _P, C.c_int64, _I64P, _P]),
     ("crys_query_finalize_host", C.c_int, [C.c_int, _P, _P, _P, _P, C.c_int64, _I64P, _P]),
     ("crys_select_i32", C.c_int, [_P, _P, C.c_int64, crys_pred, _P, _I64P, C.c_int, C.c_int, C.c_int]),
+    ("crys_block_ops_run", C.c_int, [_P, _P, C.c_int64, C.c_int, C.c_int, crys_pred, _P, _P, _P, _P, _P]),
     ("crys_project_f32", C.c_int, [_P, _P, _P, C.c_int64, C.c_float, C.c_float, _P, C.c_int,
                                    C.c_int, C.c_int]),
     ("crys_ht_build", C.c_int, [_P, _P, _P, C.c_int64, C.c_int64, C.POINTER(_P)]),

@@ -692,6 +692,26 @@ crys_status crys_db_column(const crys_db* db, const char* table, const char* col
   });
 }
 
+crys_status crys_db_column_rows(const crys_db* db, const char* table, const char* column, int64_t* rows) {
+  return guarded([&] {
+    CRYS_CHECK(db && table && column && rows, CRYS_ECONFIG, "null argument");
+    const bool fact = std::string(table) == "lineorder";
+    int64_t total = 0;
+    if (!db->is_group()) {
+      auto it = db->cols.find(std::string(table) + "." + column);
+      CRYS_CHECK(it != db->cols.end(), CRYS_ECONTRACT, std::string("table ") + table + ": no column " + column);
+      total = it->second.rows;
+    }
+    for (const crys_db* part : db->shards) {
+      auto it = part->cols.find(std::string(table) + "." + column);
+      CRYS_CHECK(it != part->cols.end(), CRYS_ECONTRACT, std::string("table ") + table + ": no column " + column);
+      total += it->second.rows;
+      if (!fact) break;
+    }
+    *rows = total;
+  });
+}
+
 crys_status crys_db_download_column(const crys_db* db, const char* table, const char* column,
                                     int32_t* h_out, int64_t rows) {
   if (db && db->is_group()) {  // lineorder: the shards in row order; dimensions: shard 0
@@ -923,6 +943,20 @@ crys_status crys_select_i32(crys_ctx* ctx, const int32_t* d_in, int64_t n, crys_
     crys::timing_begin(ctx);
     *count = crys::select_i32(ctx, d_in, n, lo, hi, d_out, order, bt, ipt);
     crys::timing_end(ctx);
+  });
+}
+
+crys_status crys_block_ops_run(crys_ctx* ctx, const int32_t* d_in, int64_t n, int bt, int ipt, crys_pred pred,
+                               int32_t* d_out, int64_t* d_counts, int64_t* d_prefix, int64_t* d_totals,
+                               int64_t* d_aggs) {
+  return guarded([&] {
+    bind(ctx);
+    CRYS_CHECK(bt > 0 && ipt > 0, CRYS_ECONFIG, "TileConfig: block_threads/items_per_thread must be positive");
+    CRYS_CHECK(d_in && d_out && d_counts && d_prefix && d_totals && d_aggs, CRYS_ECONFIG, "null argument");
+    int32_t lo, hi;
+    crys::lower_pred(pred, &lo, &hi);
+    crys::block_ops_run(ctx, d_in, n, bt, ipt, lo, hi, d_out, d_counts, d_prefix, d_totals, d_aggs);
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   });
 }
 

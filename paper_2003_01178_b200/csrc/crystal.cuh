@@ -121,7 +121,31 @@ __device__ __forceinline__ void BlockLoadSel(const int32_t* __restrict__ tile, i
   }
 }
 
-// Striped BlockLoad: item k of thread t = tile[t + k*BT] (tile.hpp:3-8 ownership).
+// ---------------------------------------------------------------- Striped
+// The reference's logical ownership (tile.hpp:3-8, block_ops.hpp:1-8): item k
+// of logical thread t is tile slot t + k*bt.  `bt` is a runtime value (any
+// positive TileConfig); CTA threads t >= bt own no slot.
+
+// Items of this thread inside a (partial) tile of `valid` slots, ipt <= IPT.
+template <int IPT>
+__device__ __forceinline__ unsigned BlockValidMaskStriped(int bt, int ipt, int valid) {
+  unsigned m = 0;
+  if ((int)threadIdx.x >= bt) return 0;
+#pragma unroll
+  for (int k = 0; k < IPT; ++k)
+    if (k < ipt && (int)threadIdx.x + k * bt < valid) m |= 1u << k;
+  return m;
+}
+
+// Striped BlockLoad: item k of thread t = tile[t + k*bt] for the slots `mask`
+// selects (BlockValidMaskStriped; a BlockLoadSel when it is a flag mask).
+template <int IPT, class T>
+__device__ __forceinline__ void BlockLoadStriped(const T* __restrict__ tile, int bt, unsigned mask,
+                                                 T (&items)[IPT]) {
+#pragma unroll
+  for (int k = 0; k < IPT; ++k)
+    if ((mask >> k) & 1u) items[k] = tile[threadIdx.x + k * bt];
+}
 template <int IPT>
 __device__ __forceinline__ void BlockLoadStriped(const int32_t* __restrict__ tile, int bt,
                                                  int valid, int32_t (&items)[IPT]) {
@@ -130,6 +154,28 @@ __device__ __forceinline__ void BlockLoadStriped(const int32_t* __restrict__ til
     const int s = threadIdx.x + k * bt;
     if (s < valid) items[k] = ld_stream1(tile + s);
   }
+}
+
+// BlockShuffle (block_ops.hpp:101-122), the per-thread step: this thread's
+// flagged items, in item (stride) order, written from s_out[prefix] on --
+// with `prefix` from BlockScan of the per-thread counts the tile comes out
+// thread-major (the Figure-5 order, e.g. {9,6,8,7,6,9,8,6,7,8}).  Returns the
+// thread's count.  The caller barriers before the compacted tile is read.
+template <int IPT, class T>
+__device__ __forceinline__ int BlockShuffle(const T (&items)[IPT], unsigned flags, int prefix, T* s_out) {
+  int pos = prefix;
+#pragma unroll
+  for (int k = 0; k < IPT; ++k)
+    if ((flags >> k) & 1u) s_out[pos++] = items[k];
+  return pos - prefix;
+}
+
+// BlockStore (block_ops.hpp:125-131): the compacted tile s_tile[0, n) to
+// dest[0, n), coalesced over the CTA's BT threads.  Bounds are the caller's
+// contract (the reference's ContractError is a host-side check).
+template <int BT, class T>
+__device__ __forceinline__ void BlockStore(const T* s_tile, int n, T* __restrict__ dest) {
+  for (int i = threadIdx.x; i < n; i += BT) dest[i] = s_tile[i];
 }
 
 // BlockPred / BlockPredAnd (block_ops.hpp:54-69).  Every PredicateSpec op
@@ -200,6 +246,58 @@ __device__ __forceinline__ long long BlockAggregateSum(const int32_t (&items)[IP
   for (int k = 0; k < IPT; ++k)
     if ((flags >> k) & 1u) s += items[k];
   return s;
+}
+
+// BlockAggregate (block_ops.hpp:133-173): SUM / COUNT / MIN / MAX over the
+// items `mask` selects (the valid slots, or the flagged ones), reduced over
+// the whole CTA.  Integers accumulate in 8 bytes (AggValue<i32> = i64; 8 x
+// INT32_MAX does not wrap); floats in double.  Empty input -> the identity:
+// 0 / 0 / numeric_limits<T>::max() / lowest() (+-inf for float).  Every
+// thread of the CTA calls it; the result is returned to all of them.
+enum BlockAggKind { kBlockSum = 0, kBlockCount = 1, kBlockMin = 2, kBlockMax = 3 };
+
+template <class T>
+struct AggTraits;
+template <>
+struct AggTraits<int32_t> {
+  using Acc = long long;
+  __device__ static Acc min_identity() { return (Acc)INT32_MAX; }
+  __device__ static Acc max_identity() { return (Acc)INT32_MIN; }
+};
+template <>
+struct AggTraits<float> {
+  using Acc = double;
+  __device__ static Acc min_identity() { return __longlong_as_double(0x7ff0000000000000ll); }
+  __device__ static Acc max_identity() { return __longlong_as_double((long long)0xfff0000000000000ull); }
+};
+
+template <class Acc>
+__device__ __forceinline__ Acc agg_combine(int kind, Acc a, Acc b) {
+  return kind == kBlockMin ? (b < a ? b : a) : kind == kBlockMax ? (b > a ? b : a) : a + b;
+}
+
+template <int BT, int IPT, class T>
+__device__ __forceinline__ typename AggTraits<T>::Acc BlockAggregate(int kind, const T (&items)[IPT], unsigned mask,
+                                                                     typename AggTraits<T>::Acc* s_red) {
+  using Acc = typename AggTraits<T>::Acc;
+  const Acc id = kind == kBlockMin ? AggTraits<T>::min_identity()
+                 : kind == kBlockMax ? AggTraits<T>::max_identity() : Acc(0);
+  Acc v = id;
+#pragma unroll
+  for (int k = 0; k < IPT; ++k)
+    if ((mask >> k) & 1u) v = agg_combine<Acc>(kind, v, kind == kBlockCount ? Acc(1) : (Acc)items[k]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = agg_combine<Acc>(kind, v, __shfl_xor_sync(0xffffffffu, v, o));
+  constexpr int W = BT / 32;
+  if constexpr (W > 1) {
+    if (lane_id() == 0) s_red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    v = id;
+#pragma unroll
+    for (int w = 0; w < W; ++w) v = agg_combine<Acc>(kind, v, s_red[w]);
+    __syncthreads();  // s_red reuse
+  }
+  return v;
 }
 
 // BlockProbeHashTable = block_lookup (hash_table.hpp:68-87) over interleaved

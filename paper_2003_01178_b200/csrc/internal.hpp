@@ -242,6 +242,8 @@ void ssb_run_group(crys_ctx* gctx, const crys_db* gdb, int qid, int bt, int ipt,
 void emit_rows(int qid, const std::vector<int64_t>& cell, const std::vector<int64_t>& sums,
                int32_t* h_groups, int64_t* h_sums, int64_t max_rows, int64_t* nrows);
 
+void block_ops_run(crys_ctx* ctx, const int32_t* in, int64_t n, int bt, int ipt, int32_t lo, int32_t hi,
+                   int32_t* out, int64_t* counts, int64_t* prefix, int64_t* totals, int64_t* aggs);
 int64_t select_i32(crys_ctx* ctx, const int32_t* d_in, int64_t n, int32_t lo, int32_t hi,
                    int32_t* d_out, int order, int bt, int ipt);
 void project_f32(crys_ctx* ctx, const float* x1, const float* x2, int64_t n, float a, float b,

@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(kCrysPB) select_crystal_kernel(
   }
   __syncthreads();
   const long long off = s_off;
-  for (int i = threadIdx.x; i < total; i += kCrysPB) out[off + i] = s_out[i];
+  BlockStore<kCrysPB, int32_t>(s_out, total, out + off);
   if (threadIdx.x == 0 && base + chunk >= n) *total_out = off + total;
 }
 
@@ -551,11 +551,8 @@ __device__ __forceinline__ int crystal_compact(const int32_t* __restrict__ in, i
     const unsigned long long ex = BlockScan<kCrysPB>(packed, s_scan, tot);
     int before = run;
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      int pos = before + (int)((ex >> (16 * g)) & 0xffff);
-#pragma unroll
-      for (int k = 0; k < IPTM; ++k)
-        if ((f[g] >> k) & 1u) s_out[pos++] = x[g][k];
+    for (int g = 0; g < G; ++g) {  // BlockShuffle of pair group g at its Crystal position
+      BlockShuffle<IPTM, int32_t>(x[g], f[g], before + (int)((ex >> (16 * g)) & 0xffff), s_out);
       before += (int)((tot >> (16 * g)) & 0xffff);
     }
     run = before;
@@ -594,7 +591,7 @@ __global__ void __launch_bounds__(kCrysPB) select_crystal_reg_kernel(
   } else {
     off = block_lookback<kCrysPB>(status, c, run, s_red);
   }
-  for (int i = threadIdx.x; i < run; i += kCrysPB) out[off + i] = s_out[i];
+  BlockStore<kCrysPB, int32_t>(s_out, run, out + off);
   if (threadIdx.x == 0 && base + chunk >= n) *total_out = off + run;
 }
 

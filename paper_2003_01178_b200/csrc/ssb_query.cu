@@ -1379,7 +1379,7 @@ static crys_group_box host_box(const QueryPlan& plan, const HostBox* hb) {
     const int32_t full = gp.hi - gp.lo + 1;
     const int32_t lo = std::max(0, hb->dmin[gp.join_index]);
     const int32_t hi = std::min(full - 1, hb->dmax[gp.join_index]);
-    b.lo[g] = gp.lo + lo;
+    b.lo[g] = gp.lo + (hi >= lo ? lo : 0);  // an empty part keeps its domain's low value
     b.card[g] = hi >= lo ? hi - lo + 1 : 0;
     b.cells *= b.card[g];
   }

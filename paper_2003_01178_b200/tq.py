@@ -440,8 +440,13 @@ class DeviceDatabase:
         check(LIB.crys_db_column(self.h, table.encode(), column.encode(), C.byref(p), C.byref(n)))
         return p.value or 0, n.value
 
+    def rows(self, table: str, column: str) -> int:
+        n = C.c_int64()
+        check(LIB.crys_db_column_rows(self.h, table.encode(), column.encode(), C.byref(n)))
+        return n.value
+
     def download(self, table: str, column: str) -> np.ndarray:
-        _, n = self.column_ptr(table, column)
+        n = self.rows(table, column)
         out = np.empty(n, np.int32)
         check(LIB.crys_db_download_column(self.h, table.encode(), column.encode(),
                                           out.ctypes.data_as(C.c_void_p), n))
@@ -717,6 +722,33 @@ def select_tile_into(inp, pred: PredicateSpec, out, config: TileConfig = TileCon
     if workers < 1:
         raise ConfigError("run_kernel: workers must be >= 1")
     return _select(inp, pred, out, _lib.CRYS_ORDER_CRYSTAL, config)
+
+
+def block_ops_run(column, pred: PredicateSpec, config: TileConfig) -> Dict[str, np.ndarray]:
+    """The Crystal device primitives over `column` (a CUDA int32 tensor), one
+    logical tile per CTA (crys_block_ops_run): per tile the compacted tile
+    (BlockLoad -> BlockPred -> BlockScan -> BlockShuffle -> BlockStore), the
+    per-logical-thread counts and exclusive prefixes, the match total and
+    BlockAggregate SUM/COUNT/MIN/MAX over the matches and over all valid
+    slots.  Returned as host arrays (test / inspection API)."""
+    import torch
+    config.validate()
+    pi, n = _dev(column, "int32")
+    bt, ipt = config.block_threads, config.items_per_thread
+    tiles = (n + bt * ipt - 1) // (bt * ipt)
+    dev = column.device
+    out = torch.zeros(tiles * bt * ipt, dtype=torch.int32, device=dev)
+    counts = torch.zeros(tiles * bt, dtype=torch.int64, device=dev)
+    prefix = torch.zeros(tiles * bt, dtype=torch.int64, device=dev)
+    totals = torch.zeros(tiles, dtype=torch.int64, device=dev)
+    aggs = torch.zeros(tiles * 8, dtype=torch.int64, device=dev)
+    ctx = _ctx_for(column)
+    check(LIB.crys_block_ops_run(ctx.h, C.c_void_p(pi), n, bt, ipt, pred._c(), C.c_void_p(out.data_ptr()),
+                                 C.c_void_p(counts.data_ptr()), C.c_void_p(prefix.data_ptr()),
+                                 C.c_void_p(totals.data_ptr()), C.c_void_p(aggs.data_ptr())))
+    return {"out": out.cpu().numpy().reshape(tiles, bt * ipt), "counts": counts.cpu().numpy().reshape(tiles, bt),
+            "prefix": prefix.cpu().numpy().reshape(tiles, bt), "totals": totals.cpu().numpy(),
+            "aggs": aggs.cpu().numpy().reshape(tiles, 8)}
 
 
 def _project(x1, x2, a, b, out, sigmoid, config):

@@ -126,9 +126,11 @@ def test_group_fixture_column_upload(tq):
 def _bad_tables(kind):
     from oracle.oracle import Oracle
     host = Oracle().generate(1, 42)
-    if kind == "dup":  # duplicate supplier key: BuildError (hash_table.cpp:51-93)
-        host["supplier"]["s_suppkey"] = host["supplier"]["s_suppkey"].copy()
-        host["supplier"]["s_suppkey"][7] = host["supplier"]["s_suppkey"][8]
+    if kind == "dup":  # duplicate key among q2.1's filtered suppliers: BuildError (hash_table.cpp:51-93)
+        sup = {k: v.copy() for k, v in host["supplier"].items()}
+        amer = np.nonzero(sup["s_region"] == 1)[0]  # AMERICA: both rows pass the filter
+        sup["s_suppkey"][amer[2]] = sup["s_suppkey"][amer[3]]
+        host["supplier"] = sup
     else:  # a brand outside p_brand1's declared domain [0, 999] on a part that passes q2.1's filter
         part = {k: v.copy() for k, v in host["part"].items()}
         part["p_brand1"][part["p_category"] == 1] = 1500  # MFGR#12 = category code 1

@@ -155,3 +155,26 @@ def test_hash_build_errors(orc):
 def test_sort_digest_definition():
     k = np.arange(10, dtype=np.int32)
     assert sort_digest(k, k, stride=1) == sort_digest(k.copy(), k.copy(), stride=1)
+
+
+def test_block_ops_restatement_pinned_to_reference_examples():
+    """The block-primitive restatement against the reference's own worked
+    examples: the Figure-5 tile (test_tile_engine.cpp:18-22, :57-79) and the
+    block_aggregate case (:190-221)."""
+    from oracle.oracle import block_ops
+    fig5 = [9, 4, 7, 6, 4, 1, 6, 1, 3, 8, 9, 7, 6, 2, 8, 8]
+    r = block_ops(fig5, 4, 4, 6, 2 ** 31 - 1)  # y > 5
+    assert r["counts"][0].tolist() == [2, 1, 4, 3]
+    assert r["prefix"][0].tolist() == [0, 2, 3, 7]
+    assert r["totals"][0] == 10
+    assert r["out"][0][:10].tolist() == [9, 6, 8, 7, 6, 9, 8, 6, 7, 8]
+    vals = [3, -7, 12, 0, 5, 5, -2, 9]
+    r = block_ops(vals, 4, 2, -2 ** 31, 2 ** 31 - 1)
+    assert r["aggs"][0][4:].tolist() == [25, 8, -7, 12]
+    # mask {0, 2, 6} -> values 3, 12, -2 (a predicate that selects exactly them)
+    r = block_ops([3, 12, -2], 4, 1, -2, 12)
+    assert r["aggs"][0][:4].tolist() == [13, 3, -2, 12]
+    r = block_ops([100], 4, 1, 0, 5)  # no match: the identities
+    assert r["aggs"][0][:4].tolist() == [0, 0, 2 ** 31 - 1, -2 ** 31]
+    r = block_ops([2 ** 31 - 1] * 8, 4, 2, 0, 2 ** 31 - 1)  # 8 x INT32_MAX does not wrap
+    assert r["aggs"][0][0] == 8 * (2 ** 31 - 1)
