@@ -185,6 +185,12 @@ crys_status crys_fill_float_pairs(crys_ctx* ctx, float* d_x1, float* d_x2, int64
  * and group arity of qid. */
 crys_status crys_query_shape(int qid, int64_t* cells, int32_t* ngroup, int32_t* njoins);
 
+/* The query's plan (plan_for, ssb_plans.cpp:21-322) as JSON: fact filters,
+ * ordered joins (dimension table / key / fact key / filters as inclusive
+ * ranges / payload), group parts and the aggregate.  Writes at most cap bytes
+ * (NUL-terminated); *len = the full length. */
+crys_status crys_query_plan_json(int qid, char* out, size_t cap, size_t* len);
+
 /* Replaces tq::run_query(db, id, config, workers, stats) (ssb_queries.hpp:76-78,
  * ssb_queries.cpp:277-286) on one GPU: dimension hash builds, one fused
  * lineorder pass, group compaction.  Rows come back lexicographically ordered

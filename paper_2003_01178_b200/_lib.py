@@ -71,6 +71,7 @@ SIGNATURES = [
     ("crys_db_column_rows", C.c_int, [_P, C.c_char_p, C.c_char_p, _I64P]),
     ("crys_db_free", None, [_P]),
     ("crys_query_shape", C.c_int, [C.c_int, _I64P, _I32P, _I32P]),
+    ("crys_query_plan_json", C.c_int, [C.c_int, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     ("crys_run_query", C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, _P, _P, C.c_int64, _I64P, _P]),
     ("crys_run_query_host", C.c_int, [_P, C.POINTER(crys_host_column), C.c_int, C.c_int, C.c_int,
                                       C.c_int, _P, _P, C.c_int64, _I64P, _P]),

@@ -775,6 +775,18 @@ crys_status crys_query_shape(int qid, int64_t* cells, int32_t* ngroup, int32_t* 
   });
 }
 
+crys_status crys_query_plan_json(int qid, char* out, size_t cap, size_t* len) {
+  return guarded([&] {
+    const std::string j = crys::plan_json(qid);
+    if (len) *len = j.size();
+    if (out && cap) {
+      const size_t n = std::min(cap - 1, j.size());
+      std::memcpy(out, j.data(), n);
+      out[n] = 0;
+    }
+  });
+}
+
 static void fill_survivors(int qid, const crys::ResultRows& r, int64_t* h_survivors) {
   if (!h_survivors) return;
   const crys::QueryPlan& p = crys::plan_for(qid);

@@ -102,6 +102,7 @@ struct QueryPlan {  // QueryPlan (ssb_plans.hpp:78-85)
 };
 
 const QueryPlan& plan_for(int qid);  // ConfigError for an unknown id
+std::string plan_json(int qid);
 int dict_code(const std::string& dict, const std::string& value);
 
 // Lowers PredicateSpec (tile.hpp:92-133) to an inclusive range.

@@ -69,6 +69,12 @@ struct PipeArgs {
   unsigned long long* surv;    // [4]
   int32_t* err;
   int32_t l2_ahead;            // > 0: bulk-prefetch tile it + l2_ahead into L2 when issuing tile it
+  // split plans (ssb_scan.cuh): every row alive after the dense joins goes
+  // to its CTA's region of the survivor list as {row, partial group index |
+  // bad << 31}; ssb_gather_kernel runs the rest of the plan over the list
+  uint2* list;                 // [gridDim.x][list_cap]
+  int64_t list_cap;
+  unsigned* list_count;        // [gridDim.x] entries per region
 };
 
 // Host: fill the uniform-decode fields of a direct table.
@@ -183,7 +189,8 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) ssb_pipeline_kernel(const Pip
   constexpr int R = TILE / W;   // rows per consumer warp per stage
   constexpr int V = R / 128;    // int4 key vectors per lane (phase A)
   static_assert(R % 128 == 0 && V >= 1 && V <= 4, "phase A: 4..16 rows per lane");
-  static_assert(NC - NJ == 1 || NC - NJ == 2, "aggregate columns");
+  constexpr int NA = NC - NJ;   // aggregate columns: revenue [, supplycost]
+  static_assert(NA == 1 || NA == 2, "aggregate columns");
   extern __shared__ __align__(128) unsigned char smem[];
   int32_t* ring = reinterpret_cast<int32_t*>(smem);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)STAGES * NC * TILE * 4);
@@ -288,7 +295,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) ssb_pipeline_kernel(const Pip
 #pragma unroll
       for (int j = 1; j < NJ; ++j) q.key[j] = st[j * TILE + row];
       q.va = st[NJ * TILE + row];
-      q.vb = NC - NJ == 2 ? st[(NJ + 1) * TILE + row] : 0;
+      q.vb = NA == 2 ? st[(NJ + 1) * TILE + row] : 0;
 #pragma unroll
       for (int j = 1; j < NJ; ++j) {  // every probe load in flight before any is used
         const uint32_t off = (uint32_t)q.key[j] - rt[j].kmin;
@@ -327,7 +334,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) ssb_pipeline_kernel(const Pip
           bad_any = true;
         } else {
           long long v = q.va;
-          if (NC - NJ == 2) v -= (long long)q.vb;
+          if (NA == 2) v -= (long long)q.vb;
           if (a.smem_agg >= 0) {
             smem_add_i64(&s_sum[idx], v);
             atomicAdd(&s_cnt[idx], 1u);

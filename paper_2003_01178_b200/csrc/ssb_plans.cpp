@@ -204,3 +204,39 @@ void lower_pred(const crys_pred& p, int32_t* lo, int32_t* hi) {
 }
 
 }  // namespace crys
+
+namespace crys {
+
+// The plan as JSON (introspection for tools / tests; the same contract the
+// fused kernels implement).
+std::string plan_json(int qid) {
+  const QueryPlan& p = plan_for(qid);
+  std::string s = "{\"qid\":" + std::to_string(p.qid) + ",\"name\":\"" + p.name + "\",\"fact_filters\":[";
+  for (size_t i = 0; i < p.fact_filters.size(); ++i)
+    s += std::string(i ? "," : "") + "{\"column\":\"" + p.fact_filters[i].column + "\",\"lo\":" +
+         std::to_string(p.fact_filters[i].lo) + ",\"hi\":" + std::to_string(p.fact_filters[i].hi) + "}";
+  s += "],\"joins\":[";
+  for (size_t j = 0; j < p.joins.size(); ++j) {
+    const DimJoin& d = p.joins[j];
+    s += std::string(j ? "," : "") + "{\"dim_table\":\"" + d.dim_table + "\",\"dim_key\":\"" + d.dim_key +
+         "\",\"fact_key\":\"" + d.fact_key + "\",\"payload\":\"" + d.payload + "\",\"filters\":[";
+    for (size_t f = 0; f < d.filters.size(); ++f) {
+      s += std::string(f ? "," : "") + "{\"column\":\"" + d.filters[f].column + "\",\"ranges\":[";
+      for (size_t r = 0; r < d.filters[f].ranges.size(); ++r)
+        s += std::string(r ? "," : "") + "[" + std::to_string(d.filters[f].ranges[r].first) + "," +
+             std::to_string(d.filters[f].ranges[r].second) + "]";
+      s += "]}";
+    }
+    s += "]}";
+  }
+  s += "],\"group\":[";
+  for (size_t g = 0; g < p.group.size(); ++g)
+    s += std::string(g ? "," : "") + "{\"join\":" + std::to_string(p.group[g].join_index) + ",\"lo\":" +
+         std::to_string(p.group[g].lo) + ",\"hi\":" + std::to_string(p.group[g].hi) + ",\"label\":\"" +
+         p.group[g].label + "\"}";
+  static const char* kAgg[3] = {"revenue", "extendedprice*discount", "revenue-supplycost"};
+  s += std::string("],\"agg\":\"") + kAgg[p.agg] + "\"}";
+  return s;
+}
+
+}  // namespace crys

@@ -32,7 +32,9 @@
 
 #include "crystal.cuh"
 #include "internal.hpp"
+#include "ssb_gather.cuh"
 #include "ssb_pipeline.cuh"
+#include "ssb_scan.cuh"
 
 namespace crys {
 
@@ -561,7 +563,9 @@ int blocks_per_sm(const void* fn, int bt, size_t smem) {
   return nb;
 }
 
-constexpr size_t kSmemOptin = 232448;  // 227 KB dynamic shared memory per CTA (sm_100a)
+// 227 KB of shared memory per CTA on sm_100a, less a margin for the kernels'
+// few static __shared__ words
+constexpr size_t kSmemOptin = 232448 - 256;
 
 // Shared-memory placement of the probe tables (plan order: join 0 is probed
 // for every row, later joins only for survivors) and then of the CTA-private
@@ -587,7 +591,7 @@ size_t place_smem(pipe::PipeArgs& pa, int nj, size_t fixed, int64_t cells) {
 }
 
 template <int NJ, int NC, int W, int TILE, int STAGES, int K0, bool S0>
-void launch_pipeline(crys_ctx* ctx, const pipe::PipeArgs& pa, size_t dyn, const std::string& name) {
+int launch_pipeline(crys_ctx* ctx, pipe::PipeArgs pa, size_t dyn, const std::string& name) {
   auto fn = pipe::ssb_pipeline_kernel<NJ, NC, W, TILE, STAGES, K0, S0>;
   const int threads = (W + 1) * 32;
   const int nb = blocks_per_sm((const void*)fn, threads, dyn);
@@ -596,30 +600,118 @@ void launch_pipeline(crys_ctx* ctx, const pipe::PipeArgs& pa, size_t dyn, const 
   fn<<<grid, threads, dyn, ctx->stream>>>(pa);
   CRYS_LAUNCHED(std::string("ssb_pipeline ") + name + " grid=" + std::to_string(grid) +
                 " smem=" + std::to_string(dyn));
+  return grid;
 }
 
 template <int NJ, int NC, int W, int TILE, int STAGES>
-void launch_pipeline_k0(crys_ctx* ctx, pipe::PipeArgs pa, int64_t cells, const std::string& name) {
+int launch_pipeline_k0(crys_ctx* ctx, pipe::PipeArgs pa, int64_t cells, const std::string& name) {
   const size_t fixed = pipe::fixed_smem<NC, TILE, STAGES>();
   CRYS_CHECK(fixed <= kSmemOptin, CRYS_ENOTBUILT, "pipeline ring exceeds shared memory");
   const size_t dyn = place_smem(pa, NJ, fixed, cells);
   const bool s0 = pa.tab[0].smem >= 0;
   switch (pa.tab[0].kind) {
     case kTabBitmap:
-      if (s0) launch_pipeline<NJ, NC, W, TILE, STAGES, kTabBitmap, true>(ctx, pa, dyn, name);
-      else launch_pipeline<NJ, NC, W, TILE, STAGES, kTabBitmap, false>(ctx, pa, dyn, name);
+      if (s0) return launch_pipeline<NJ, NC, W, TILE, STAGES, kTabBitmap, true>(ctx, pa, dyn, name);
+      return launch_pipeline<NJ, NC, W, TILE, STAGES, kTabBitmap, false>(ctx, pa, dyn, name);
+    case kTabU8:
+      if (s0) return launch_pipeline<NJ, NC, W, TILE, STAGES, kTabU8, true>(ctx, pa, dyn, name);
+      return launch_pipeline<NJ, NC, W, TILE, STAGES, kTabU8, false>(ctx, pa, dyn, name);
+    case kTabU16:
+      if (s0) return launch_pipeline<NJ, NC, W, TILE, STAGES, kTabU16, true>(ctx, pa, dyn, name);
+      return launch_pipeline<NJ, NC, W, TILE, STAGES, kTabU16, false>(ctx, pa, dyn, name);
+    default:
+      return launch_pipeline<NJ, NC, W, TILE, STAGES, kTabHash, false>(ctx, pa, dyn, name);
+  }
+}
+
+// Dense half of a split plan (ssb_scan.cuh): the first D joins streamed
+// through a ring of the D key columns only (deeper for the same shared
+// memory), survivors to the per-CTA list regions.  Returns the grid.
+template <int D, int W, int TILE, int STAGES, int K0, bool S0>
+int launch_scan(crys_ctx* ctx, pipe::PipeArgs pa, size_t dyn, const std::string& name) {
+  auto fn = pipe::ssb_scan_emit_kernel<D, W, TILE, TILE / W / 128, STAGES, K0, S0>;
+  const int threads = (W + 1) * 32;
+  const int nb = blocks_per_sm((const void*)fn, threads, dyn);
+  const int64_t ntiles = (pa.n + TILE - 1) / TILE;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)nb * ctx->num_sms));
+  const int64_t cap = ((ntiles + grid - 1) / grid) * TILE;  // every row of the CTA's tiles
+  CRYS_CHECK(cap * grid <= pa.list_cap, CRYS_ECONTRACT, "survivor list workspace too small");
+  pa.list_cap = cap;
+  fn<<<grid, threads, dyn, ctx->stream>>>(pa);
+  CRYS_LAUNCHED(std::string("ssb_scan_emit ") + name + " grid=" + std::to_string(grid) + " smem=" +
+                std::to_string(dyn));
+  return grid;
+}
+
+// Ring shapes (consumer warps W, rows per tile, stages): scan_shape() picks
+// one of these per launch (the autotuner's candidates).
+template <int D, int W, int TILE, int S>
+int launch_emit_shape(crys_ctx* ctx, pipe::PipeArgs pa, const std::string& name, int64_t* list_cap);
+
+int scan_cfg_env() {
+  static const int v = [] {
+    const char* e = getenv("CRYS_SCAN_CFG");
+    return e ? atoi(e) : -1;
+  }();
+  return v;
+}
+
+template <int D>
+int launch_emit(crys_ctx* ctx, pipe::PipeArgs pa, const std::string& name, int64_t* list_cap, int shape) {
+  if (scan_cfg_env() >= 0) shape = scan_cfg_env();
+  switch (shape) {
+    case 1: return launch_emit_shape<D, 16, D == 1 ? 4096 : 2048, D == 1 ? 6 : 4>(ctx, pa, name, list_cap);
+    case 2: return launch_emit_shape<D, 8, D == 1 ? 4096 : 2048, 4>(ctx, pa, name, list_cap);
+    case 3: return launch_emit_shape<D, 16, D == 1 ? 8192 : 4096, 3>(ctx, pa, name, list_cap);
+    default: return launch_emit_shape<D, 16, D == 1 ? 8192 : (D == 2 ? 4096 : 2048), 4>(ctx, pa, name, list_cap);
+  }
+}
+
+template <int D, int W, int TILE, int S>
+int launch_emit_shape(crys_ctx* ctx, pipe::PipeArgs pa, const std::string& name, int64_t* list_cap) {
+  const size_t fixed = ((size_t)S * D * TILE * 4 + 2 * S * 8 + 127) & ~(size_t)127;
+  const size_t dyn = place_smem(pa, D, fixed, 0);
+  const bool s0 = pa.tab[0].smem >= 0;
+  const int64_t ntiles = (pa.n + TILE - 1) / TILE;
+  int grid;
+  switch (pa.tab[0].kind) {
+    case kTabBitmap:
+      grid = s0 ? launch_scan<D, W, TILE, S, kTabBitmap, true>(ctx, pa, dyn, name)
+                : launch_scan<D, W, TILE, S, kTabBitmap, false>(ctx, pa, dyn, name);
       break;
     case kTabU8:
-      if (s0) launch_pipeline<NJ, NC, W, TILE, STAGES, kTabU8, true>(ctx, pa, dyn, name);
-      else launch_pipeline<NJ, NC, W, TILE, STAGES, kTabU8, false>(ctx, pa, dyn, name);
+      grid = s0 ? launch_scan<D, W, TILE, S, kTabU8, true>(ctx, pa, dyn, name)
+                : launch_scan<D, W, TILE, S, kTabU8, false>(ctx, pa, dyn, name);
       break;
     case kTabU16:
-      if (s0) launch_pipeline<NJ, NC, W, TILE, STAGES, kTabU16, true>(ctx, pa, dyn, name);
-      else launch_pipeline<NJ, NC, W, TILE, STAGES, kTabU16, false>(ctx, pa, dyn, name);
+      grid = s0 ? launch_scan<D, W, TILE, S, kTabU16, true>(ctx, pa, dyn, name)
+                : launch_scan<D, W, TILE, S, kTabU16, false>(ctx, pa, dyn, name);
       break;
     default:
-      launch_pipeline<NJ, NC, W, TILE, STAGES, kTabHash, false>(ctx, pa, dyn, name);
+      grid = launch_scan<D, W, TILE, S, kTabHash, false>(ctx, pa, dyn, name);
   }
+  *list_cap = ((ntiles + grid - 1) / grid) * TILE;
+  return grid;
+}
+
+// Gather half: joins D..NJ-1 and the aggregate over the survivor list.  A
+// persistent grid (4 CTAs of 256 threads per SM, 4 list entries per thread
+// per round); the aggregate is CTA-private in shared memory for small group
+// domains (q2.x, q3.1, q4.1, q4.2: hot cells), global atomics otherwise.
+constexpr int kGatherBT = 256, kGatherK = 4;
+template <int NJB, int NA>
+void launch_gather(crys_ctx* ctx, pipe::GatherArgs ga, int regions, int64_t cells, const std::string& name) {
+  CRYS_CHECK(regions <= pipe::kMaxRegions, CRYS_ENOTBUILT, "too many survivor-list regions");
+  ga.nregions = regions;
+  for (int j = 0; j < NJB; ++j) ga.tab[j].smem = -1;
+  const size_t agg = ((size_t)cells * 12 + 15) & ~(size_t)15;
+  ga.smem_agg = cells <= 8192 ? 0 : -1;
+  const size_t dyn = ga.smem_agg >= 0 ? agg : 0;
+  auto fn = pipe::ssb_gather_kernel<NJB, NA, kGatherBT, kGatherK>;
+  const int nb = blocks_per_sm((const void*)fn, kGatherBT, dyn);
+  const int grid = std::min(nb, 4) * ctx->num_sms;
+  fn<<<grid, kGatherBT, dyn, ctx->stream>>>(ga);
+  CRYS_LAUNCHED(std::string("ssb_gather ") + name + " smem=" + std::to_string(dyn));
 }
 
 // Tuning knob CRYS_PIPE_CFG selects the (consumer warps, tile rows, stages)
@@ -637,6 +729,16 @@ int pipe_cfg() {
 int l2_ahead() {
   static const int v = [] {
     const char* e = getenv("CRYS_L2_AHEAD");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+// CRYS_SPLIT=D forces split plans at join D (0 = the all-dense pipeline);
+// read with CRYS_PIPE_CFG / CRYS_L2_AHEAD, which disable the autotuner.
+int split_env() {
+  static const int v = [] {
+    const char* e = getenv("CRYS_SPLIT");
     return e ? atoi(e) : 0;
   }();
   return v;
@@ -695,13 +797,20 @@ struct QueryGraph {
 // (q2.x, q3.x) try four instantiations with and without the L2 bulk prefetch;
 // 6-column plans (q4.x, whose 48 KB stages leave no room for wider rings)
 // only the look-ahead distances of the default instantiation.
+// split > 0: the plan runs split at join `split` (EMIT kernel over joins
+// 0..split-1, then the gather kernel; ssb_gather.cuh).
 struct TuneCand {
-  int cfg, l2;
+  int cfg, l2, split;
 };
-constexpr int kTuneN = 8;
-constexpr TuneCand kTune4[kTuneN] = {{0, 0}, {4, 0}, {3, 0}, {6, 0}, {0, 2}, {4, 2}, {3, 2}, {6, 2}};
-constexpr int kTuneN6 = 3;
-constexpr TuneCand kTune6[kTuneN6] = {{0, 0}, {0, 2}, {0, 4}};
+// Split candidates run the dense head with one join (the measured winner
+// whenever join 0 is selective: q3.2-q3.4, q4.3); cfg then names the scan
+// ring shape (launch_emit).  Splitting after two joins was measured slower
+// everywhere (the second join's L2 probes stall the scan's consumers).
+constexpr int kTuneN = 11;
+constexpr TuneCand kTune4[kTuneN] = {{0, 0, 0}, {4, 0, 0}, {3, 0, 0}, {6, 0, 0}, {0, 2, 0}, {4, 2, 0},
+                                     {3, 2, 0}, {6, 2, 0}, {3, 2, 1}, {3, 4, 1}, {2, 2, 1}};
+constexpr int kTuneN6 = 6;
+constexpr TuneCand kTune6[kTuneN6] = {{0, 0, 0}, {0, 2, 0}, {0, 4, 0}, {3, 2, 1}, {3, 4, 1}, {2, 2, 1}};
 struct PipeTune {
   int chosen = -1;  // index into the plan shape's candidate list once decided
   int ncand = 0;
@@ -722,6 +831,8 @@ struct QueryWorkspace {
   DevBuf tables;   // every join's direct probe table, contiguous, 16 B aligned
   DevBuf result;   // ResultHeader + RowOut[cells]
   DevBuf packed;   // the packed partial of a device group member (NCCL payload)
+  DevBuf list;     // split plans: survivor list (uint2 per entry), regions of list_cap
+  DevBuf list_count;
   PinnedBuf host;
   HostBox* hbox = nullptr;  // host-mapped digit extents (box_publish_kernel)
   std::map<SeqKey, QueryGraph> graphs;
@@ -884,11 +995,13 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* dimdb, const std::vector
         d.nkeys = (uint32_t)((int64_t)hi - lo + 1);
         if (dj.payload.empty() || d.gcard == 0) {
           d.kind = kTabBitmap;
-          tbl_bytes[j] = ((size_t)(d.nkeys + 31) / 32) * 4;
+          // one extra (absent) entry past the key range: probes may clamp an
+          // out-of-range key to index nkeys instead of testing it (ssb_scan.cuh)
+          tbl_bytes[j] = ((size_t)(d.nkeys + 1 + 31) / 32) * 4;
           d.clear_value = 0u;
         } else {
           d.kind = d.gcard <= 254 ? kTabU8 : kTabU16;
-          tbl_bytes[j] = (size_t)d.nkeys * (d.kind == kTabU8 ? 1 : 2);
+          tbl_bytes[j] = (size_t)(d.nkeys + 1) * (d.kind == kTabU8 ? 1 : 2);
           d.clear_value = 0xFFFFFFFFu;
         }
         tbl_bytes[j] = (tbl_bytes[j] + 15) & ~(size_t)15;
@@ -980,20 +1093,63 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* dimdb, const std::vector
           pa.col[nj + 1] = facts[f]->col("lineorder", "lo_supplycost", &rows);
           CRYS_CHECK(rows == pa.n, CRYS_ECONTRACT, "lineorder columns of different length");
         }
-        if (nj == 3 && plan.agg == kAggRevenue)
+        const bool shape3 = nj == 3 && plan.agg == kAggRevenue;
+        const bool shape4 = nj == 4 && plan.agg == kAggRevenueMinusSupplyCost;
+        CRYS_CHECK(shape3 || shape4, CRYS_ENOTBUILT, "no fused pipeline for this plan shape");
+        if (c.split > 0 && c.split < nj) {  // dense joins 0..D-1, survivor list, gather tail
+          const int D = c.split, nb = nj - D;
+          pipe::PipeArgs pe = pa;
+          pe.cells = 0;
+          pe.list = ws.list.as<uint2>();
+          pe.list_cap = (int64_t)(ws.list.bytes / sizeof(uint2));
+          pe.list_count = ws.list_count.as<unsigned>();
+          int64_t cap = 0;
+          const int grid = D == 1   ? launch_emit<1>(ctx, pe, plan.name, &cap, c.cfg)
+                           : D == 2 ? launch_emit<2>(ctx, pe, plan.name, &cap, c.cfg)
+                                    : launch_emit<3>(ctx, pe, plan.name, &cap, c.cfg);
+          pipe::GatherArgs ga;
+          std::memset(&ga, 0, sizeof(ga));
+          ga.list = pe.list;
+          ga.list_cap = cap;
+          ga.list_count = pe.list_count;
+          for (int j = 0; j < nb; ++j) {
+            ga.col[j] = pa.col[D + j];
+            ga.tab[j] = pa.tab[D + j];
+          }
+          ga.col[nb] = pa.col[nj];
+          ga.col[nb + 1] = pa.col[nj + 1];
+          ga.meta = pa.meta;
+          ga.cells = (int32_t)cells;
+          ga.g_sum = pa.g_sum;
+          ga.g_cnt = pa.g_cnt;
+          ga.surv = pa.surv + D;
+          ga.err = pa.err;
+          if (shape3 && nb == 1) launch_gather<1, 1>(ctx, ga, grid, cells, plan.name);
+          else if (shape3 && nb == 2) launch_gather<2, 1>(ctx, ga, grid, cells, plan.name);
+          else if (shape4 && nb == 1) launch_gather<1, 2>(ctx, ga, grid, cells, plan.name);
+          else if (shape4 && nb == 2) launch_gather<2, 2>(ctx, ga, grid, cells, plan.name);
+          else launch_gather<3, 2>(ctx, ga, grid, cells, plan.name);
+          count_launch(ctx, 2);
+          continue;
+        }
+        if (shape3)
           launch_pipeline_cfg<3, 4>(ctx, pa, cells, plan.name, c.cfg);
-        else if (nj == 4 && plan.agg == kAggRevenueMinusSupplyCost)
-          launch_pipeline_cfg<4, 6>(ctx, pa, cells, plan.name, c.cfg);
         else
-          fail(CRYS_ENOTBUILT, "no fused pipeline for this plan shape");
+          launch_pipeline_cfg<4, 6>(ctx, pa, cells, plan.name, c.cfg);
         count_launch(ctx);
       }
     };
+    {  // survivor-list workspace of split plans (regions of whole CTA tile sets)
+      int64_t nmax = 0;
+      for (int64_t r : nrows) nmax = std::max(nmax, r);
+      ws.list.reserve(sizeof(uint2) * (size_t)(nmax + ((int64_t)ctx->num_sms * 4 + 1) * 4096));
+      ws.list_count.reserve(sizeof(unsigned) * (size_t)ctx->num_sms * 8);
+    }
     const int cfg = pipe_cfg();  // CRYS_PIPE_CFG > 0 forces an instantiation
-    TuneCand run{cfg, l2_ahead()};
+    TuneCand run{cfg, l2_ahead(), split_env()};
     const TuneCand* cands = nj == 3 ? kTune4 : kTune6;
     const int ncand = nj == 3 ? kTuneN : kTuneN6;
-    if (cfg == 0 && l2_ahead() == 0 && (nj == 3 || nj == 4) && tune_enabled() && tune_ok) {
+    if (cfg == 0 && l2_ahead() == 0 && split_env() == 0 && (nj == 3 || nj == 4) && tune_enabled() && tune_ok) {
       PipeTune& tn = ws.tune[{dimdb->uid, qid}];
       if (tn.chosen >= 0) {
         run = cands[tn.chosen];
@@ -1225,7 +1381,8 @@ static std::vector<uintptr_t> query_signature(crys_ctx* ctx, const std::vector<c
   std::vector<uintptr_t> sig = {(uintptr_t)ctx->stream, (uintptr_t)ws.agg.p, ws.agg.bytes,
                                 (uintptr_t)ws.meta.p, (uintptr_t)ws.tables.p, ws.tables.bytes,
                                 (uintptr_t)ws.result.p, ws.result.bytes, (uintptr_t)ws.host.p, ws.host.bytes,
-                                (uintptr_t)ws.packed.p, ws.packed.bytes, (uintptr_t)ws.hbox};
+                                (uintptr_t)ws.packed.p, ws.packed.bytes, (uintptr_t)ws.hbox,
+                                (uintptr_t)ws.list.p, ws.list.bytes, (uintptr_t)ws.list_count.p};
   for (int j = 0; j < kMaxJoins; ++j) {
     sig.push_back((uintptr_t)ws.slots[j].p);
     sig.push_back((uintptr_t)ws.compact[j].p);
@@ -1263,7 +1420,7 @@ static bool still_tuning(crys_ctx* ctx, const crys_db* dimdb, int qid) {
   const QueryPlan& plan = plan_for(qid);
   QueryWorkspace& ws = ws_of(ctx);
   const bool tunable = (plan.joins.size() == 3 || plan.joins.size() == 4) && tune_enabled() &&
-                       pipe_cfg() == 0 && l2_ahead() == 0;
+                       pipe_cfg() == 0 && l2_ahead() == 0 && split_env() == 0;
   if (!tunable) return false;
   auto it = ws.tune.find({dimdb->uid, qid});
   return it == ws.tune.end() || it->second.chosen < 0;

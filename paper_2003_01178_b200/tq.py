@@ -289,6 +289,16 @@ def query_shape(qid) -> Tuple[int, int, int]:
     return cells.value, ng.value, nj.value
 
 
+def query_plan(qid) -> dict:
+    """plan_for(id) (ssb_plans.cpp:21-322) as a dict: fact filters, ordered
+    joins with their inclusive-range filters and payloads, group parts, agg."""
+    n = C.c_size_t()
+    check(LIB.crys_query_plan_json(int(qid), None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    check(LIB.crys_query_plan_json(int(qid), buf, n.value + 1, C.byref(n)))
+    return json.loads(buf.value.decode())
+
+
 @dataclass
 class ResultRow:
     group: Tuple[int, ...]
