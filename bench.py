@@ -55,20 +55,65 @@ def fact_bytes(q, rows):
 
 
 def ncu_traffic():
-    """DRAM traffic of the 13 fused lineorder launches from the committed
-    `ncu --set full` capture (profiles/*_suite_traffic.json, newest round):
-    mean dram__bytes_read.sum + dram__bytes_write.sum per launch."""
+    """Per-query DRAM traffic of the fused lineorder kernels from the committed
+    `ncu --set full` capture of one suite pass (profiles/r*_suite_traffic.json,
+    newest round): dram__bytes_read.sum + dram__bytes_write.sum, summed over a
+    query's launches (one fused pass, or the scan + gather of a split plan)."""
     import glob
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_suite_traffic.json")))
     if not files:
         return None, None
     with open(files[-1]) as f:
         d = json.load(f)
-    L = d["launches"]
-    if len(L) != 13:
+    if "per_query" in d:
+        per = [d["per_query"][q]["dram_bytes"] for q in QUERY_NAMES]
+    elif len(d.get("launches", [])) == 13:
+        per = [x["dram_read"] + x["dram_write"] for x in d["launches"]]
+    else:
         return None, None
-    per = [x["dram_read"] + x["dram_write"] for x in L]
-    return sum(per) / 13.0, os.path.relpath(files[-1], ROOT)
+    return per, os.path.relpath(files[-1], ROOT)
+
+
+def min_bytes():
+    """Per-query minimum DRAM bytes at SF=20 in plan load order (full columns,
+    128 B lines, 32 B sectors): profiles/r02_min_bytes.json (tools/min_bytes.py)."""
+    p = os.path.join(ROOT, "profiles", "r02_min_bytes.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d, os.path.relpath(p, ROOT)
+    except Exception:
+        return None, None
+
+
+def host_info():
+    """CPU model, NUMA layout and core count of this host (for cpu_baseline)."""
+    model, numa = None, None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            k, _, v = ln.partition(":")
+            if k.strip() == "Model name":
+                model = v.strip()
+            elif k.strip() == "NUMA node(s)":
+                numa = int(v.strip())
+    except Exception:
+        pass
+    if model is None:
+        try:
+            with open("/proc/cpuinfo") as f:
+                for ln in f:
+                    if ln.startswith("model name"):
+                        model = ln.split(":", 1)[1].strip()
+                        break
+        except Exception:
+            pass
+    return {"cpu_model": model, "numa_nodes": numa, "logical_cpus": os.cpu_count()}
+
+
+def suite_config(sf):
+    """The workload description both arms print (identical key sets)."""
+    return {"workload": f"SSB 13-query suite SF={sf}", "sf": sf, "queries": QUERY_NAMES}
 
 
 def peaks():
@@ -217,10 +262,12 @@ def cpu_baseline(sf):
     t, per = reference_suite(ref, h, cores, rows)
     ref.free(h)
     total = sum(fact_bytes(q, rows) for q in range(13))
-    return {"value": round(total / t / 1e9, 3), "unit": "GB/s", "cores": cores, "kind": "reference",
+    line = {"value": round(total / t / 1e9, 3), "unit": "GB/s", "cores": cores, "kind": "reference",
             "sample": f"one pass of all 13 queries at SF={sf}: tq::run_query(TileConfig{{128,4}}, "
                       f"workers={cores}) incl. dimension builds",
             "ms_per_query": [round(x, 2) for x in per], "seconds": round(t, 2)}
+    line.update(host_info())
+    return line
 
 
 def run_reference_arm(args, rank, world):
@@ -263,12 +310,12 @@ def run_reference_arm(args, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1000 * tt / args.steps, 3),
             "higher_is_better": True, "scaling": "weak" if world > 1 else "strong",
             "vs_baseline": None, "dtype": "int32/int64", "data": "synthetic generate_ssb(sf, 42)",
-            "config": {"workload": f"SSB 13-query suite SF={sf}", "sf": sf, "sample_sf": sample_sf,
-                       "queries": QUERY_NAMES},
+            "config": suite_config(sf),
+            "sample_sf": sample_sf,
             "impl": "reference",
             "ms_per_query": dict(zip(QUERY_NAMES, ms_q)),
-            "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": cores,
-                             "kind": "reference", "sample": sample},
+            "cpu_baseline": dict({"value": round(value, 3), "unit": "GB/s", "cores": cores,
+                                  "kind": "reference", "sample": sample}, **host_info()),
             "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -294,6 +341,187 @@ def paper_model(rows, kern_ms, tot_ms, ms_step):
             "q21_frac_model_q21": round(m21 / kern_ms[3], 3),
             "suite_model_ms": round(sum(q_ms), 4),
             "suite_frac": round(sum(q_ms) / ms_step, 3)}
+
+
+# --------------------------------------------------------------- operator block
+# The paper's operator microbenchmarks (BASELINE configs[1]-[3]; SURVEY 8(d)
+# C2, C2', C3, C4') at their full sizes, inputs from the reference CLI's own
+# generators computed in HBM, each checked against the reference's goldens
+# (tests/golden/ops.json), device-timed (CUDA events inside the library around
+# the dominant kernels), bytes by the reference's bytes_moved conventions
+# (tools/tq_main.cpp:308, :353, :426, :483), and the paper's model fraction.
+
+def _digest_u32(t):
+    """col_digest (tests/golden/make_golden.py): sum((u32)v * (2i + 1)) mod 2^64, on the device."""
+    import torch
+    v = t.to(torch.int64) & 0xFFFFFFFF
+    w = torch.arange(t.numel(), dtype=torch.int64, device=t.device) * 2 + 1
+    s = int((v * w).sum().item())  # int64 arithmetic wraps mod 2^64
+    return f"{s & 0xFFFFFFFFFFFFFFFF:016x}"
+
+
+def ops_block(ctx, hbm, reps=3):
+    import torch
+    from paper_2003_01178_b200 import cost_models as cm
+    from paper_2003_01178_b200 import tq
+    with open(os.path.join(ROOT, "tests", "golden", "ops.json")) as f:
+        gold = json.load(f)
+    prof = cm.b200_profile()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    out = []
+    t_start = time.perf_counter()
+
+    def timed(fn):
+        fn()  # warm-up
+        ks = []
+        for _ in range(reps):
+            ctx.enable_timing(True)
+            r = fn()
+            k, _ = ctx.last_timing()
+            ctx.enable_timing(False)
+            ks.append(k)
+        return statistics.median(ks), r
+
+    def emit(rec, nbytes, kms, model):
+        gbs = nbytes / (kms * 1e-3) / 1e9
+        rec.update({"kernel_ms": round(kms, 4), "bytes": int(nbytes), "gbs": round(gbs, 1),
+                    "frac_of_peak": round(gbs / hbm, 4), "model_ms": round(model.total_ms, 4),
+                    "frac_of_model": round(model.total_ms / kms, 4)})
+        out.append(rec)
+
+    ctx.bind_torch_stream()
+    # C2 select, 2^29 int32, sigma in {0, 0.5, 1}, input and Crystal order
+    n = 1 << 29
+    x = torch.empty(n, dtype=torch.int32, device=dev)
+    tq.random_i32(x, 42, 1, 0, (1 << 20) - 1)
+    o = torch.empty_like(x)
+    for sigma in ("0.0", "0.5", "1.0"):
+        pred = tq.PredicateSpec.lt(int(round(float(sigma) * (1 << 20))))
+        for name, fn in (("input_order", lambda: tq.select_branching_into(x, pred, o)),
+                         ("crystal_128x4", lambda: tq.select_tile_into(x, pred, o, tq.TileConfig(128, 4)))):
+            kms, m = timed(fn)
+            emit({"op": "select", "variant": name, "n": n, "sigma": float(sigma), "matched": int(m),
+                  "golden_ok": int(m) == gold["select_2e29_counts"][sigma]},
+                 4 * n + 4 * m, kms, cm.model_select(n, m / n, prof))
+    del x, o
+    # C2' project, 2^29 float pairs, linear and sigmoid
+    x1 = torch.empty(n, dtype=torch.float32, device=dev)
+    x2 = torch.empty_like(x1)
+    tq.project_inputs(x1, x2, 42)
+    po = torch.empty_like(x1)
+    for name, fn in (("linear", lambda: tq.project_linear_into(x1, x2, 0.75, -1.25, po)),
+                     ("sigmoid", lambda: tq.project_sigmoid_into(x1, x2, 0.75, -1.25, po))):
+        kms, _ = timed(fn)
+        emit({"op": "project", "variant": name, "n": n,
+              "golden_ok": None, "golden": "digests pinned at n=100000 by tests/test_gpu_ops.py"},
+             12 * n, kms, cm.model_project(n, prof))
+    del x1, x2, po
+    # C3 join probe, 2^28 probes against 8 KB / 1 MB / 64 MB / 1 GB tables
+    P = 1 << 28
+    pp = torch.empty(P, dtype=torch.int32, device=dev)
+    tq.random_i32(pp, 42, 3, 0, 999)
+    pk = torch.empty_like(pp)
+    jg = {r["ht_bytes"]: r["checksum"] for r in gold["join_p2e28"]}
+    for H in (8 << 10, 1 << 20, 64 << 20, 1 << 30):
+        cap = H // 8
+        bn = cap // 2
+        bk = torch.arange(1, bn + 1, dtype=torch.int32, device=dev)
+        bp = torch.empty(bn, dtype=torch.int32, device=dev)
+        tq.random_i32(bp, 42, 4, 0, 999)
+        tq.random_i32(pk, 42, 5, 1, bn)
+        ht = tq.HashTable.build(bk, bp, cap)
+        kms, cs = timed(lambda: tq.join_probe_tile(pk, pp, ht))
+        emit({"op": "join_probe", "ht_bytes": H, "build_n": bn, "P": P, "checksum": int(cs),
+              "golden_ok": int(cs) == jg.get(H)}, 8 * P, kms, cm.model_join_probe(P, H, prof))
+        ht.free()
+        del bk, bp
+    del pp, pk
+    # C4' radix sort, 2^28 pairs, LSB (4 x 8-bit, == std::stable_sort) and MSB
+    n = 1 << 28
+    k0 = torch.empty(n, dtype=torch.int32, device=dev)
+    tq.random_i32(k0, 42, 6, -(2 ** 31) // 2, (2 ** 31 - 1) // 2)
+    idx = torch.arange(n, dtype=torch.int32, device=dev)
+    k, p = torch.empty_like(k0), torch.empty_like(k0)
+    g = gold["lsb_2e28"]
+    for name, fn in (("lsb_4x8", lambda: tq.lsb_radix_sort(k, p)), ("msb_8bit", lambda: tq.msb_radix_sort(k, p))):
+        ks = []
+        for r in range(reps + 1):
+            k.copy_(k0)
+            p.copy_(idx)
+            ctx.enable_timing(True)
+            fn()
+            kk, _ = ctx.last_timing()
+            ctx.enable_timing(False)
+            if r:
+                ks.append(kk)
+        if name == "lsb_4x8":
+            ok = _digest_u32(k) == g["keys"] and _digest_u32(p) == g["payloads"]
+        else:
+            ok = _digest_u32(k) == g["keys"] and bool(torch.equal(k0[p.long()], k))
+        emit({"op": "sort", "variant": name, "n": n, "golden_ok": ok,
+              "convention": "80N bytes (20N per 8-bit pass x 4, tools/tq_main.cpp:482-483)"},
+             80 * n, statistics.median(ks), cm.model_sort(n, 4, prof))
+    del k0, idx, k, p
+    torch.cuda.empty_cache()
+    return {"ops": out, "seconds": round(time.perf_counter() - t_start, 1),
+            "timing": "kernel-only device time (CUDA events in the library around the op's kernels), "
+                      f"median of {reps} after a warm-up"}
+
+
+def ops_cpu_baseline():
+    """The reference's own CPU operators (oracle/_ref, every host core) on the
+    same inputs, bounded to ~20 s: the cpu_baseline beside the ops block."""
+    from oracle.oracle import Oracle, RefImpl
+    orc, ref = Oracle(), RefImpl()
+    cores = os.cpu_count() or 1
+    res = []
+
+    def t(fn, reps=1):
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            ts.append((time.perf_counter() - t0) * 1e3)
+        return min(ts)
+
+    n = 1 << 29
+    x = orc.random_i32(n, 42, 1, 0, (1 << 20) - 1)
+    m = len(ref.select(0, x, "lt", 1 << 19, workers=cores))
+    ms = t(lambda: ref.select(0, x, "lt", 1 << 19, workers=cores))
+    res.append({"op": "select", "variant": "branching", "n": n, "sigma": 0.5, "ms": round(ms, 2),
+                "gbs": round((4 * n + 4 * m) / (ms * 1e-3) / 1e9, 2)})
+    del x
+    x1, x2 = orc.project_inputs(n, 42)
+    for sig in (False, True):
+        ms = t(lambda: ref.project(x1, x2, 0.75, -1.25, sig, workers=cores))
+        res.append({"op": "project", "variant": "sigmoid" if sig else "linear", "n": n, "ms": round(ms, 2),
+                    "gbs": round(12 * n / (ms * 1e-3) / 1e9, 2)})
+    del x1, x2
+    P = 1 << 28
+    pp = orc.random_i32(P, 42, 3, 0, 999)
+    for H in (1 << 20, 1 << 30):
+        cap = H // 8
+        bn = cap // 2
+        pk = orc.random_i32(P, 42, 5, 1, bn)
+        _, h = ref.ht_build(np.arange(1, bn + 1, dtype=np.int32), orc.random_i32(bn, 42, 4, 0, 999), cap,
+                            workers=cores)
+        ms = t(lambda: ref.join_probe(h, pk, pp, 2, 128, 4, cores))
+        ref.ht_free(h)
+        res.append({"op": "join_probe", "variant": "tile", "ht_bytes": H, "P": P, "ms": round(ms, 2),
+                    "gbs": round(8 * P / (ms * 1e-3) / 1e9, 2)})
+    del pp, pk
+    n = 1 << 28
+    k0 = orc.random_i32(n, 42, 6, -(2 ** 31) // 2, (2 ** 31 - 1) // 2)
+    k, p = k0.copy(), np.arange(n, dtype=np.int32)
+    ms = t(lambda: ref.sort(k, p, False, cores))
+    res.append({"op": "sort", "variant": "lsb_4x8", "n": n, "ms": round(ms, 2),
+                "gbs": round(80 * n / (ms * 1e-3) / 1e9, 2)})
+    ns = 1 << 25  # MSB's serial recursion takes ~10 s at 2^28: a 2^25 sample
+    k, p = k0[:ns].copy(), np.arange(ns, dtype=np.int32)
+    ms = t(lambda: ref.sort(k, p, True, cores))
+    res.append({"op": "sort", "variant": "msb_8bit", "n": ns, "sample": "2^25 prefix of the 2^28 input",
+                "ms": round(ms, 2), "gbs": round(80 * ns / (ms * 1e-3) / 1e9, 2)})
+    return {"cores": cores, "kind": "reference", "ops": res, **host_info()}
 
 
 # --------------------------------------------------------------- GPU arm
@@ -398,11 +626,11 @@ def run_ours(args, rank, world):
                 "higher_is_better": True, "scaling": "strong" if world > 1 else "strong",
                 "vs_baseline": None, "dtype": "int32/int64",
                 "data": "synthetic: generate_ssb(sf, seed=42) generated bit-exactly in HBM",
-                "config": {"workload": f"SSB 13-query suite SF={sf}"
-                                       + (f", lineorder sharded over {world} GPUs + NCCL reduce" if world > 1 else ""),
-                           "sf": sf, "lineorder_rows": rows_total, "tile": [cfg.block_threads, cfg.items_per_thread],
-                           "l2": "inputs larger than L2 (each lineorder column >= 480 MB vs 126 MB L2); no flush",
-                           "queries": QUERY_NAMES},
+                "config": suite_config(sf),
+                "details": {"lineorder_rows": rows_total, "tile": [cfg.block_threads, cfg.items_per_thread],
+                            "sharding": (f"lineorder row ranges over {world} GPUs, dimensions replicated, "
+                                         "one reduce of packed partials per query") if world > 1 else "one GPU",
+                            "l2": "inputs larger than L2 (each lineorder column >= 480 MB vs 126 MB L2); no flush"},
                 "gpu_launches": int(launches),
                 "clocks": clocks}
         if world == 1:
@@ -413,16 +641,45 @@ def run_ours(args, rank, world):
             alg = sum(fact_bytes(q, rows_total) for q in range(13))
             achieved = alg / (sum(kern_ms) * 1e-3) / 1e9
             traffic, tsrc = ncu_traffic()
+            mb, msrc = min_bytes()
+            read_gbs = getattr(args, "read_gbs", None)
             line["model"] = paper_model(rows_total, kern_ms, tot_ms, ms_step)
             line["roofline"] = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
                                 "unit": "GB/s", "frac": round(achieved / hbm, 4),
-                                "traffic": round(traffic) if traffic else None,
+                                "traffic": round(sum(traffic) / 13) if traffic else None,
                                 "traffic_source": tsrc,
                                 "algorithmic_bytes_per_launch": round(alg / 13),
                                 "peak_kind": peak_kind,
-                                "kernel": "ssb_flight1_kernel / ssb_pipeline_kernel (fused lineorder pass)",
+                                "read_peak_gbs": read_gbs,
+                                "kernel": "the fused lineorder pass of each query (ssb_flight1_kernel, "
+                                          "ssb_pipeline_kernel, or ssb_scan_emit + ssb_gather for split plans)",
                                 "algorithmic_bytes": "4 B x referenced fact columns x lineorder rows "
-                                                     "(16 B/row q1-q3, 24 B/row q4), summed over the 13 launches"}
+                                                     "(16 B/row q1-q3, 24 B/row q4), summed over the 13 queries",
+                                "note": "kernels that skip dead 128 B lines exceed 1.0 on this full-column "
+                                        "convention; per_query holds the fractions on the bytes they must read"}
+            pq = {}
+            for q, name in enumerate(QUERY_NAMES):
+                k = kern_ms[q]
+                rec = {"ms": round(tot_ms[q], 4), "fused_kernel_ms": round(k, 4),
+                       "full_bytes": fact_bytes(q, rows_total),
+                       "frac_full": round(fact_bytes(q, rows_total) / (k * 1e-3) / 1e9 / hbm, 3),
+                       "model_ms": line["model"]["model_ms"][name],
+                       "frac_model": line["model"]["frac_fused_kernel"][name]}
+                if mb and mb["sf"] == sf:
+                    m = mb["queries"][name]
+                    rec["line128_bytes"] = m["line128"]
+                    rec["sector32_bytes"] = m["sector32"]
+                    rec["frac_line128"] = round(m["line128"] / (k * 1e-3) / 1e9 / hbm, 3)
+                    rec["frac_sector32"] = round(m["sector32"] / (k * 1e-3) / 1e9 / hbm, 3)
+                    if read_gbs:
+                        rec["frac_line128_vs_read_peak"] = round(m["line128"] / (k * 1e-3) / 1e9 / read_gbs, 3)
+                if traffic:
+                    rec["dram_bytes"] = int(traffic[q])
+                    rec["frac_dram"] = round(traffic[q] / (k * 1e-3) / 1e9 / hbm, 3)
+                pq[name] = rec
+            line["per_query"] = pq
+            if mb and mb["sf"] == sf:
+                line["min_bytes_source"] = msrc
         out = line
     return out, sh, sf
 
@@ -531,6 +788,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-ops", action="store_true", help="skip the operator block (select/project/join/sort)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps
@@ -547,12 +805,27 @@ def main():
         # CRYS_BENCH_BACKEND=gloo (+ CRYS_BENCH_ONE_GPU=1) lets the N>1 code path
         # run on a single-GPU box as a functional check; never a reported number
         dist.init_process_group(os.environ.get("CRYS_BENCH_BACKEND", "nccl"))
+    if world == 1:  # measured read-only bandwidth (the fused passes only read)
+        import torch
+        from paper_2003_01178_b200 import tq
+        buf = torch.empty(1 << 30, dtype=torch.int32, device=f"cuda:{local_device()}")
+        buf.zero_()
+        args.read_gbs = round(tq.stream_read_gbs(buf, 5), 1)
+        del buf
+        torch.cuda.empty_cache()
     line, sh, sf = run_ours(args, rank, world)
     e2e = None if args.no_e2e else e2e_host(args, sh, sf, rank, world)
     if rank == 0:
         line["e2e"] = e2e
+        if world == 1 and not args.no_ops:
+            sh.db.free()
+            import torch
+            torch.cuda.empty_cache()
+            line["ops"] = ops_block(sh.ctx, peaks()[0])
         if world == 1 and not args.no_cpu:
             line["cpu_baseline"] = cpu_baseline(sf)
+            if not args.no_ops:
+                line["ops"]["cpu_baseline"] = ops_cpu_baseline()
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -324,6 +324,12 @@ crys_status crys_block_ops_run(crys_ctx* ctx, const int32_t* d_in, int64_t n, in
                                crys_pred pred, int32_t* d_out, int64_t* d_counts, int64_t* d_prefix,
                                int64_t* d_totals, int64_t* d_aggs);
 
+/* Read-only HBM bandwidth of this device, measured: a 128-bit streaming read
+ * of [d_buf, d_buf + bytes) (use >> L2, e.g. 4 GB), best of `reps`, in GB/s.
+ * The fused query kernels only read; this is the read-side reference beside
+ * the copy bandwidth of MEASURED_PEAKS.json. */
+crys_status crys_stream_read_gbs(crys_ctx* ctx, const void* d_buf, size_t bytes, int reps, double* gbs);
+
 /* ------------------------------------------------------------ timing hooks
  * Device-timed (CUDA events on the ctx stream) duration of the last call's
  * dominant kernel (the fused lineorder pass / select / probe / sort passes)

@@ -95,6 +95,7 @@ SIGNATURES = [
     ("crys_sort_pairs", C.c_int, [_P, _P, _P, C.c_int64, C.c_int, C.c_int]),
     ("crys_radix_histogram", C.c_int, [_P, _P, C.c_int64, C.c_int, C.c_int, C.c_int64, _P]),
     ("crys_radix_partition", C.c_int, [_P, _P, _P, C.c_int64, C.c_int, C.c_int, _P, _P]),
+    ("crys_stream_read_gbs", C.c_int, [_P, _P, C.c_size_t, C.c_int, C.POINTER(C.c_double)]),
     ("crys_last_timing", C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     ("crys_enable_timing", C.c_int, [_P, C.c_int]),
 ]

@@ -972,6 +972,14 @@ crys_status crys_block_ops_run(crys_ctx* ctx, const int32_t* d_in, int64_t n, in
   });
 }
 
+crys_status crys_stream_read_gbs(crys_ctx* ctx, const void* d_buf, size_t bytes, int reps, double* gbs) {
+  return guarded([&] {
+    bind(ctx);
+    CRYS_CHECK(gbs != nullptr, CRYS_ECONFIG, "null argument");
+    *gbs = crys::stream_read(ctx, d_buf, bytes, reps);
+  });
+}
+
 crys_status crys_project_f32(crys_ctx* ctx, const float* d_x1, const float* d_x2, int64_t n,
                              float a, float b, float* d_out, int sigmoid, int bt, int ipt) {
   return guarded([&] {

@@ -243,6 +243,7 @@ void ssb_run_group(crys_ctx* gctx, const crys_db* gdb, int qid, int bt, int ipt,
 void emit_rows(int qid, const std::vector<int64_t>& cell, const std::vector<int64_t>& sums,
                int32_t* h_groups, int64_t* h_sums, int64_t max_rows, int64_t* nrows);
 
+double stream_read(crys_ctx* ctx, const void* d, size_t bytes, int reps);
 void block_ops_run(crys_ctx* ctx, const int32_t* in, int64_t n, int bt, int ipt, int32_t lo, int32_t hi,
                    int32_t* out, int64_t* counts, int64_t* prefix, int64_t* totals, int64_t* aggs);
 int64_t select_i32(crys_ctx* ctx, const int32_t* d_in, int64_t n, int32_t lo, int32_t hi,

@@ -1520,4 +1520,54 @@ int64_t join_probe_sum(crys_ctx* ctx, const int32_t* d_keys, const int32_t* d_pa
   return (int64_t)h;
 }
 
+// Read-only HBM stream (the roofline's read-side reference): every 16 B of
+// [d, d + bytes) loaded once with L1-bypassing 128-bit loads, XOR-folded
+// into one word so nothing is optimised away.  4 loads in flight per thread.
+__global__ void __launch_bounds__(512) stream_read_kernel(const int4* __restrict__ d, int64_t n16,
+                                                          unsigned long long* sink) {
+  unsigned acc = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n16; i += 4 * stride) {
+    const int4 a = ld_stream4(reinterpret_cast<const int32_t*>(d + i));
+    const int4 b = ld_stream4(reinterpret_cast<const int32_t*>(d + i + stride));
+    const int4 c = ld_stream4(reinterpret_cast<const int32_t*>(d + i + 2 * stride));
+    const int4 e = ld_stream4(reinterpret_cast<const int32_t*>(d + i + 3 * stride));
+    acc ^= (unsigned)(a.x ^ a.y ^ a.z ^ a.w ^ b.x ^ b.y ^ b.z ^ b.w ^ c.x ^ c.y ^ c.z ^ c.w ^ e.x ^ e.y ^ e.z ^ e.w);
+  }
+  for (; i < n16; i += stride) {
+    const int4 a = ld_stream4(reinterpret_cast<const int32_t*>(d + i));
+    acc ^= (unsigned)(a.x ^ a.y ^ a.z ^ a.w);
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0 && acc == 0x9e3779b9u) atomicAdd(sink, 1ull);  // practically never
+}
+
+double stream_read(crys_ctx* ctx, const void* d, size_t bytes, int reps) {
+  CRYS_CHECK(d && bytes >= 16 && reps >= 1, CRYS_ECONFIG, "stream read: bad argument");
+  ctx->scratch2.reserve(64);
+  auto* sink = ctx->scratch2.as<unsigned long long>();
+  const int64_t n16 = (int64_t)(bytes / 16);
+  const int grid = ctx->num_sms * 4;
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  stream_read_kernel<<<grid, 512, 0, ctx->stream>>>(static_cast<const int4*>(d), n16, sink);  // warm-up
+  float best = 1e30f;
+  for (int r = 0; r < reps; ++r) {
+    CUDA_TRY(cudaEventRecord(e0, ctx->stream));
+    stream_read_kernel<<<grid, 512, 0, ctx->stream>>>(static_cast<const int4*>(d), n16, sink);
+    CUDA_TRY(cudaEventRecord(e1, ctx->stream));
+    CUDA_TRY(cudaEventSynchronize(e1));
+    float ms = 0;
+    CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+    best = std::min(best, ms);
+  }
+  count_launch(ctx, reps + 1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  CRYS_LAUNCHED("stream_read_kernel");
+  return (double)(n16 * 16) / (best * 1e-3) / 1e9;
+}
+
 }  // namespace crys

@@ -761,6 +761,15 @@ def block_ops_run(column, pred: PredicateSpec, config: TileConfig) -> Dict[str, 
             "aggs": aggs.cpu().numpy().reshape(tiles, 8)}
 
 
+def stream_read_gbs(buf, reps: int = 5) -> float:
+    """Measured read-only HBM bandwidth over a CUDA tensor (crys_stream_read_gbs)."""
+    ctx = _ctx_for(buf)
+    g = C.c_double()
+    check(LIB.crys_stream_read_gbs(ctx.h, C.c_void_p(buf.data_ptr()), buf.numel() * buf.element_size(),
+                                   int(reps), C.byref(g)))
+    return g.value
+
+
 def _project(x1, x2, a, b, out, sigmoid, config):
     config.validate()
     if _is_host(x1):

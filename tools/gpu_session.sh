@@ -17,9 +17,9 @@ if [[ $what == bench || $what == all ]]; then
 fi
 if [[ $what == ncu || $what == all ]]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
-     --log-file $OUT/launches.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > $OUT/ncu_bench.log 2>&1
+     --log-file $OUT/launches.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-ops > $OUT/ncu_bench.log 2>&1
   SUITE=1 timeout 900 ncu --set full --clock-control none --import-source on \
-     --nvtx --nvtx-include "profiled/" -k 'regex:ssb_(flight1|pipeline)' -c 13 \
+     --nvtx --nvtx-include "profiled/" -k 'regex:ssb_(flight1|pipeline|scan_emit|gather)' -c 30 \
      -o $OUT/prof_suite -f python tools/profile_query.py > $OUT/ncu_full.log 2>&1
 fi
 echo done

@@ -76,7 +76,25 @@ def traffic(rep, out_json):
                          "dram_write": val("dram__bytes_write.sum"),
                          "us": float(r[ti].replace(",", "")) * tscale.get(units[ti], 1e-3),
                          "l2_hit_pct": float(r[hdr.index("lts__t_sector_hit_rate.pct")])})
-    json.dump({"source": rep, "launches": launches}, open(out_json, "w"), indent=1)
+    # one suite pass in query order: flight 1 = one launch, a fused join pass
+    # = one launch, a split plan = scan + gather
+    names = ["q11", "q12", "q13", "q21", "q22", "q23", "q31", "q32", "q33", "q34", "q41", "q42", "q43"]
+    per_query, i = {}, 0
+    for q in names:
+        if i >= len(launches):
+            break
+        parts = [launches[i]]
+        i += 1
+        if "scan_emit" in parts[0]["kernel"] and i < len(launches) and "gather" in launches[i]["kernel"]:
+            parts.append(launches[i])
+            i += 1
+        per_query[q] = {"kernels": [x["kernel"] for x in parts],
+                        "dram_bytes": sum(x["dram_read"] + x["dram_write"] for x in parts),
+                        "us": sum(x["us"] for x in parts)}
+    doc = {"source": rep, "launches": launches}
+    if len(per_query) == 13 and i == len(launches):
+        doc["per_query"] = per_query
+    json.dump(doc, open(out_json, "w"), indent=1)
     for L in launches:
         print(f"{L['us']:9.1f} us  {(L['dram_read'] + L['dram_write']) / 1e9:7.3f} GB  "
               f"L2 hit {L['l2_hit_pct']:5.1f}%  {L['kernel'][:80]}")
