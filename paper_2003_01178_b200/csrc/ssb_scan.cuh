@@ -156,6 +156,81 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) ssb_scan_emit_kernel(const Pi
   int64_t row0 = (int64_t)blockIdx.x * TILE + warp * R;  // first row of this warp's slice
   const int64_t row_step = (int64_t)gridDim.x * TILE;
 
+  const unsigned lt = (1u << lane) - 1u;
+  // Everything after join 0 for one tile (`stp` = its stage, still held):
+  // join 1's probe words `raw` were issued one tile earlier (software
+  // pipelining: the L2 probes of a large join-1 table overlap the next
+  // stage's wait and join-0 pass), later joins are probed here; the rows alive
+  // after every dense join go to the list one per lane per round (rounds are
+  // warp-uniform), their group digits re-read from the stage; then the stage
+  // is released.
+  auto finish = [&](const int32_t* stp, int sp, unsigned h, const uint32_t (&raw)[NB], int64_t r0) {
+    if constexpr (D >= 2) {
+      const RegTab& t = rt[1];
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        if (!((h >> b) & 1u)) continue;
+        const int32_t key = stp[TILE + (b >> 2) * 128 + 4 * lane + (b & 3)];
+        bool hit1;
+        if (!t.hash) {
+          const uint32_t off = (uint32_t)key - t.kmin;
+          const uint32_t c = ((raw[b] >> ((off & t.emask) << t.lb)) & t.mask) ^ t.flip;
+          hit1 = off < t.n && c != t.mask;
+        } else {
+          uint32_t c;
+          bool bj;
+          hit1 = probe_reg(t, a.tab[1], meta, key, &c, &bj);
+        }
+        if (!hit1) h &= ~(1u << b);
+      }
+      surv[1] += __popc(h);
+#pragma unroll
+      for (int jj = 2; jj < D; ++jj) {
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          uint32_t c;
+          bool bj;
+          if (((h >> b) & 1u) &&
+              !probe_reg(rt[jj], a.tab[jj], meta, stp[jj * TILE + (b >> 2) * 128 + 4 * lane + (b & 3)], &c, &bj))
+            h &= ~(1u << b);
+        }
+        surv[jj] += __popc(h);
+      }
+    }
+    const uint32_t lrow = (uint32_t)r0 + (uint32_t)lane * 4u;
+    while (__any_sync(0xffffffffu, h != 0)) {
+      const bool act = h != 0;
+      const int b = act ? __ffs(h) - 1 : 0;
+      h &= h - 1u;
+      const int r = (b >> 2) * 128 + 4 * lane + (b & 3);  // row in the warp slice
+      const uint32_t c0 = entry_digit<K0>(probe_entry<K0, S0>(t0, sbase, stp[r]));
+      uint32_t idx = (t0.gstride != 0 && c0 == 0xFFFFu) ? 0x80000000u : c0 * (uint32_t)t0.gstride;
+#pragma unroll
+      for (int jj = 1; jj < D; ++jj) {
+        uint32_t c;
+        bool bj;
+        probe_reg(rt[jj], a.tab[jj], meta, stp[jj * TILE + r], &c, &bj);
+        if (rt[jj].gstride != 0 && bj) idx = 0x80000000u;
+        else if (!(idx >> 31)) idx += c * rt[jj].gstride;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, act);
+      const int leader = __ffs(bal) - 1;
+      unsigned base = 0;
+      if (lane == leader) base = atomicAdd(&s_list_n, (unsigned)__popc(bal));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (act) my_list[base + __popc(bal & lt)] = make_uint2(lrow + (uint32_t)((b >> 2) * 128 + (b & 3)), idx);
+    }
+    release_slot(empty + sp, lane == 0);  // the stage is no longer read
+  };
+
+  // the previous tile, waiting for its join-1 probe words (D >= 2)
+  unsigned p_hit = 0;
+  uint32_t p_raw[NB];
+  int p_s = -1;
+  int64_t p_row0 = 0;
+#pragma unroll
+  for (int b = 0; b < NB; ++b) p_raw[b] = 0;
+
   for (int it = 0; it < my_tiles; ++it, row0 += row_step) {
     const int s = it % STAGES;
     const int64_t left = a.n - row0;
@@ -182,55 +257,33 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) ssb_scan_emit_kernel(const Pi
         if ((b >> 2) * 128 + 4 * lane + (b & 3) >= valid) hit &= ~(1u << b);
     }
     surv[0] += __popc(hit);
-    // later dense joins, membership only, for the lane's live rows (vector
-    // LDS of the keys of a 4-row group that still holds one)
-#pragma unroll
-    for (int jj = 1; jj < D; ++jj) {
+    if constexpr (D == 1) {
+      finish(st, s, hit, p_raw, row0);
+    } else {
+      // join 1's probe words for this tile's live rows, consumed next iteration
+      uint32_t raw[NB];
+      const RegTab& t = rt[1];
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        if (!((hit >> (v * 4)) & 0xFu)) continue;
-        const int4 k4 = reinterpret_cast<const int4*>(st + jj * TILE)[v * 32 + lane];
+        const bool any = ((hit >> (v * 4)) & 0xFu) != 0;
+        int4 k4 = make_int4(0, 0, 0, 0);
+        if (any && !t.hash) k4 = reinterpret_cast<const int4*>(st + TILE)[v * 32 + lane];
         const int32_t kk[4] = {k4.x, k4.y, k4.z, k4.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          uint32_t c;
-          bool bj;
-          if (((hit >> (v * 4 + e)) & 1u) && !probe_reg(rt[jj], a.tab[jj], meta, kk[e], &c, &bj))
-            hit &= ~(1u << (v * 4 + e));
+          const uint32_t off = (uint32_t)kk[e] - t.kmin;
+          raw[4 * v + e] = (((hit >> (4 * v + e)) & 1u) && !t.hash) ? t.p[(off < t.n ? off : 0u) >> t.sh5] : 0u;
         }
       }
-      surv[jj] += __popc(hit);
-    }
-    // The rows alive after every dense join, one per lane per round (rounds
-    // are warp-uniform): the group digits are re-read from the still-held
-    // stage (no per-row state in registers), and each round's survivors go to
-    // the list with one shared atomic.
-    const unsigned lt = (1u << lane) - 1u;
-    const uint32_t lrow = (uint32_t)row0 + (uint32_t)lane * 4u;
-    while (__any_sync(0xffffffffu, hit != 0)) {
-      const bool act = hit != 0;
-      const int b = act ? __ffs(hit) - 1 : 0;
-      hit &= hit - 1u;
-      const int r = (b >> 2) * 128 + 4 * lane + (b & 3);  // row in the warp slice
-      const uint32_t c0 = entry_digit<K0>(probe_entry<K0, S0>(t0, sbase, st[r]));
-      uint32_t idx = (t0.gstride != 0 && c0 == 0xFFFFu) ? 0x80000000u : c0 * (uint32_t)t0.gstride;
+      if (p_s >= 0) finish(ring + (size_t)p_s * D * TILE + warp * R, p_s, p_hit, p_raw, p_row0);
+      p_s = s;
+      p_hit = hit;
+      p_row0 = row0;
 #pragma unroll
-      for (int jj = 1; jj < D; ++jj) {
-        uint32_t c;
-        bool bj;
-        probe_reg(rt[jj], a.tab[jj], meta, st[jj * TILE + r], &c, &bj);
-        if (rt[jj].gstride != 0 && bj) idx = 0x80000000u;
-        else if (!(idx >> 31)) idx += c * rt[jj].gstride;
-      }
-      const unsigned bal = __ballot_sync(0xffffffffu, act);
-      const int leader = __ffs(bal) - 1;
-      unsigned base = 0;
-      if (lane == leader) base = atomicAdd(&s_list_n, (unsigned)__popc(bal));
-      base = __shfl_sync(0xffffffffu, base, leader);
-      if (act) my_list[base + __popc(bal & lt)] = make_uint2(lrow + (uint32_t)((b >> 2) * 128 + (b & 3)), idx);
+      for (int b = 0; b < NB; ++b) p_raw[b] = raw[b];
     }
-    release_slot(empty + s, lane == 0);  // the stage is no longer read
   }
+  if (D >= 2 && p_s >= 0) finish(ring + (size_t)p_s * D * TILE + warp * R, p_s, p_hit, p_raw, p_row0);
   // survivors of the dense joins (per-lane counts): one atomic per warp and join
 #pragma unroll
   for (int j = 0; j < D; ++j) {
