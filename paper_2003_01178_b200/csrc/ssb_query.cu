@@ -91,6 +91,7 @@ struct Flight1Args {
   const int32_t* agg_a;
   const int32_t* agg_b;
   int32_t agg_b_is_f1;
+  int32_t l2_ahead;  // ring kernel: L2 bulk-prefetch distance (tiles)
   unsigned long long* g_sum;
   unsigned long long* g_cnt;
   unsigned long long* surv;
@@ -365,9 +366,17 @@ __device__ __forceinline__ T block_sum(T v, T* red) {
 // column is read only in vectors that still hold a live row (BlockLoadSel),
 // so dead 32 B sectors are never fetched.
 // PF: the NEXT tile's first column is loaded before this tile's dependent
-// (selective) loads, so the chain of three selective latencies overlaps a
+// (selective) loads, so the chain of selective latencies overlaps a
 // streaming read.
-template <int BT, int IPT, bool PF = false>
+// CH: depth of the dependent chain of selective loads.  The result is the
+//   conjunction of the three predicates whatever the order the columns are
+//   fetched in; only the bytes and the latencies differ:
+//   0  discount by f0, quantity by f01, price by f012 (3 round trips; the
+//      reference's order, fewest bytes)
+//   1  discount by f0, then quantity and price together by f01 (2)
+//   2  discount, quantity and price together by f0 (1; most bytes: pays when
+//      the date filter is selective, q1.2 / q1.3)
+template <int BT, int IPT, bool PF = false, int CH = 0>
 __global__ void __launch_bounds__(BT) ssb_flight1_kernel(const Flight1Args a) {
   using L = VecLayout<BT, IPT>;
   __shared__ long long red[BT / 32];
@@ -392,12 +401,28 @@ __global__ void __launch_bounds__(BT) ssb_flight1_kernel(const Flight1Args a) {
       BlockLoad<BT, IPT>(a.fcol[0] + base, valid, x);
     }
     unsigned f = BlockPred<IPT>(x, a.flo[0], a.fhi[0], BlockValidMask<BT, IPT>(valid));
-    BlockLoadSel<BT, IPT>(a.fcol[1] + base, valid, f, d);
-    f = BlockPredAnd<IPT>(d, a.flo[1], a.fhi[1], f);
-    BlockLoadSel<BT, IPT>(a.fcol[2] + base, valid, f, x);
-    f = BlockPredAnd<IPT>(x, a.flo[2], a.fhi[2], f);
-    BlockLoadSel<BT, IPT>(a.agg_a + base, valid, f, e);
-    if (!a.agg_b_is_f1) BlockLoadSel<BT, IPT>(a.agg_b + base, valid, f, d);
+    if constexpr (CH == 0) {
+      BlockLoadSel<BT, IPT>(a.fcol[1] + base, valid, f, d);
+      f = BlockPredAnd<IPT>(d, a.flo[1], a.fhi[1], f);
+      BlockLoadSel<BT, IPT>(a.fcol[2] + base, valid, f, x);
+      f = BlockPredAnd<IPT>(x, a.flo[2], a.fhi[2], f);
+      BlockLoadSel<BT, IPT>(a.agg_a + base, valid, f, e);
+      if (!a.agg_b_is_f1) BlockLoadSel<BT, IPT>(a.agg_b + base, valid, f, d);
+    } else if constexpr (CH == 1) {
+      BlockLoadSel<BT, IPT>(a.fcol[1] + base, valid, f, d);
+      f = BlockPredAnd<IPT>(d, a.flo[1], a.fhi[1], f);
+      BlockLoadSel<BT, IPT>(a.fcol[2] + base, valid, f, x);
+      BlockLoadSel<BT, IPT>(a.agg_a + base, valid, f, e);
+      f = BlockPredAnd<IPT>(x, a.flo[2], a.fhi[2], f);
+      if (!a.agg_b_is_f1) BlockLoadSel<BT, IPT>(a.agg_b + base, valid, f, d);
+    } else {
+      BlockLoadSel<BT, IPT>(a.fcol[1] + base, valid, f, d);
+      BlockLoadSel<BT, IPT>(a.fcol[2] + base, valid, f, x);
+      BlockLoadSel<BT, IPT>(a.agg_a + base, valid, f, e);
+      f = BlockPredAnd<IPT>(d, a.flo[1], a.fhi[1], f);
+      f = BlockPredAnd<IPT>(x, a.flo[2], a.fhi[2], f);
+      if (!a.agg_b_is_f1) BlockLoadSel<BT, IPT>(a.agg_b + base, valid, f, d);
+    }
 #pragma unroll
     for (int k = 0; k < IPT; ++k)
       if ((f >> k) & 1u) sum += (long long)e[k] * (long long)d[k];
@@ -411,6 +436,9 @@ __global__ void __launch_bounds__(BT) ssb_flight1_kernel(const Flight1Args a) {
     atomicAdd(a.surv, (unsigned long long)c);
   }
 }
+
+// (included inside crys::{anonymous}: it uses Flight1Args)
+#include "ssb_flight1.cuh"
 
 // Occupied cells -> (cell, sum) rows (grouped_result, ssb_queries.cpp:145-155).
 // Flight 1 always yields its single row (ssb_queries.cpp:207-209).  Only the
@@ -525,7 +553,15 @@ using F1Fn = void (*)(const Flight1Args);
 struct F1Launch {
   F1Fn fn;
   int bt, ipt;
+  int tile = 0;      // rows per CTA per iteration (0: bt * ipt)
+  size_t smem = 0;   // dynamic shared memory (ring kernels)
+  int l2 = 0;        // ring kernels: L2 bulk-prefetch distance
 };
+template <int W, int V, int S, int PR, int L2, bool ST = false, int D = 1, bool CHN = false>
+constexpr F1Launch f1_ring() {
+  return F1Launch{ssb_flight1_ring_kernel<W, V, S, PR, ST, D, CHN>, (W + 1) * 32, 0, W * 128 * V,
+                  ((size_t)S * D * W * 128 * V * 4 + 2 * S * 8 + 127) & ~(size_t)127, L2};
+}
 
 // Results are tile-invariant (test_ssb.cpp:251-261), so the TileConfig of a
 // query is validated but the GPU runs its own tuned shape; CRYS_F1_TILE=BTxIPT
@@ -544,6 +580,33 @@ F1Launch select_flight1() {
   // default: 256 x 8 with the next tile's first column prefetched (measured on
   // B200, tools/tune_f1pf.sh: q1.2 0.204 -> 0.193 ms, q1.3 0.184 -> 0.177 ms)
   return {ssb_flight1_kernel<256, 8, true>, 256, 8};
+}
+
+// Autotuner candidates of flight 1: register tiles (chain depth CH) and the
+// date-column TMA ring (ssb_flight1.cuh; warps x rows/lane x stages x
+// pipelined rounds, L2 look-ahead).
+// Measured on B200 at SF=20 (tools/f1_probe.py, profiles/r02_flight1.txt):
+// q1.1 wins with the two-column ring and chained gathers (0.262 -> 0.221 ms),
+// q1.2 / q1.3 with the date-only ring and chained gathers (0.192 -> 0.111,
+// 0.177 -> 0.078 ms).
+constexpr int kTuneF1 = 8;
+const F1Launch kF1Cands[kTuneF1] = {
+    {ssb_flight1_kernel<256, 8, true, 0>, 256, 8}, f1_ring<24, 4, 4, 2, 2>(),
+    f1_ring<16, 4, 3, 2, 0, true, 2>(),            f1_ring<16, 8, 3, 2, 0, true, 1, true>(),
+    f1_ring<24, 4, 4, 2, 2, true, 1, true>(),      f1_ring<16, 8, 3, 3, 0, false, 1, true>(),
+    f1_ring<16, 4, 3, 2, 0, true, 2, true>(),      f1_ring<16, 4, 3, 3, 2, false, 2, true>()};
+// CRYS_F1_CAND=k forces candidate k (A/B runs); -1: autotuned
+int flight1_cand() {
+  static const int k = [] {
+    const char* e = getenv("CRYS_F1_CAND");
+    const int v = e ? atoi(e) : -1;
+    return v >= 0 && v < kTuneF1 ? v : -1;
+  }();
+  return k;
+}
+bool flight1_forced() {
+  static const bool f = getenv("CRYS_F1_TILE") != nullptr || flight1_cand() >= 0;
+  return f;
 }
 
 int blocks_per_sm(const void* fn, int bt, size_t smem) {
@@ -905,6 +968,40 @@ static BoxPlan box_plan(const QueryPlan& plan, BoxMode mode) {
   return bp;
 }
 
+// Per-(database, query) autotuning: once decided, *chosen = the candidate and
+// false is returned.  Otherwise every candidate is enqueued three times (the
+// first run warms it up, the other two are timed together with events;
+// [sums | counts | survivors | err] re-zeroed between runs, the last run's
+// result is kept), the measurement is left in flight for tune_done() and true
+// is returned.
+template <class F>
+static bool tune_or_measure(QueryWorkspace& ws, uint64_t uid, int qid, int ncand, cudaStream_t st,
+                            unsigned long long* d_agg, int64_t cells, int* chosen, F&& launch_k) {
+  PipeTune& tn = ws.tune[{uid, qid}];
+  if (tn.chosen >= 0) {
+    *chosen = tn.chosen;
+    return false;
+  }
+  CRYS_CHECK(ncand <= kTuneN, CRYS_ENOTBUILT, "too many autotuner candidates");
+  tn.ncand = ncand;
+  for (int k = 0; k < ncand; ++k) {
+    if (!tn.e0[k]) {
+      CUDA_TRY(cudaEventCreate(&tn.e0[k]));
+      CUDA_TRY(cudaEventCreate(&tn.e1[k]));
+    }
+    for (int rep = 0; rep < 3; ++rep) {
+      if (k + rep > 0)  // the prologue zeroed it once
+        CUDA_TRY(cudaMemsetAsync(d_agg, 0, sizeof(unsigned long long) * (size_t)(2 * cells + 5), st));
+      if (rep == 1) CUDA_TRY(cudaEventRecord(tn.e0[k], st));
+      launch_k(k);
+      if (rep == 2) CUDA_TRY(cudaEventRecord(tn.e1[k], st));
+    }
+  }
+  tn.in_flight = true;
+  ws.measuring = &tn;
+  return true;
+}
+
 // Enqueues dimension builds (from `dimdb`) + the fused lineorder pass of `qid`
 // over every fact shard in `facts` (lineorder columns; several shards of one
 // device accumulate into the same aggregate), into d_agg = [sums | counts]
@@ -1150,28 +1247,11 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* dimdb, const std::vector
     const TuneCand* cands = nj == 3 ? kTune4 : kTune6;
     const int ncand = nj == 3 ? kTuneN : kTuneN6;
     if (cfg == 0 && l2_ahead() == 0 && split_env() == 0 && (nj == 3 || nj == 4) && tune_enabled() && tune_ok) {
-      PipeTune& tn = ws.tune[{dimdb->uid, qid}];
-      if (tn.chosen >= 0) {
-        run = cands[tn.chosen];
-      } else {  // every candidate twice, the second run timed; the last run's result is kept
-        tn.ncand = ncand;
-        for (int k = 0; k < ncand; ++k) {
-          if (!tn.e0[k]) {
-            CUDA_TRY(cudaEventCreate(&tn.e0[k]));
-            CUDA_TRY(cudaEventCreate(&tn.e1[k]));
-          }
-          for (int rep = 0; rep < 2; ++rep) {
-            if (k + rep > 0)  // re-zero [sums | counts | survivors | err] (the prologue zeroed it once)
-              CUDA_TRY(cudaMemsetAsync(d_agg, 0, sizeof(unsigned long long) * (size_t)(2 * cells + 5), st));
-            if (rep == 1) CUDA_TRY(cudaEventRecord(tn.e0[k], st));
-            launch(cands[k]);
-            if (rep == 1) CUDA_TRY(cudaEventRecord(tn.e1[k], st));
-          }
-        }
-        tn.in_flight = true;
-        ws.measuring = &tn;
+      int chosen = -1;
+      if (tune_or_measure(ws, dimdb->uid, qid, ncand, st, d_agg, cells, &chosen,
+                          [&](int k) { launch(cands[k]); }))
         return;
-      }
+      run = cands[chosen];
     }
     timing_kernel_begin(ctx);
     launch(run);
@@ -1183,9 +1263,10 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* dimdb, const std::vector
   fa.g_sum = d_agg;
   fa.g_cnt = d_agg + cells;
   fa.surv = d_surv;
-  F1Launch L = select_flight1();
-  const int nb = blocks_per_sm((const void*)L.fn, L.bt, 0);
-  timing_kernel_begin(ctx);
+  auto launch_f1 = [&](F1Launch L) {
+  const int nb = blocks_per_sm((const void*)L.fn, L.bt, L.smem);
+  const int64_t tile = L.tile ? L.tile : (int64_t)L.bt * L.ipt;
+  fa.l2_ahead = L.l2;
   for (size_t f = 0; f < facts.size(); ++f) {
     const int64_t n = nrows[f];
     fa.n = n;
@@ -1199,13 +1280,24 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* dimdb, const std::vector
     fa.agg_a = facts[f]->col("lineorder", "lo_extendedprice", &rows);
     fa.agg_b = facts[f]->col("lineorder", "lo_discount", &rows);
     fa.agg_b_is_f1 = plan.fact_filters.size() > 1 && plan.fact_filters[1].column == "lo_discount";
-    const int64_t ntiles = (n + (int64_t)L.bt * L.ipt - 1) / ((int64_t)L.bt * L.ipt);
+    const int64_t ntiles = (n + tile - 1) / tile;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)nb * ctx->num_sms));
-    L.fn<<<grid, L.bt, 0, st>>>(fa);
+    L.fn<<<grid, L.bt, L.smem, st>>>(fa);
     CRYS_LAUNCHED(std::string("fused ") + plan.name + " bt=" + std::to_string(L.bt) + " ipt=" +
                   std::to_string(L.ipt) + " grid=" + std::to_string(grid));
     count_launch(ctx);
   }
+  };
+  F1Launch L = flight1_cand() >= 0 ? kF1Cands[flight1_cand()] : select_flight1();
+  if (!flight1_forced() && tune_enabled() && tune_ok) {
+    int chosen = -1;
+    if (tune_or_measure(ws, dimdb->uid, qid, kTuneF1, st, d_agg, cells, &chosen,
+                        [&](int k) { launch_f1(kF1Cands[k]); }))
+      return;
+    L = kF1Cands[chosen];
+  }
+  timing_kernel_begin(ctx);
+  launch_f1(L);
   timing_kernel_end(ctx);
 }
 
@@ -1419,8 +1511,10 @@ static void tune_done(crys_ctx* ctx) {
 static bool still_tuning(crys_ctx* ctx, const crys_db* dimdb, int qid) {
   const QueryPlan& plan = plan_for(qid);
   QueryWorkspace& ws = ws_of(ctx);
-  const bool tunable = (plan.joins.size() == 3 || plan.joins.size() == 4) && tune_enabled() &&
-                       pipe_cfg() == 0 && l2_ahead() == 0 && split_env() == 0;
+  const bool tunable = plan.joins.empty()
+                           ? tune_enabled() && !flight1_forced()
+                           : (plan.joins.size() == 3 || plan.joins.size() == 4) && tune_enabled() &&
+                                 pipe_cfg() == 0 && l2_ahead() == 0 && split_env() == 0;
   if (!tunable) return false;
   auto it = ws.tune.find({dimdb->uid, qid});
   return it == ws.tune.end() || it->second.chosen < 0;
