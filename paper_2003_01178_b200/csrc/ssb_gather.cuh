@@ -40,12 +40,19 @@ struct GatherArgs {
   unsigned long long* g_cnt;
   unsigned long long* surv;   // survivors[D..NJ-1]
   int32_t* err;
+  // late-materialising plans (ssb_scanbm.cuh): entries {row, key, key, key};
+  // the first NPRE keys are those of the dense joins that feed a group part,
+  // whose digits are decoded here from their code tables (membership was
+  // already decided by the bitmaps)
+  const uint4* list4;
+  ProbeTab pre[3];
 };
 
-template <int NJB, int NA, int BT, int K>
+template <int NJB, int NA, int BT, int K, int NPRE = 0>
 __global__ void __launch_bounds__(BT) ssb_gather_kernel(const GatherArgs a) {
   static_assert(NJB >= 1 && NJB <= kMaxJ && (NA == 1 || NA == 2), "gather shape");
-  extern __shared__ __align__(16) unsigned char smem[];
+  static_assert(NPRE >= 0 && NPRE <= 3, "digit joins of the dense head");
+  extern __shared__ __align__(128) unsigned char smem[];
   __shared__ long long s_pre[kMaxRegions + 1];  // entries before each region
   __shared__ long long s_scan[BT / 32 + 1];
   const int lane = threadIdx.x & 31;
@@ -76,6 +83,9 @@ __global__ void __launch_bounds__(BT) ssb_gather_kernel(const GatherArgs a) {
   RegTab rt[NJB];
 #pragma unroll
   for (int j = 0; j < NJB; ++j) rt[j] = reg_tab(a.tab[j], nullptr);
+  RegTab rp[NPRE > 0 ? NPRE : 1];
+#pragma unroll
+  for (int p = 0; p < NPRE; ++p) rp[p] = reg_tab(a.pre[p], nullptr);
   uint32_t surv[NJB];
 #pragma unroll
   for (int j = 0; j < NJB; ++j) surv[j] = 0;
@@ -85,11 +95,12 @@ __global__ void __launch_bounds__(BT) ssb_gather_kernel(const GatherArgs a) {
   for (long long base = (long long)blockIdx.x * BT * K; base < total; base += (long long)gridDim.x * BT * K) {
     uint32_t row[K], idx[K];
     bool alive[K], bad[K];
+    uint32_t pkey[NPRE > 0 ? NPRE : 1][K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const long long i = base + k * BT + threadIdx.x;
       alive[k] = i < total;
-      uint2 e = make_uint2(0u, 0u);
+      long long at = 0;
       if (alive[k]) {
         int lo = 0, hi = a.nregions;  // region: the last r with s_pre[r] <= i
         while (hi - lo > 1) {
@@ -97,11 +108,41 @@ __global__ void __launch_bounds__(BT) ssb_gather_kernel(const GatherArgs a) {
           if (s_pre[mid] <= i) lo = mid;
           else hi = mid;
         }
-        e = a.list[(long long)lo * a.list_cap + (i - s_pre[lo])];
+        at = (long long)lo * a.list_cap + (i - s_pre[lo]);
       }
-      row[k] = e.x;
-      bad[k] = (e.y >> 31) != 0;
-      idx[k] = e.y & 0x7fffffffu;
+      if (a.list4 == nullptr) {
+        const uint2 e = alive[k] ? a.list[at] : make_uint2(0u, 0u);
+        row[k] = e.x;
+        bad[k] = (e.y >> 31) != 0;
+        idx[k] = e.y & 0x7fffffffu;
+      } else {
+        const uint4 e = alive[k] ? a.list4[at] : make_uint4(0u, 0u, 0u, 0u);
+        row[k] = e.x;
+        bad[k] = false;
+        idx[k] = 0;
+        pkey[0][k] = e.y;
+        if (NPRE > 1) pkey[NPRE > 1 ? 1 : 0][k] = e.z;
+        if (NPRE > 2) pkey[NPRE > 2 ? 2 : 0][k] = e.w;
+      }
+    }
+    // digits of the dense joins' group parts (K code probes in flight per join)
+#pragma unroll
+    for (int p = 0; p < NPRE; ++p) {
+      const RegTab& t = rp[p];
+      uint32_t raw[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const uint32_t off = pkey[p][k] - t.kmin;
+        raw[k] = alive[k] ? __ldg(t.p + ((off < t.n ? off : 0u) >> t.sh5)) : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const uint32_t off = pkey[p][k] - t.kmin;
+        const uint32_t c = ((raw[k] >> ((off & t.emask) << t.lb)) & t.mask) ^ t.flip;
+        alive[k] = alive[k] && off < t.n && c != t.mask;
+        idx[k] += c * t.gstride;
+        bad[k] = bad[k] || c == t.badc;
+      }
     }
 #pragma unroll
     for (int j = 0; j < NJB; ++j) {

@@ -23,6 +23,7 @@
 //                             index = lexicographic group order (:153).
 #include <algorithm>
 #include <climits>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -35,6 +36,7 @@
 #include "ssb_gather.cuh"
 #include "ssb_pipeline.cuh"
 #include "ssb_scan.cuh"
+#include "ssb_scanbm.cuh"
 
 namespace crys {
 
@@ -65,6 +67,7 @@ struct DimBuildDesc {
   int2* slots;             // kTabHash: linear-probing slots
   uint32_t clear_words;    // 32-bit words of the table to clear
   uint32_t clear_value;    // 0 (bitmap) or 0xFFFFFFFF (codes: all absent)
+  uint32_t* bits;          // code tables: the membership bitmap beside them (late-materialising plans)
 };
 
 struct DimBuildArgs {
@@ -74,9 +77,9 @@ struct DimBuildArgs {
 
 struct PrologueArgs {
   DimBuildArgs* unused;
-  uint32_t* tbl[kMaxJoins];
-  uint32_t words[kMaxJoins];
-  uint32_t value[kMaxJoins];
+  uint32_t* tbl[2 * kMaxJoins];  // probe tables, then the membership bitmaps of code tables
+  uint32_t words[2 * kMaxJoins];
+  uint32_t value[2 * kMaxJoins];
   unsigned long long* zero64;  // aggregate [2*cells] + counters (may be null)
   int64_t zero64_n;
   unsigned long long* zero64b; // result header (may be null)
@@ -173,7 +176,7 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 __global__ void query_prologue_kernel(const PrologueArgs a) {
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int j = 0; j < kMaxJoins; ++j) {
+  for (int j = 0; j < 2 * kMaxJoins; ++j) {
     uint32_t* t = a.tbl[j];
     if (!t) continue;
     const uint32_t v = a.value[j];
@@ -287,6 +290,7 @@ __global__ void __launch_bounds__(256) dim_filter_kernel(const DimBuildArgs a) {
       } else {
         ok = claim_code<16>(d.tbl, off, dig < 0 ? pipe::kU16Bad : (uint32_t)dig);
       }
+      if (d.bits) atomicOr(d.bits + (off >> 5), 1u << (off & 31));
       if (!ok) atomicCAS(&m->err, 0, 2);  // duplicate key (BuildError)
     }
   }
@@ -762,19 +766,95 @@ int launch_emit_shape(crys_ctx* ctx, pipe::PipeArgs pa, const std::string& name,
 // per round); the aggregate is CTA-private in shared memory for small group
 // domains (q2.x, q3.1, q4.1, q4.2: hot cells), global atomics otherwise.
 constexpr int kGatherBT = 256, kGatherK = 4;
-template <int NJB, int NA>
+template <int NJB, int NA, int NPRE = 0>
 void launch_gather(crys_ctx* ctx, pipe::GatherArgs ga, int regions, int64_t cells, const std::string& name) {
   CRYS_CHECK(regions <= pipe::kMaxRegions, CRYS_ENOTBUILT, "too many survivor-list regions");
   ga.nregions = regions;
   for (int j = 0; j < NJB; ++j) ga.tab[j].smem = -1;
+  for (int p = 0; p < 3; ++p) ga.pre[p].smem = -1;  // probed through L2 here
   const size_t agg = ((size_t)cells * 12 + 15) & ~(size_t)15;
   ga.smem_agg = cells <= 8192 ? 0 : -1;
   const size_t dyn = ga.smem_agg >= 0 ? agg : 0;
-  auto fn = pipe::ssb_gather_kernel<NJB, NA, kGatherBT, kGatherK>;
+  auto fn = pipe::ssb_gather_kernel<NJB, NA, kGatherBT, kGatherK, NPRE>;
   const int nb = blocks_per_sm((const void*)fn, kGatherBT, dyn);
   const int grid = std::min(nb, 4) * ctx->num_sms;
   fn<<<grid, kGatherBT, dyn, ctx->stream>>>(ga);
   CRYS_LAUNCHED(std::string("ssb_gather ") + name + " smem=" + std::to_string(dyn));
+}
+
+template <int NJB, int NA>
+void gather_pre(crys_ctx* ctx, pipe::GatherArgs ga, int regions, int64_t cells, const std::string& name, int npre) {
+  switch (npre) {
+    case 0: return launch_gather<NJB, NA, 0>(ctx, ga, regions, cells, name);
+    case 1: return launch_gather<NJB, NA, 1>(ctx, ga, regions, cells, name);
+    case 2: return launch_gather<NJB, NA, 2>(ctx, ga, regions, cells, name);
+    default: return launch_gather<NJB, NA, 3>(ctx, ga, regions, cells, name);
+  }
+}
+
+// Late-materialising plan (ssb_scanbm.cuh): the dense membership head over
+// joins 0..D-1.  Ring shapes (consumer warps, rows per lane / 4, stages) in
+// order of preference; the bitmaps go into what the ring leaves of 227 KB
+// (join 0 first: it is tested for every row), the rest are tested in L2.
+struct BmShape {
+  int w, v, s;
+};
+constexpr BmShape kBmShapes[4] = {{16, 2, 4}, {16, 2, 3}, {16, 2, 2}, {16, 1, 4}};
+
+template <int D, int W, int V, int S>
+int launch_scanbm_shape(crys_ctx* ctx, pipe::BmArgs ba, size_t dyn, const std::string& name, int64_t* cap) {
+  constexpr int TILE = W * 128 * V;
+  bool allsh = true;
+  for (int j = 0; j < D; ++j) allsh = allsh && ba.smem[j] >= 0;
+  auto fn = allsh ? pipe::ssb_scan_bm_kernel<D, W, V, S, true> : pipe::ssb_scan_bm_kernel<D, W, V, S, false>;
+  const int threads = (W + 1) * 32;
+  const int nb = blocks_per_sm((const void*)fn, threads, dyn);
+  const int64_t ntiles = (ba.n + TILE - 1) / TILE;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)nb * ctx->num_sms));
+  *cap = ((ntiles + grid - 1) / grid) * TILE;  // every row of the CTA's tiles
+  CRYS_CHECK(*cap * grid <= ba.list_cap, CRYS_ECONTRACT, "survivor list workspace too small");
+  ba.list_cap = *cap;
+  fn<<<grid, threads, dyn, ctx->stream>>>(ba);
+  CRYS_LAUNCHED(std::string("ssb_scan_bm ") + name + " D=" + std::to_string(D) + " grid=" + std::to_string(grid) +
+                " smem=" + std::to_string(dyn));
+  return grid;
+}
+
+template <int D>
+int launch_scanbm(crys_ctx* ctx, pipe::BmArgs ba, int pref, const std::string& name, int64_t* cap) {
+  size_t bytes[3] = {0, 0, 0};
+  for (int j = 0; j < D; ++j) bytes[j] = (size_t)ba.words[j] * 4;
+  // placement for shape k: bitmaps in join order while they fit
+  auto place = [&](int k, int32_t* off) {
+    const BmShape& sh = kBmShapes[k];
+    size_t at = ((size_t)sh.s * D * sh.w * 128 * sh.v * 4 + 2 * sh.s * 8 + 127) & ~(size_t)127;
+    bool all = true;
+    for (int j = 0; j < D; ++j) {
+      if (at + bytes[j] <= kSmemOptin) {
+        off[j] = (int32_t)at;
+        at += bytes[j];
+      } else {
+        off[j] = -1;
+        all = false;
+      }
+    }
+    return std::make_pair(all, at);
+  };
+  int k = 0;
+  int32_t off[3] = {-1, -1, -1};
+  if (pref == 0) {  // the deepest ring that keeps every bitmap on chip, else the deepest ring
+    for (k = 0; k < 4 && !place(k, off).first; ++k) {
+    }
+    if (k == 4) k = 0;
+  }
+  const size_t dyn = place(k, off).second;
+  for (int j = 0; j < 3; ++j) ba.smem[j] = j < D ? off[j] : -1;
+  switch (k) {
+    case 0: return launch_scanbm_shape<D, 16, 2, 4>(ctx, ba, dyn, name, cap);
+    case 1: return launch_scanbm_shape<D, 16, 2, 3>(ctx, ba, dyn, name, cap);
+    case 2: return launch_scanbm_shape<D, 16, 2, 2>(ctx, ba, dyn, name, cap);
+    default: return launch_scanbm_shape<D, 16, 1, 4>(ctx, ba, dyn, name, cap);
+  }
 }
 
 // Tuning knob CRYS_PIPE_CFG selects the (consumer warps, tile rows, stages)
@@ -802,6 +882,16 @@ int l2_ahead() {
 int split_env() {
   static const int v = [] {
     const char* e = getenv("CRYS_SPLIT");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+// CRYS_BM=1: split plans (CRYS_SPLIT=D) run late-materialising (membership
+// bitmaps, ssb_scanbm.cuh) with ring preference CRYS_PIPE_CFG.
+int bm_env() {
+  static const int v = [] {
+    const char* e = getenv("CRYS_BM");
     return e ? atoi(e) : 0;
   }();
   return v;
@@ -864,16 +954,22 @@ struct QueryGraph {
 // 0..split-1, then the gather kernel; ssb_gather.cuh).
 struct TuneCand {
   int cfg, l2, split;
+  int bm = 0;  // 1: late-materialising split (membership bitmaps, ssb_scanbm.cuh); cfg = ring preference
 };
 // Split candidates run the dense head with one join (the measured winner
 // whenever join 0 is selective: q3.2-q3.4, q4.3); cfg then names the scan
 // ring shape (launch_emit).  Splitting after two joins was measured slower
 // everywhere (the second join's L2 probes stall the scan's consumers).
-constexpr int kTuneN = 11;
-constexpr TuneCand kTune4[kTuneN] = {{0, 0, 0}, {4, 0, 0}, {3, 0, 0}, {6, 0, 0}, {0, 2, 0}, {4, 2, 0},
-                                     {3, 2, 0}, {6, 2, 0}, {3, 2, 1}, {3, 4, 1}, {2, 2, 1}};
-constexpr int kTuneN6 = 6;
-constexpr TuneCand kTune6[kTuneN6] = {{0, 0, 0}, {0, 2, 0}, {0, 4, 0}, {3, 2, 1}, {3, 4, 1}, {2, 2, 1}};
+// bm candidates: the late-materialising split after two joins (ssb_scanbm.cuh)
+// with L2 look-ahead 0 / 2 / 4 (B200, SF=20: q2.1 0.323 -> 0.237 ms, q2.3
+// 0.289 -> 0.171, q4.2 0.477 -> 0.376).
+constexpr int kTuneN = 14;
+constexpr TuneCand kTune4[kTuneN] = {{0, 0, 0},    {4, 0, 0},    {3, 0, 0},   {6, 0, 0},   {0, 2, 0},
+                                     {4, 2, 0},    {3, 2, 0},    {6, 2, 0},   {3, 2, 1},   {3, 4, 1},
+                                     {2, 2, 1},    {0, 0, 2, 1}, {0, 2, 2, 1}, {0, 4, 2, 1}};
+constexpr int kTuneN6 = 9;
+constexpr TuneCand kTune6[kTuneN6] = {{0, 0, 0}, {0, 2, 0},    {0, 4, 0},    {3, 2, 1},   {3, 4, 1},
+                                      {2, 2, 1}, {0, 0, 2, 1}, {0, 2, 2, 1}, {0, 4, 2, 1}};
 struct PipeTune {
   int chosen = -1;  // index into the plan shape's candidate list once decided
   int ncand = 0;
@@ -895,6 +991,7 @@ struct QueryWorkspace {
   DevBuf result;   // ResultHeader + RowOut[cells]
   DevBuf packed;   // the packed partial of a device group member (NCCL payload)
   DevBuf list;     // split plans: survivor list (uint2 per entry), regions of list_cap
+  DevBuf list4;    // late-materialising plans: {row, key, key, key} per entry
   DevBuf list_count;
   PinnedBuf host;
   HostBox* hbox = nullptr;  // host-mapped digit extents (box_publish_kernel)
@@ -1045,6 +1142,9 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* dimdb, const std::vector
   std::memset(&pa, 0, sizeof(pa));
   int64_t max_rows = 0, max_cap = 0;
   bool any_ht = false;
+  // membership bitmaps of the direct joins (late-materialising plans)
+  const uint32_t* mem[kMaxJoins] = {nullptr, nullptr, nullptr, nullptr};
+  size_t mem_bytes[kMaxJoins] = {0, 0, 0, 0}, mem_off[kMaxJoins];
   if (nj) {
     CRYS_CHECK(nj <= kMaxJoins, CRYS_ENOTBUILT, "at most four joins");
     // group parts -> (join, lo, card, stride): mixed radix, last part fastest
@@ -1059,6 +1159,7 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* dimdb, const std::vector
       stride *= (int64_t)(gp.hi - gp.lo + 1);
     }
     size_t tbl_bytes[kMaxJoins] = {0, 0, 0, 0}, tbl_off[kMaxJoins] = {0, 0, 0, 0}, tbl_total = 0;
+    mem_off[0] = mem_off[1] = mem_off[2] = mem_off[3] = SIZE_MAX;
     constexpr int64_t kMaxDirect = int64_t(1) << 26;  // key-range bound of the direct tables
     for (int j = 0; j < nj; ++j) {
       const DimJoin& dj = plan.joins[j];
@@ -1105,6 +1206,12 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* dimdb, const std::vector
         d.clear_words = (uint32_t)(tbl_bytes[j] / 4);
         tbl_off[j] = tbl_total;
         tbl_total += tbl_bytes[j];
+        // membership bitmap over the same domain (bit nkeys: the absent pad)
+        mem_bytes[j] = ((size_t)(d.nkeys + 1 + 127) / 128) * 16;
+        if (d.kind != kTabBitmap) {
+          mem_off[j] = tbl_total;
+          tbl_total += mem_bytes[j];
+        }
       } else {
         d.kind = kTabHash;
         any_ht = true;
@@ -1132,12 +1239,21 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* dimdb, const std::vector
       pro.tbl[j] = reinterpret_cast<uint32_t*>(da.d[j].tbl);
       pro.words[j] = da.d[j].clear_words;
       pro.value[j] = da.d[j].clear_value;
+      // the join's membership bitmap: the table itself, or the one beside the codes
+      mem[j] = reinterpret_cast<const uint32_t*>(da.d[j].tbl);
+      if (mem_off[j] != SIZE_MAX) {
+        da.d[j].bits = reinterpret_cast<uint32_t*>(ws.tables.as<char>() + mem_off[j]);
+        mem[j] = da.d[j].bits;
+        pro.tbl[kMaxJoins + j] = da.d[j].bits;
+        pro.words[kMaxJoins + j] = (uint32_t)(mem_bytes[j] / 4);
+        pro.value[kMaxJoins + j] = 0u;
+      }
     }
   }
   // ---- launches: prologue, dimension builds
   {
     int64_t work = std::max<int64_t>(pro.zero64_n, pro.zero64b_n);
-    for (int j = 0; j < kMaxJoins; ++j) work = std::max<int64_t>(work, pro.words[j]);
+    for (int j = 0; j < 2 * kMaxJoins; ++j) work = std::max<int64_t>(work, pro.words[j]);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, (int64_t)ctx->num_sms * 4));
     query_prologue_kernel<<<grid, 256, 0, st>>>(pro);
     CRYS_LAUNCHED("query_prologue_kernel");
@@ -1176,6 +1292,12 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* dimdb, const std::vector
     pa.surv = d_surv;
     pa.err = d_err;
     CRYS_CHECK(plan.agg != kAggExtPriceTimesDiscount, CRYS_ENOTBUILT, "join flights aggregate revenue");
+    // late materialisation needs direct tables (membership bitmaps) for joins 0..D-1
+    auto bm_eligible = [&](int D) {
+      for (int j = 0; j < D; ++j)
+        if (!mem[j]) return false;
+      return true;
+    };
     auto launch = [&](TuneCand c) {
       pa.l2_ahead = c.l2;
       for (size_t f = 0; f < facts.size(); ++f) {
@@ -1193,7 +1315,58 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* dimdb, const std::vector
         const bool shape3 = nj == 3 && plan.agg == kAggRevenue;
         const bool shape4 = nj == 4 && plan.agg == kAggRevenueMinusSupplyCost;
         CRYS_CHECK(shape3 || shape4, CRYS_ENOTBUILT, "no fused pipeline for this plan shape");
-        if (c.split > 0 && c.split < nj) {  // dense joins 0..D-1, survivor list, gather tail
+        if (c.bm && c.split > 0 && c.split < nj && bm_eligible(c.split)) {  // late materialisation
+          const int D = c.split;
+          pipe::BmArgs ba;
+          std::memset(&ba, 0, sizeof(ba));
+          ba.n = pa.n;
+          int npre = 0, pre_j[3] = {-1, -1, -1};
+          for (int j = 0; j < D; ++j) {
+            ba.col[j] = pa.col[j];
+            ba.bm[j] = mem[j];
+            ba.kmin[j] = pa.tab[j].kmin;
+            ba.nk[j] = pa.tab[j].n;
+            ba.words[j] = (uint32_t)(mem_bytes[j] / 4);
+            if (pa.tab[j].gstride != 0) pre_j[npre++] = j;
+          }
+          for (int w = 0; w < 3; ++w) ba.key_of[w] = pre_j[w];
+          ba.list = ws.list4.as<uint4>();
+          ba.list_cap = (int64_t)(ws.list4.bytes / sizeof(uint4));
+          ba.list_count = ws.list_count.as<unsigned>();
+          ba.surv = pa.surv;
+          ba.l2_ahead = c.l2;
+          int64_t cap = 0;
+          const int grid = D == 1   ? launch_scanbm<1>(ctx, ba, c.cfg, plan.name, &cap)
+                           : D == 2 ? launch_scanbm<2>(ctx, ba, c.cfg, plan.name, &cap)
+                                    : launch_scanbm<3>(ctx, ba, c.cfg, plan.name, &cap);
+          pipe::GatherArgs ga;
+          std::memset(&ga, 0, sizeof(ga));
+          ga.list4 = ba.list;
+          ga.list_cap = cap;
+          ga.list_count = ba.list_count;
+          const int nb = nj - D;
+          for (int j = 0; j < nb; ++j) {
+            ga.col[j] = pa.col[D + j];
+            ga.tab[j] = pa.tab[D + j];
+          }
+          ga.col[nb] = pa.col[nj];
+          ga.col[nb + 1] = pa.col[nj + 1];
+          for (int p = 0; p < npre; ++p) ga.pre[p] = pa.tab[pre_j[p]];
+          ga.meta = pa.meta;
+          ga.cells = (int32_t)cells;
+          ga.g_sum = pa.g_sum;
+          ga.g_cnt = pa.g_cnt;
+          ga.surv = pa.surv + D;
+          ga.err = pa.err;
+          if (shape3 && nb == 1) gather_pre<1, 1>(ctx, ga, grid, cells, plan.name, npre);
+          else if (shape3 && nb == 2) gather_pre<2, 1>(ctx, ga, grid, cells, plan.name, npre);
+          else if (shape4 && nb == 1) gather_pre<1, 2>(ctx, ga, grid, cells, plan.name, npre);
+          else if (shape4 && nb == 2) gather_pre<2, 2>(ctx, ga, grid, cells, plan.name, npre);
+          else gather_pre<3, 2>(ctx, ga, grid, cells, plan.name, npre);
+          count_launch(ctx, 2);
+          continue;
+        }
+        if (c.split > 0 && c.split < nj && !c.bm) {  // dense joins 0..D-1, survivor list, gather tail
           const int D = c.split, nb = nj - D;
           pipe::PipeArgs pe = pa;
           pe.cells = 0;
@@ -1240,10 +1413,11 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* dimdb, const std::vector
       int64_t nmax = 0;
       for (int64_t r : nrows) nmax = std::max(nmax, r);
       ws.list.reserve(sizeof(uint2) * (size_t)(nmax + ((int64_t)ctx->num_sms * 4 + 1) * 4096));
+      ws.list4.reserve(sizeof(uint4) * (size_t)(nmax + ((int64_t)ctx->num_sms + 1) * 4096));
       ws.list_count.reserve(sizeof(unsigned) * (size_t)ctx->num_sms * 8);
     }
     const int cfg = pipe_cfg();  // CRYS_PIPE_CFG > 0 forces an instantiation
-    TuneCand run{cfg, l2_ahead(), split_env()};
+    TuneCand run{cfg, l2_ahead(), split_env(), bm_env()};
     const TuneCand* cands = nj == 3 ? kTune4 : kTune6;
     const int ncand = nj == 3 ? kTuneN : kTuneN6;
     if (cfg == 0 && l2_ahead() == 0 && split_env() == 0 && (nj == 3 || nj == 4) && tune_enabled() && tune_ok) {

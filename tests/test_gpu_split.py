@@ -1,6 +1,7 @@
-"""Split SSB plans (csrc/ssb_scan.cuh + ssb_gather.cuh: the first D joins
-streamed densely into a survivor list, the rest of the plan gathered at the
-listed rows) forced for every join query with CRYS_SPLIT=D, D in {1, 2, 3},
+"""Split SSB plans (csrc/ssb_scan.cuh or, with CRYS_BM=1, ssb_scanbm.cuh +
+ssb_gather.cuh: the first D joins streamed densely into a survivor list, the
+rest of the plan gathered at the listed rows) forced for every join query
+with CRYS_SPLIT=D, D in {1, 2, 3},
 against the reference's goldens (fixture, SF=1, SF=20).  The knob is read
 once per process, so each D runs in a child process; the autotuner picks
 split plans by itself in the default configuration."""
@@ -38,10 +39,13 @@ print(json.dumps(out))
 """
 
 
+@pytest.mark.parametrize("bm", [0, 1])
 @pytest.mark.parametrize("split", [1, 2, 3])
-def test_split_plans_match_goldens(split):
+def test_split_plans_match_goldens(split, bm):
+    """bm=1: the late-materialising head (membership bitmaps, ssb_scanbm.cuh)
+    with the uint4 survivor list and the digit joins resolved in the gather."""
     code = CHILD % {"root": ROOT, "tests": os.path.join(ROOT, "tests"), "split": split}
-    env = dict(os.environ, CRYS_SPLIT=str(split))
+    env = dict(os.environ, CRYS_SPLIT=str(split), CRYS_BM=str(bm))
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=900, env=env)
     assert r.returncode == 0, r.stderr[-3000:]
     res = json.loads(r.stdout.strip().splitlines()[-1])

@@ -1,9 +1,11 @@
 """A/B of the split SSB plans on one B200: for CRYS_SPLIT in {0 (all-dense
-fused pipeline), 1, 2, 3}, every join query at SF (default 20) -- fused-pass
-device time (median of reps, CUDA events inside the library) and a golden
-check.  One process per split value (the knob is read once).
+fused pipeline), 1, 2, 3} (with --bm: CRYS_BM=1, the late-materialising
+membership-bitmap head, and CRYS_PIPE_CFG = ring preference), every join
+query at SF (default 20) -- fused-pass device time (median of reps, CUDA
+events inside the library) and a golden check.  One process per setting (the
+knobs are read once).
 
-    python tools/split_probe.py [--sf 20] [--reps 5]"""
+    python tools/split_probe.py [--sf 20] [--reps 5] [--bm] [--splits 0,1,2,3] [--pref 0]"""
 import json
 import os
 import statistics
@@ -48,13 +50,17 @@ def main():
     ap.add_argument("--sf", type=int, default=20)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--child", action="store_true")
+    ap.add_argument("--bm", action="store_true")
+    ap.add_argument("--splits", default="0,1,2,3")
+    ap.add_argument("--pref", default="0")
     args = ap.parse_args()
     if args.child:
         child(args.sf, args.reps)
         return
     res = {}
-    for split in (0, 1, 2, 3):
-        env = dict(os.environ, CRYS_SPLIT=str(split), CRYS_PIPE_CFG=os.environ.get("CRYS_PIPE_CFG", "0"))
+    for split in map(int, args.splits.split(",")):
+        env = dict(os.environ, CRYS_SPLIT=str(split), CRYS_PIPE_CFG=args.pref if args.bm else
+                   os.environ.get("CRYS_PIPE_CFG", "0"), CRYS_BM="1" if args.bm else "0")
         r = subprocess.run([sys.executable, __file__, "--child", "--sf", str(args.sf), "--reps", str(args.reps)],
                            capture_output=True, text=True, env=env, timeout=900)
         if r.returncode != 0:
