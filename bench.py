@@ -684,6 +684,40 @@ def run_ours(args, rank, world):
     return out, sh, sf
 
 
+def sf100_point(args, ctx):
+    """The N>1 runs' workload (BASELINE configs[4]: the SF=100 suite) on this
+    one GPU, so a scaling curve compares the same work at every N: the N=1
+    headline stays SF=20 (configs[3]); this is the SF=100 N=1 point."""
+    import torch
+    from paper_2003_01178_b200 import tq
+    torch.cuda.empty_cache()
+    db = tq.DeviceDatabase.generate(100, 42, ctx=ctx)
+    cfg = tq.TileConfig(args.bt, args.ipt)
+
+    def step():
+        for q in range(13):
+            tq.run_query(db, q, cfg)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    steps = max(1, min(args.steps, 5))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    rows = 6_000_000 * 100
+    db.free()
+    torch.cuda.empty_cache()
+    return {"workload": "SSB 13-query suite SF=100 (configs[4]) on one GPU", "sf": 100, "steps": steps,
+            "ms_per_step": round(ms, 4),
+            "value": round(sum(fact_bytes(q, rows) for q in range(13)) / (ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+            "note": "same metric as the N>1 lines (strong scaling over SF=100); the headline N=1 value is SF=20"}
+
+
 def suite_upload_order():
     """(table, column) of every column the 13 plans read, in first-use order,
     so the suite's first queries overlap the upload of later queries' columns."""
@@ -789,6 +823,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ops", action="store_true", help="skip the operator block (select/project/join/sort)")
+    ap.add_argument("--no-scale-point", action="store_true",
+                    help="skip the SF=100 one-GPU point (the N>1 runs' workload)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps
@@ -817,6 +853,9 @@ def main():
     e2e = None if args.no_e2e else e2e_host(args, sh, sf, rank, world)
     if rank == 0:
         line["e2e"] = e2e
+        if world == 1 and not args.no_scale_point and (args.sf or 20) != 100:
+            sh.db.free()
+            line["sf100_one_gpu"] = sf100_point(args, sh.ctx)
         if world == 1 and not args.no_ops:
             sh.db.free()
             import torch

@@ -410,6 +410,172 @@ __global__ void __launch_bounds__(BT) select_seg_kernel(const int32_t* __restric
   for (int i = threadIdx.x; i < (int)mine; i += BT) __stcs(out + off + i, s_items[i]);
 }
 
+// Round-robin persistent select (the default input-order path): every input
+// row is read from HBM ONCE, then once more from L2, with no chained
+// look-back.  Grid = two co-resident CTAs per SM (cooperative launch).  Round k
+// is the segment [k SEG, (k+1) SEG) (SEG = G CTAs x W warps x WU rows, ~16 MB:
+// L2-sized); warp w of CTA c owns the contiguous WU rows at (c W + w) WU.
+//   iteration k:  COUNT round k (128-bit loads, L2 evict_last) -> the warp's
+//                 count in smem, the CTA's in counts[k][c] (+1: 0 = not yet);
+//                 WRITE round k - LAG (re-read from L2, evict_first): offset =
+//                 rows before the round + the round's counts of CTAs < c + the
+//                 counts of warps < w; per 32-row group one ballot, stores
+//                 straight to global memory in input order.
+// A CTA keeps its own running base (it reads all G counts of every round),
+// so the only cross-CTA dependence is "round k - LAG has been counted", which
+// was published a whole count phase earlier: the exchange latency (~2 us
+// under full HBM load) is hidden behind that phase instead of chaining tile
+// after tile like a decoupled look-back (profiles/r01_select_tuning.txt).
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned lanemask_lt_u32() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+__device__ __forceinline__ int32_t ld_hint1(const int32_t* p, uint64_t pol) {
+  int32_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
+}
+
+constexpr int kRrMaxG = 32 * 16;  // counts per round read by one warp (<= 16 per lane)
+
+template <int BT, int WU, int LAG, int UW>
+__global__ void __launch_bounds__(BT, 2) select_rr_kernel(const int32_t* __restrict__ in, int64_t n, int32_t lo,
+                                                          int32_t hi, int32_t* __restrict__ out, int rounds,
+                                                          uint32_t* counts, long long* total_out) {
+  constexpr int W = BT / 32;
+  constexpr int PER = (kRrMaxG + 31) / 32;
+  constexpr int U = WU >= 1024 ? 8 : WU / 128;  // count phase: 128-bit loads in flight per lane
+  constexpr int NS = LAG + 1;                   // rounds in flight per CTA
+  static_assert(WU % (128 * U) == 0 && WU % (32 * UW) == 0, "warp unit");
+  __shared__ int s_wc[NS][W];
+  __shared__ long long s_off;
+  const int G = gridDim.x, c = blockIdx.x;
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  const unsigned lt = lanemask_lt_u32();
+  const uint32_t span = (uint32_t)hi - (uint32_t)lo;  // lo <= x <= hi  <=>  x - lo <= hi - lo (unsigned)
+  const int64_t seg = (int64_t)G * W * WU;
+  const uint64_t keep = pipe::policy_evict_last(), drop = pipe::policy_evict_first();
+  const bool vec_ok = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+  long long base = 0;   // warp 0: rows selected in rounds [0, resolved)
+  int resolved = 0;     // warp 0: rounds whose totals are in base
+  long long mine = 0;   // thread 0: this CTA's selected rows (the grand total is their sum)
+  for (int k = 0; k < rounds + LAG; ++k) {
+    const int j = k - LAG;
+    uint32_t cv[PER];  // warp 0: the counts of round j, in flight during the count phase
+    if (warp == 0 && j >= 0) {
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const int cc = i * 32 + (int)lane;
+        cv[i] = cc < G ? ld_relaxed_u32(counts + (size_t)j * G + cc) : 1u;
+      }
+    }
+    if (k < rounds) {  // ---- COUNT round k
+      const int64_t r0 = k * seg + ((int64_t)c * W + warp) * WU;
+      int cnt = 0;
+      if (vec_ok && r0 + WU <= n) {
+        for (int u = 0; u < WU; u += 128 * U) {
+          int4 v[U];
+#pragma unroll
+          for (int q = 0; q < U; ++q) v[q] = ld_hint4(in + r0 + u + q * 128 + 4 * lane, keep);
+#pragma unroll
+          for (int q = 0; q < U; ++q)
+            cnt += ((uint32_t)v[q].x - (uint32_t)lo <= span) + ((uint32_t)v[q].y - (uint32_t)lo <= span) +
+                   ((uint32_t)v[q].z - (uint32_t)lo <= span) + ((uint32_t)v[q].w - (uint32_t)lo <= span);
+        }
+      } else {
+        for (int64_t i = r0 + lane; i < min(r0 + WU, n); i += 32)
+          cnt += (uint32_t)ld_hint1(in + i, keep) - (uint32_t)lo <= span;
+      }
+      cnt = warp_sum(cnt);
+      if (lane == 0) s_wc[k % NS][warp] = cnt;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int tot = 0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) tot += s_wc[k % NS][w];
+        st_relaxed_u32(counts + (size_t)k * G + c, (uint32_t)tot + 1u);
+        mine += tot;
+      }
+    }
+    if (j < 0) continue;  // uniform
+    {  // a round this CTA selected nothing from needs no offset: no exchange wait
+      int any = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) any |= s_wc[j % NS][w];
+      if (!any) continue;  // uniform
+    }
+    if (warp == 0) {  // ---- offset of this CTA's share of round j
+      for (; resolved < j; ++resolved) {  // totals of skipped rounds (rare: only near-empty selections)
+        long long t = 0;
+        for (int cc = (int)lane; cc < G; cc += 32) {
+          uint32_t x;
+          while ((x = ld_relaxed_u32(counts + (size_t)resolved * G + cc)) == 0u) __nanosleep(32);
+          t += (long long)x - 1;
+        }
+        base += warp_sum(t);
+      }
+      long long before = 0, all = 0;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const int cc = i * 32 + (int)lane;
+        while (cv[i] == 0u) {
+          __nanosleep(32);
+          cv[i] = ld_relaxed_u32(counts + (size_t)j * G + cc);
+        }
+        const long long x = cc < G ? (long long)cv[i] - 1 : 0;
+        all += x;
+        before += cc < c ? x : 0;
+      }
+      before = warp_sum(before);
+      all = warp_sum(all);
+      if (lane == 0) s_off = base + before;
+      base += all;
+      resolved = j + 1;
+    }
+    __syncthreads();  // s_off published (the next write of s_off follows the next count barrier)
+    // ---- WRITE round j: this warp's rows, re-read from L2, in input order
+    if (s_wc[j % NS][warp] == 0) continue;  // nothing selected in this warp's rows: no re-read
+    long long off = s_off;
+#pragma unroll
+    for (int w = 0; w < W; ++w) off += w < (int)warp ? s_wc[j % NS][w] : 0;
+    int32_t* o = out + off;
+    const int64_t r0 = j * seg + ((int64_t)c * W + warp) * WU;
+    if (r0 + WU <= n) {
+      for (int u = 0; u < WU; u += 32 * UW) {
+        int32_t x[UW];
+#pragma unroll
+        for (int q = 0; q < UW; ++q) x[q] = ld_hint1(in + r0 + u + q * 32 + lane, drop);
+#pragma unroll
+        for (int q = 0; q < UW; ++q) {
+          const bool p = (uint32_t)x[q] - (uint32_t)lo <= span;
+          const unsigned m = __ballot_sync(0xffffffffu, p);
+          if (p) __stcs(o + __popc(m & lt), x[q]);
+          o += __popc(m);
+        }
+      }
+    } else {
+      for (int64_t i0 = r0; i0 < min(r0 + WU, n); i0 += 32) {
+        const int64_t i = i0 + lane;
+        const int32_t x = i < n ? ld_hint1(in + i, drop) : 0;
+        const bool p = i < n && (uint32_t)x - (uint32_t)lo <= span;
+        const unsigned m = __ballot_sync(0xffffffffu, p);
+        if (p) __stcs(o + __popc(m & lt), x);
+        o += __popc(m);
+      }
+    }
+  }
+  if (threadIdx.x == 0 && mine) atomicAdd(reinterpret_cast<unsigned long long*>(total_out), (unsigned long long)mine);
+}
+
 __global__ void select_seg_total_kernel(const unsigned long long* stot, long long nseg, long long* total_out) {
   unsigned long long t = 0;
   for (long long i = threadIdx.x; i < nseg; i += 32) t += stot[i];
@@ -908,7 +1074,8 @@ constexpr int kJR = kJTile / kJW;
 template <int STAGES, bool SMEM>
 __global__ void __launch_bounds__((kJW + 1) * 32, 1) join_ring_kernel(
     const int32_t* __restrict__ keys, const int32_t* __restrict__ pays, int64_t n,
-    const int2* __restrict__ gslots, uint32_t mask, int shift, unsigned long long* out, int l2_ahead) {
+    const int2* __restrict__ gslots, uint32_t mask, int shift, unsigned long long* out, int l2_ahead,
+    uint32_t slo, uint32_t shi) {
   constexpr int IT = kJR / 32;  // rows per lane per stage
   extern __shared__ __align__(128) unsigned char smem[];
   int32_t* ring = reinterpret_cast<int32_t*>(smem);
@@ -990,9 +1157,11 @@ __global__ void __launch_bounds__((kJW + 1) * 32, 1) join_ring_kernel(
 #pragma unroll
       for (int i = 0; i < IT; ++i) {
         const int row = (i / 4) * 128 + lane * 4 + (i & 3);
-        if (row < valid && k[i] != kEmptyKey) {  // INT32_MIN is unstorable: always a miss
+        // INT32_MIN is unstorable: always a miss.  A multi-pass probe takes
+        // only the keys whose home slot is in this pass's slice [slo, shi).
+        sl[i] = ht_slot_of(k[i], shift);
+        if (row < valid && k[i] != kEmptyKey && sl[i] - slo < shi - slo) {
           pending |= 1u << i;
-          sl[i] = ht_slot_of(k[i], shift);
           e[i] = SMEM ? slots[sl[i]] : __ldg(slots + sl[i]);
         }
       }
@@ -1217,6 +1386,44 @@ int64_t join_part_min_bytes() {
   return v;
 }
 
+// CRYS_JOIN_PART_MINK: at least 2^k buckets in the partitioned probe (few
+// buckets serialise the scatter's shared-memory rank atomics).
+int join_part_min_k() {
+  static const int v = [] {
+    const char* e = getenv("CRYS_JOIN_PART_MINK");
+    return e ? std::max(0, std::min(8, atoi(e))) : 0;
+  }();
+  return v;
+}
+
+// CRYS_JOIN_PASS_MB: tables larger than this (and below the partitioned
+// sizes) are probed in ceil(table / this) slot-slice passes (0 = one pass).
+int64_t join_pass_bytes() {
+  static const int64_t v = [] {
+    const char* e = getenv("CRYS_JOIN_PASS_MB");
+    return (int64_t)(e ? atoll(e) : 0) << 20;
+  }();
+  return v;
+}
+
+// Ring depth of the probe through L2 (2, 4 or 6 stages of 32 KB).  A random
+// probe costs one L1tex wavefront per lane (~1 line per SM-cycle: 2^28 probes
+// >= 0.92 ms on 148 SMs), so what is left to win is L1 hits: a shallower ring
+// leaves more of the SM's 256 KB to cache table lines.  Measured on B200
+// (2^28 probes, profiles/r02_join_stages.txt): 2 stages are fastest up to
+// 8 MB and from 64 MB on (64 MB 3.45 -> 2.42 ms, 1 GB partitioned 2.63 ->
+// 2.32), 4 stages at 16-32 MB.  CRYS_JOIN_L2_STAGES forces one.
+int join_l2_stages(size_t tbytes, bool partitioned) {
+  static const int v = [] {
+    const char* e = getenv("CRYS_JOIN_L2_STAGES");
+    const int x = e ? atoi(e) : 0;
+    return x == 2 || x == 4 || x == 6 ? x : 0;
+  }();
+  if (v) return v;
+  if (partitioned) return 2;
+  return tbytes > (8u << 20) && tbytes < (48u << 20) ? 4 : 2;
+}
+
 int join_l2_ahead(bool table_on_chip) {
   static const int v = [] {
     const char* e = getenv("CRYS_JOIN_L2");
@@ -1268,6 +1475,45 @@ void launch_scan(const ScanBufs& b, int64_t ntiles, cudaStream_t st) {
   select_scan_blocks_kernel<<<1, 1024, 0, st>>>(b.btot, b.nblk, b.bases);
 }
 
+// CRYS_SEL_RR: round-robin select instantiation <threads, rows per warp per
+// round, lag, write loads per lane> (the table in rr_plan).
+int sel_rr_variant() {
+  static const int v = [] {
+    const char* e = getenv("CRYS_SEL_RR");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+struct RrLaunch {
+  const void* fn = nullptr;
+  int bt = 0, grid = 0, rounds = 0;
+  uint32_t* counts = nullptr;
+};
+
+RrLaunch rr_plan(crys_ctx* ctx, int64_t n) {
+  RrLaunch r;
+  int wu = 0;
+  auto pick = [&](auto fn, int bt, int rows_per_warp) {
+    r.fn = (const void*)fn;
+    r.bt = bt;
+    wu = rows_per_warp;
+  };
+  switch (sel_rr_variant()) {  // segment = 296 CTAs x warps x rows per warp (x 4 B)
+    case 1: pick(select_rr_kernel<512, 1024, 2, 16>, 512, 1024); break;  // 19.4 MB, lag 2, 16 loads
+    case 2: pick(select_rr_kernel<512, 768, 2, 8>, 512, 768); break;     // 14.5 MB, lag 2
+    case 3: pick(select_rr_kernel<512, 768, 3, 8>, 512, 768); break;     // 14.5 MB, lag 3
+    case 4: pick(select_rr_kernel<512, 1024, 2, 4>, 512, 1024); break;   // 19.4 MB, lag 2, 4 loads
+    default: pick(select_rr_kernel<512, 1024, 2, 8>, 512, 1024); break;  // 19.4 MB, lag 2
+  }
+  const int per_sm = occupancy(r.fn, r.bt, 0);
+  const int64_t per_cta = (int64_t)(r.bt / 32) * wu;
+  r.grid = (int)std::min<int64_t>({(int64_t)per_sm * ctx->num_sms, (int64_t)kRrMaxG, (n + per_cta - 1) / per_cta});
+  const int64_t seg = (int64_t)r.grid * per_cta;
+  r.rounds = (int)((n + seg - 1) / seg);
+  return r;
+}
+
 }  // namespace
 
 int64_t select_i32(crys_ctx* ctx, const int32_t* d_in, int64_t n, int32_t lo, int32_t hi,
@@ -1292,14 +1538,36 @@ int64_t select_i32(crys_ctx* ctx, const int32_t* d_in, int64_t n, int32_t lo, in
     dyn = sizeof(int32_t) * (size_t)(2 * chunk + pairs);
   }
   const int64_t ntiles = (n + tile - 1) / tile;
-  ctx->status.reserve(sizeof(unsigned long long) * (size_t)(ntiles + 3));
+  // the round-robin path (default for 16 B-aligned input): its per-round
+  // counts share the zeroed status buffer
+  RrLaunch rr{};
+  // (lo > hi is the empty predicate: the segmented path handles it; the
+  // round-robin kernel tests x - lo <= hi - lo unsigned)
+  if (order == CRYS_ORDER_INPUT && cfg == 0 && lo <= hi)
+    rr = rr_plan(ctx, n);
+  const size_t words = (size_t)(ntiles + 3) + (rr.fn ? (size_t)(rr.rounds * (int64_t)rr.grid + 1) / 2 : 0);
+  ctx->status.reserve(sizeof(unsigned long long) * words);
   auto* status = ctx->status.as<unsigned long long>();
   auto* total = reinterpret_cast<long long*>(status + ntiles + 1);
-  CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(unsigned long long) * (size_t)(ntiles + 3), st));
+  if (rr.fn) rr.counts = reinterpret_cast<uint32_t*>(status + ntiles + 3);
+  CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(unsigned long long) * words, st));
   timing_kernel_begin(ctx);
   if (order == CRYS_ORDER_INPUT) {
     constexpr int BT = 128, IPT = 32;
-    if (cfg == 1) {
+    if (rr.fn) {
+      cudaLaunchConfig_t lc = {};
+      lc.gridDim = dim3((unsigned)rr.grid);
+      lc.blockDim = dim3((unsigned)rr.bt);
+      lc.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeCooperative;  // every CTA co-resident (they wait on each other's counts)
+      attr[0].val.cooperative = 1;
+      lc.attrs = attr;
+      lc.numAttrs = 1;
+      void* args[] = {(void*)&d_in, (void*)&n, (void*)&lo, (void*)&hi, (void*)&d_out, (void*)&rr.rounds,
+                      (void*)&rr.counts, (void*)&total};
+      CUDA_TRY(cudaLaunchKernelExC(&lc, rr.fn, args));
+    } else if (cfg == 1) {
       select_input_kernel<BT, IPT><<<(unsigned)ntiles, BT, 0, st>>>(d_in, n, lo, hi, d_out, status, ntiles, total);
     } else if (cfg != 3) {
       const long long seg = sel_seg();
@@ -1454,16 +1722,16 @@ int64_t join_probe_sum(crys_ctx* ctx, const int32_t* d_keys, const int32_t* d_pa
       auto fn = join_ring_kernel<2, true>;
       ensure_dyn_smem((const void*)fn, ring2 + tbytes);
       fn<<<grid, (kJW + 1) * 32, ring2 + tbytes, st>>>(d_keys, d_payloads, n, ht->slots.as<int2>(), mask,
-                                                       ht->shift, out, join_l2_ahead(true));
+                                                       ht->shift, out, join_l2_ahead(true), 0u, ~0u);
     } else if (smem) {
       auto fn = join_ring_kernel<4, true>;
       ensure_dyn_smem((const void*)fn, ring4 + tbytes);
       fn<<<grid, (kJW + 1) * 32, ring4 + tbytes, st>>>(d_keys, d_payloads, n, ht->slots.as<int2>(), mask,
-                                                       ht->shift, out, join_l2_ahead(true));
+                                                       ht->shift, out, join_l2_ahead(true), 0u, ~0u);
     } else {
       const int64_t pmin = join_part_min_bytes();
       const int logcap = 32 - ht->shift;
-      int k = 0;  // buckets of <= join_part_slice() table slices
+      int k = std::min(join_part_min_k(), logcap);  // buckets of <= join_part_slice() table slices
       while (k < 8 && k < logcap && (tbytes >> k) > join_part_slice()) ++k;
       const int32_t* pk = d_keys;
       const int32_t* pp = d_payloads;
@@ -1486,10 +1754,33 @@ int64_t join_probe_sum(crys_ctx* ctx, const int32_t* d_keys, const int32_t* d_pa
         pk = ok;
         pp = op;
       }
-      auto fn = join_ring_kernel<6, false>;
-      ensure_dyn_smem((const void*)fn, ring6);
-      fn<<<grid, (kJW + 1) * 32, ring6, st>>>(pk, pp, n, ht->slots.as<int2>(), mask, ht->shift,
-                                              out, join_l2_ahead(false));
+      // Tables between the on-chip sizes and the partitioned ones: K passes
+      // over the probe stream, pass p probing only the keys whose home slot
+      // lies in slice p (cap / K slots), so each pass's slice stays
+      // L2-resident (the streamed keys/payloads are evict_first).
+      int passes = 1;
+      if (pk == d_keys) {
+        const int64_t slice = join_pass_bytes();
+        if (slice > 0 && (int64_t)tbytes > slice)
+          passes = (int)std::min<int64_t>(16, ((int64_t)tbytes + slice - 1) / slice);
+      }
+      const int stages = join_l2_stages(tbytes, pk != d_keys);
+      const void* fnp = stages == 2 ? (const void*)join_ring_kernel<2, false>
+                      : stages == 4 ? (const void*)join_ring_kernel<4, false>
+                                    : (const void*)join_ring_kernel<6, false>;
+      const size_t ring = stages == 2 ? ring2 : stages == 4 ? ring4 : ring6;
+      ensure_dyn_smem(fnp, ring);
+      const uint64_t cap = (uint64_t)ht->capacity;
+      for (int p = 0; p < passes; ++p) {
+        const uint32_t slo = passes == 1 ? 0u : (uint32_t)(cap * p / passes);
+        const uint32_t shi = passes == 1 ? ~0u : (uint32_t)(cap * (p + 1) / passes);
+        const int2* slots = ht->slots.as<int2>();
+        int l2a = join_l2_ahead(false);
+        void* args[] = {(void*)&pk, (void*)&pp, (void*)&n, (void*)&slots, (void*)&mask, (void*)&ht->shift,
+                        (void*)&out, (void*)&l2a, (void*)&slo, (void*)&shi};
+        CUDA_TRY(cudaLaunchKernel(fnp, dim3(grid), dim3((kJW + 1) * 32), args, ring, st));
+      }
+      count_launch(ctx, passes - 1);
     }
     timing_kernel_end(ctx);
     count_launch(ctx);

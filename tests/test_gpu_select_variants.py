@@ -32,7 +32,7 @@ print("ok")
 """ % ROOT
 
 
-@pytest.mark.parametrize("env", [{"CRYS_SEL_RR": "0"}, {"CRYS_SEL_RR": "1"}, {"CRYS_SEL_RR": "2"},
+@pytest.mark.parametrize("env", [{"CRYS_SEL_RR": "0"}, {"CRYS_SEL_RR": "1"}, {"CRYS_SEL_RR": "2"}, {"CRYS_SEL_RR": "3"}, {"CRYS_SEL_RR": "4"},
                                  {"CRYS_SEL_CFG": "2"}, {"CRYS_SEL_CFG": "3"}])
 def test_input_order_variants(env):
     e = dict(os.environ)

@@ -19,7 +19,7 @@ if [[ $what == ncu || $what == all ]]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
      --log-file $OUT/launches.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-ops > $OUT/ncu_bench.log 2>&1
   SUITE=1 timeout 900 ncu --set full --clock-control none --import-source on \
-     --nvtx --nvtx-include "profiled/" -k 'regex:ssb_(flight1|pipeline|scan_emit|gather)' -c 30 \
+     --nvtx --nvtx-include "profiled/" -k 'regex:ssb_(flight1|pipeline|scan_emit|scan_bm|gather)' -c 30 \
      -o $OUT/prof_suite -f python tools/profile_query.py > $OUT/ncu_full.log 2>&1
 fi
 echo done
