@@ -108,6 +108,14 @@ __device__ __forceinline__ void st_stream4f(float* p, float4 v) {
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
+// Programmatic dependent launch: a kernel launched with the programmatic
+// stream-serialization attribute (launch_k) may become resident while its
+// predecessor in the stream still runs.  pdl_wait() blocks until that
+// predecessor grid has completed and its writes are visible (a no-op for a
+// normally launched kernel); pdl_trigger() lets the successor start launching.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 template <class T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

@@ -6,6 +6,7 @@
 #include <map>
 #include <memory>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -209,6 +210,28 @@ void ensure_dyn_smem(const void* fn, size_t bytes);
 
 // Launch accounting + event timing helpers.
 inline void count_launch(crys_ctx* c, int n = 1) { c->launches += n; }
+
+// CRYS_PDL=1: launch_k chains a query's kernels with programmatic dependent launch.
+bool pdl_enabled();
+
+// A kernel launch that may overlap its stream predecessor's tail (programmatic
+// stream serialization): the kernel must pdl_wait() before it reads anything
+// the predecessor wrote (common.cuh).  Captured into CUDA graphs as a
+// programmatic edge.
+template <typename... KArgs, typename... Args>
+void launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = grid;
+  lc.blockDim = block;
+  lc.dynamicSmemBytes = smem;
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = pdl_enabled() ? 1 : 0;
+  CUDA_TRY(cudaLaunchKernelEx(&lc, k, std::forward<Args>(args)...));
+}
 void timing_begin(crys_ctx* c);
 void timing_kernel_begin(crys_ctx* c);
 void timing_kernel_end(crys_ctx* c);

@@ -38,6 +38,7 @@
 // with all three gathered per date survivor).
 template <int W, int V, int STAGES, int PR, bool ST = false, int D = 1, bool CHN = false>
 __global__ void __launch_bounds__((W + 1) * 32, 1) ssb_flight1_ring_kernel(const Flight1Args a) {
+  pdl_trigger();
   static_assert(D == 1 || D == 2, "dense ring columns");
   // chained level 1: the discount (D == 1) or the quantity (D == 2)
   constexpr int R = 128 * V;   // rows per consumer warp per stage
@@ -256,6 +257,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) ssb_flight1_ring_kernel(const
     red[1][warp] = wc;
   }
   asm volatile("bar.sync 1, %0;" ::"n"(W * 32));  // consumers only
+  pdl_wait();  // the prologue zeroed the aggregate (the scan above overlapped it)
   if (threadIdx.x == 0) {
     long long s = 0, c = 0;
     for (int w = 0; w < W; ++w) {

@@ -174,6 +174,7 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // ---------------------------------------------------------- prologue
 
 __global__ void query_prologue_kernel(const PrologueArgs a) {
+  pdl_trigger();
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int j = 0; j < 2 * kMaxJoins; ++j) {
@@ -212,11 +213,48 @@ __device__ __forceinline__ bool claim_code(void* tbl, uint32_t off, uint32_t cod
   return ((old >> sh) & kMask) == kMask;
 }
 
+// Warp-aggregated forms for a warp whose lanes hold the consecutive offsets
+// off0 .. off0 + 31 (lane l: off0 + l).  warp_bitmap_or sets the bits of the
+// lanes in `bal` with at most two atomics and returns, per lane, whether its
+// bit was already set.
+__device__ __forceinline__ bool warp_bitmap_or(uint32_t* bm, uint32_t off0, unsigned bal, unsigned lane) {
+  const uint32_t w0 = off0 >> 5, s = off0 & 31u;
+  const uint32_t lo = bal << s, hi = s ? bal >> (32u - s) : 0u;
+  uint32_t o0 = 0, o1 = 0;
+  if (lane == 0) {
+    if (lo) o0 = atomicOr(bm + w0, lo);
+    if (hi) o1 = atomicOr(bm + w0 + 1, hi);
+  }
+  o0 = __shfl_sync(0xffffffffu, o0, 0);
+  o1 = __shfl_sync(0xffffffffu, o1, 0);
+  const uint32_t p = s + lane;
+  return (((p < 32u ? o0 : o1) >> (p & 31u)) & 1u) != 0u;
+}
+
+// claim_code for the lanes with `pass`, off0 aligned to the codes per word:
+// the lanes sharing a word AND their masks together, one atomic per word.
+template <int BITS>
+__device__ __forceinline__ bool warp_claim_code(void* tbl, uint32_t off0, bool pass, uint32_t code, unsigned lane) {
+  constexpr uint32_t kMask = (1u << BITS) - 1u;
+  constexpr uint32_t kPer = 32 / BITS;
+  const unsigned sh = (lane % kPer) * BITS;
+  uint32_t m = pass ? ~((~code & kMask) << sh) : 0xffffffffu;
+#pragma unroll
+  for (uint32_t o = 1; o < kPer; o <<= 1) m &= __shfl_xor_sync(0xffffffffu, m, o);
+  uint32_t old = 0xffffffffu;
+  if (lane % kPer == 0 && m != 0xffffffffu)
+    old = atomicAnd(reinterpret_cast<uint32_t*>(tbl) + off0 / kPer + lane / kPer, m);
+  old = __shfl_sync(0xffffffffu, old, lane & ~(kPer - 1));
+  return ((old >> sh) & kMask) == kMask;
+}
+
 // build_dim_table for every join at once (grid.y = join).  Each thread owns
 // kDimU rows per pass and issues all of their column loads before any
 // predicate is evaluated (one memory latency per pass, not one per column).
 constexpr int kDimU = 2;
 __global__ void __launch_bounds__(256) dim_filter_kernel(const DimBuildArgs a) {
+  pdl_wait();  // the prologue cleared the tables
+  pdl_trigger();
   const DimBuildDesc& d = a.d[blockIdx.y];
   HtMeta* m = a.meta + blockIdx.y;
   const unsigned lane = lane_id();
@@ -265,6 +303,34 @@ __global__ void __launch_bounds__(256) dim_filter_kernel(const DimBuildArgs a) {
         pos0 = __shfl_sync(0xffffffffu, pos0, leader);
       } else if ((int)lane == leader) {
         atomicAdd(&s_count, __popc(bal));
+      }
+      if (!hashed) {
+        // a warp whose 32 rows carry 32 consecutive keys (every generated
+        // dimension: key = row + 1) updates the direct table with one atomic
+        // per bitmap word / per code word instead of one per row (the
+        // per-row atomics serialised 32-way on the same word)
+        const uint32_t off = (uint32_t)key[u] - d.kmin;
+        const uint32_t off0 = __shfl_sync(0xffffffffu, off, 0);
+        const bool dense = __all_sync(0xffffffffu, row < d.rows && off == off0 + lane) && off0 + 31u < d.nkeys;
+        if (dense) {  // warp-uniform
+          const int32_t dig = pass ? digit_of(d, pay[u]) : 0;
+          if (pass && dig >= 0) {
+            dmin = min(dmin, dig);
+            dmax = max(dmax, dig);
+          }
+          bool dup;
+          if (d.kind == kTabBitmap) dup = warp_bitmap_or(reinterpret_cast<uint32_t*>(d.tbl), off0, bal, lane);
+          else if (d.kind == kTabU8 && (off0 & 3u) == 0)
+            dup = !warp_claim_code<8>(d.tbl, off0, pass, dig < 0 ? pipe::kU8Bad : (uint32_t)dig, lane);
+          else if (d.kind == kTabU16 && (off0 & 1u) == 0)
+            dup = !warp_claim_code<16>(d.tbl, off0, pass, dig < 0 ? pipe::kU16Bad : (uint32_t)dig, lane);
+          else
+            dup = pass && !(d.kind == kTabU8 ? claim_code<8>(d.tbl, off, dig < 0 ? pipe::kU8Bad : (uint32_t)dig)
+                                             : claim_code<16>(d.tbl, off, dig < 0 ? pipe::kU16Bad : (uint32_t)dig));
+          if (d.bits) warp_bitmap_or(d.bits, off0, bal, lane);
+          if (pass && dup) atomicCAS(&m->err, 0, 2);  // duplicate key (BuildError)
+          continue;
+        }
       }
       if (!pass) continue;
       const int32_t dig = digit_of(d, pay[u]);
@@ -316,6 +382,8 @@ __global__ void __launch_bounds__(256) dim_filter_kernel(const DimBuildArgs a) {
 }
 
 __global__ void dim_init_kernel(const DimBuildArgs a) {
+  pdl_wait();
+  pdl_trigger();
   const DimBuildDesc& d = a.d[blockIdx.y];
   HtMeta* m = a.meta + blockIdx.y;
   if (d.kind != kTabHash) return;
@@ -336,6 +404,8 @@ __global__ void dim_init_kernel(const DimBuildArgs a) {
 }
 
 __global__ void dim_insert_kernel(const DimBuildArgs a) {
+  pdl_wait();
+  pdl_trigger();
   const DimBuildDesc& d = a.d[blockIdx.y];
   HtMeta* m = a.meta + blockIdx.y;
   if (d.kind != kTabHash) return;
@@ -384,6 +454,7 @@ template <int BT, int IPT, bool PF = false, int CH = 0>
 __global__ void __launch_bounds__(BT) ssb_flight1_kernel(const Flight1Args a) {
   using L = VecLayout<BT, IPT>;
   __shared__ long long red[BT / 32];
+  pdl_trigger();  // the scan reads only fact columns: it overlaps the prologue
   long long sum = 0;
   unsigned cnt = 0;
   const int64_t ntiles = (a.n + L::TILE - 1) / L::TILE;
@@ -434,6 +505,7 @@ __global__ void __launch_bounds__(BT) ssb_flight1_kernel(const Flight1Args a) {
   }
   const long long s = block_sum<BT>(sum, red);
   const long long c = block_sum<BT>((long long)cnt, red);
+  pdl_wait();  // the prologue zeroed the aggregate
   if (threadIdx.x == 0) {
     atomicAdd(a.g_sum, (unsigned long long)s);
     atomicAdd(a.g_cnt, (unsigned long long)c);
@@ -453,6 +525,8 @@ __global__ void finalize_kernel(const unsigned long long* sums, const unsigned l
                                 BoxPlan bp, int packed, int flight1, ResultHeader* hdr, RowOut* rows,
                                 const unsigned long long* surv, const int32_t* err,
                                 const HtMeta* meta, int nj) {
+  pdl_wait();
+  pdl_trigger();
   const unsigned lane = lane_id();
   const BoxD box = box_of(bp, meta);
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // QueryStats + error words ride in the header
@@ -495,6 +569,8 @@ struct HostBox {
   int32_t pad[7];
 };
 __global__ void box_publish_kernel(const HtMeta* meta, int nj, HostBox* hb) {
+  pdl_wait();
+  pdl_trigger();
   if (threadIdx.x == 0) {
     for (int j = 0; j < nj; ++j) {
       hb->dmin[j] = meta[j].dmin;
@@ -664,7 +740,7 @@ int launch_pipeline(crys_ctx* ctx, pipe::PipeArgs pa, size_t dyn, const std::str
   const int nb = blocks_per_sm((const void*)fn, threads, dyn);
   const int64_t ntiles = (pa.n + TILE - 1) / TILE;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)nb * ctx->num_sms));
-  fn<<<grid, threads, dyn, ctx->stream>>>(pa);
+  launch_k(fn, grid, threads, dyn, ctx->stream, pa);
   CRYS_LAUNCHED(std::string("ssb_pipeline ") + name + " grid=" + std::to_string(grid) +
                 " smem=" + std::to_string(dyn));
   return grid;
@@ -704,7 +780,7 @@ int launch_scan(crys_ctx* ctx, pipe::PipeArgs pa, size_t dyn, const std::string&
   const int64_t cap = ((ntiles + grid - 1) / grid) * TILE;  // every row of the CTA's tiles
   CRYS_CHECK(cap * grid <= pa.list_cap, CRYS_ECONTRACT, "survivor list workspace too small");
   pa.list_cap = cap;
-  fn<<<grid, threads, dyn, ctx->stream>>>(pa);
+  launch_k(fn, grid, threads, dyn, ctx->stream, pa);
   CRYS_LAUNCHED(std::string("ssb_scan_emit ") + name + " grid=" + std::to_string(grid) + " smem=" +
                 std::to_string(dyn));
   return grid;
@@ -778,7 +854,7 @@ void launch_gather(crys_ctx* ctx, pipe::GatherArgs ga, int regions, int64_t cell
   auto fn = pipe::ssb_gather_kernel<NJB, NA, kGatherBT, kGatherK, NPRE>;
   const int nb = blocks_per_sm((const void*)fn, kGatherBT, dyn);
   const int grid = std::min(nb, 4) * ctx->num_sms;
-  fn<<<grid, kGatherBT, dyn, ctx->stream>>>(ga);
+  launch_k(fn, grid, kGatherBT, dyn, ctx->stream, ga);
   CRYS_LAUNCHED(std::string("ssb_gather ") + name + " smem=" + std::to_string(dyn));
 }
 
@@ -799,7 +875,16 @@ void gather_pre(crys_ctx* ctx, pipe::GatherArgs ga, int regions, int64_t cells, 
 struct BmShape {
   int w, v, s;
 };
-constexpr BmShape kBmShapes[4] = {{16, 2, 4}, {16, 2, 3}, {16, 2, 2}, {16, 1, 4}};
+// ring shapes {consumer warps, 128-row vectors per lane, stages}; families by
+// the autotuner's preference: 0 = 16 warps, 1 = 31 warps (a full 1024-thread
+// CTA), 2 = 24 warps.  The dense head is latency-bound (issue ~60 % with 17
+// warps per SM; fewer warps with more rows each measured slower: 8 x 16 rows
+// +15 %, 4 x 32 rows +60 %), so the wider families trade rows per lane for
+// warps.
+constexpr int kBmShapeN = 11;
+constexpr BmShape kBmShapes[kBmShapeN] = {{16, 2, 4}, {16, 2, 3}, {16, 2, 2}, {16, 1, 4}, {31, 1, 4}, {31, 1, 3},
+                                          {31, 1, 2}, {24, 2, 3}, {24, 2, 2}, {24, 1, 4}, {24, 1, 3}};
+constexpr int kBmFamily[4] = {0, 4, 7, kBmShapeN};  // first shape of each preference family
 
 template <int D, int W, int V, int S>
 int launch_scanbm_shape(crys_ctx* ctx, pipe::BmArgs ba, size_t dyn, const std::string& name, int64_t* cap) {
@@ -814,7 +899,7 @@ int launch_scanbm_shape(crys_ctx* ctx, pipe::BmArgs ba, size_t dyn, const std::s
   *cap = ((ntiles + grid - 1) / grid) * TILE;  // every row of the CTA's tiles
   CRYS_CHECK(*cap * grid <= ba.list_cap, CRYS_ECONTRACT, "survivor list workspace too small");
   ba.list_cap = *cap;
-  fn<<<grid, threads, dyn, ctx->stream>>>(ba);
+  launch_k(fn, grid, threads, dyn, ctx->stream, ba);
   CRYS_LAUNCHED(std::string("ssb_scan_bm ") + name + " D=" + std::to_string(D) + " grid=" + std::to_string(grid) +
                 " smem=" + std::to_string(dyn));
   return grid;
@@ -840,20 +925,28 @@ int launch_scanbm(crys_ctx* ctx, pipe::BmArgs ba, int pref, const std::string& n
     }
     return std::make_pair(all, at);
   };
-  int k = 0;
   int32_t off[3] = {-1, -1, -1};
-  if (pref == 0) {  // the deepest ring that keeps every bitmap on chip, else the deepest ring
-    for (k = 0; k < 4 && !place(k, off).first; ++k) {
-    }
-    if (k == 4) k = 0;
+  // the deepest ring of the preferred family that keeps every bitmap on chip,
+  // else that family's deepest ring
+  const int f = pref >= 0 && pref < 3 ? pref : 0;
+  int k = kBmFamily[f];
+  for (; k < kBmFamily[f + 1] && !place(k, off).first; ++k) {
   }
+  if (k == kBmFamily[f + 1]) k = kBmFamily[f];
   const size_t dyn = place(k, off).second;
   for (int j = 0; j < 3; ++j) ba.smem[j] = j < D ? off[j] : -1;
   switch (k) {
     case 0: return launch_scanbm_shape<D, 16, 2, 4>(ctx, ba, dyn, name, cap);
     case 1: return launch_scanbm_shape<D, 16, 2, 3>(ctx, ba, dyn, name, cap);
     case 2: return launch_scanbm_shape<D, 16, 2, 2>(ctx, ba, dyn, name, cap);
-    default: return launch_scanbm_shape<D, 16, 1, 4>(ctx, ba, dyn, name, cap);
+    case 3: return launch_scanbm_shape<D, 16, 1, 4>(ctx, ba, dyn, name, cap);
+    case 4: return launch_scanbm_shape<D, 31, 1, 4>(ctx, ba, dyn, name, cap);
+    case 5: return launch_scanbm_shape<D, 31, 1, 3>(ctx, ba, dyn, name, cap);
+    case 6: return launch_scanbm_shape<D, 31, 1, 2>(ctx, ba, dyn, name, cap);
+    case 7: return launch_scanbm_shape<D, 24, 2, 3>(ctx, ba, dyn, name, cap);
+    case 8: return launch_scanbm_shape<D, 24, 2, 2>(ctx, ba, dyn, name, cap);
+    case 9: return launch_scanbm_shape<D, 24, 1, 4>(ctx, ba, dyn, name, cap);
+    default: return launch_scanbm_shape<D, 24, 1, 3>(ctx, ba, dyn, name, cap);
   }
 }
 
@@ -893,6 +986,30 @@ int bm_env() {
   static const int v = [] {
     const char* e = getenv("CRYS_BM");
     return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+}  // namespace
+
+// CRYS_PDL=1 chains each query's kernels with programmatic dependent launch
+// (launch_k).  Off by default: measured on B200 (SF=20 suite) it did not
+// shorten the per-query overhead (0.58 ms either way) and slowed the
+// late-materialising heads by 10-25 % (3.26 -> 3.58 ms per suite).
+bool pdl_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("CRYS_PDL");
+    return e && atoi(e) == 1;
+  }();
+  return v;
+}
+
+namespace {
+
+int dim_grid_per_sm() {
+  static const int v = [] {
+    const char* e = getenv("CRYS_DIM_GRID");
+    return e ? std::max(1, atoi(e)) : 8;
   }();
   return v;
 }
@@ -963,13 +1080,16 @@ struct TuneCand {
 // bm candidates: the late-materialising split after two joins (ssb_scanbm.cuh)
 // with L2 look-ahead 0 / 2 / 4 (B200, SF=20: q2.1 0.323 -> 0.237 ms, q2.3
 // 0.289 -> 0.171, q4.2 0.477 -> 0.376).
-constexpr int kTuneN = 14;
-constexpr TuneCand kTune4[kTuneN] = {{0, 0, 0},    {4, 0, 0},    {3, 0, 0},   {6, 0, 0},   {0, 2, 0},
-                                     {4, 2, 0},    {3, 2, 0},    {6, 2, 0},   {3, 2, 1},   {3, 4, 1},
-                                     {2, 2, 1},    {0, 0, 2, 1}, {0, 2, 2, 1}, {0, 4, 2, 1}};
-constexpr int kTuneN6 = 9;
-constexpr TuneCand kTune6[kTuneN6] = {{0, 0, 0}, {0, 2, 0},    {0, 4, 0},    {3, 2, 1},   {3, 4, 1},
-                                      {2, 2, 1}, {0, 0, 2, 1}, {0, 2, 2, 1}, {0, 4, 2, 1}};
+// bm candidates with cfg 1 / 2 use the 31-warp / 24-warp ring shapes (kBmShapes).
+constexpr int kTuneN = 18;
+constexpr TuneCand kTune4[kTuneN] = {{0, 0, 0},    {4, 0, 0},    {3, 0, 0},    {6, 0, 0},    {0, 2, 0},
+                                     {4, 2, 0},    {3, 2, 0},    {6, 2, 0},    {3, 2, 1},    {3, 4, 1},
+                                     {2, 2, 1},    {0, 0, 2, 1}, {0, 2, 2, 1}, {0, 4, 2, 1}, {1, 0, 2, 1},
+                                     {1, 2, 2, 1}, {2, 0, 2, 1}, {2, 2, 2, 1}};
+constexpr int kTuneN6 = 13;
+constexpr TuneCand kTune6[kTuneN6] = {{0, 0, 0},    {0, 2, 0},    {0, 4, 0},    {3, 2, 1},    {3, 4, 1},
+                                      {2, 2, 1},    {0, 0, 2, 1}, {0, 2, 2, 1}, {0, 4, 2, 1}, {1, 0, 2, 1},
+                                      {1, 2, 2, 1}, {2, 0, 2, 1}, {2, 2, 2, 1}};
 struct PipeTune {
   int chosen = -1;  // index into the plan shape's candidate list once decided
   int ncand = 0;
@@ -1262,20 +1382,23 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* dimdb, const std::vector
   if (nj) {
     const int tpb = 256;
     const int gx_rows = (int)std::min<int64_t>((max_rows + tpb - 1) / tpb, (int64_t)ctx->num_sms * 8);
-    const int gx_filter = (int)std::min<int64_t>((max_rows + tpb * kDimU - 1) / (tpb * kDimU), (int64_t)ctx->num_sms * 8);
-    dim_filter_kernel<<<dim3(std::max(gx_filter, 1), nj), tpb, 0, st>>>(da);
+    // CTAs per dimension: CRYS_DIM_GRID per SM (default 8; measured on the
+    // SF=20 suite: 1 -> 18-41 us per build, 2 -> 12-24, 4 and 8 -> 9-20)
+    const int gx_filter = (int)std::min<int64_t>((max_rows + tpb * kDimU - 1) / (tpb * kDimU),
+                                                 (int64_t)ctx->num_sms * dim_grid_per_sm());
+    launch_k(dim_filter_kernel, dim3(std::max(gx_filter, 1), nj), tpb, 0, st, da);
     CRYS_LAUNCHED("dim_filter_kernel");
     count_launch(ctx);
     if (any_ht) {  // linear-probing builds (hash_table.cpp:20-94) for sparse key domains
       const int gx_cap = (int)std::min<int64_t>((max_cap + tpb - 1) / tpb, (int64_t)ctx->num_sms * 8);
-      dim_init_kernel<<<dim3(std::max(gx_cap, 1), nj), tpb, 0, st>>>(da);
+      launch_k(dim_init_kernel, dim3(std::max(gx_cap, 1), nj), tpb, 0, st, da);
       CRYS_LAUNCHED("dim_init_kernel");
-      dim_insert_kernel<<<dim3(std::max(gx_rows, 1), nj), tpb, 0, st>>>(da);
+      launch_k(dim_insert_kernel, dim3(std::max(gx_rows, 1), nj), tpb, 0, st, da);
       CRYS_LAUNCHED("dim_insert_kernel");
       count_launch(ctx, 2);
     }
     if (hbox) {
-      box_publish_kernel<<<1, 32, 0, st>>>(ws.meta.as<HtMeta>(), nj, hbox);
+      launch_k(box_publish_kernel, 1, 32, 0, st, ws.meta.as<HtMeta>(), nj, hbox);
       CRYS_LAUNCHED("box_publish_kernel");
       count_launch(ctx);
     }
@@ -1413,7 +1536,8 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* dimdb, const std::vector
       int64_t nmax = 0;
       for (int64_t r : nrows) nmax = std::max(nmax, r);
       ws.list.reserve(sizeof(uint2) * (size_t)(nmax + ((int64_t)ctx->num_sms * 4 + 1) * 4096));
-      ws.list4.reserve(sizeof(uint4) * (size_t)(nmax + ((int64_t)ctx->num_sms + 1) * 4096));
+      // (slack: every CTA rounds its share up to whole ring tiles of <= 8192 rows)
+      ws.list4.reserve(sizeof(uint4) * (size_t)(nmax + ((int64_t)ctx->num_sms + 1) * 8192));
       ws.list_count.reserve(sizeof(unsigned) * (size_t)ctx->num_sms * 8);
     }
     const int cfg = pipe_cfg();  // CRYS_PIPE_CFG > 0 forces an instantiation
@@ -1456,7 +1580,7 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* dimdb, const std::vector
     fa.agg_b_is_f1 = plan.fact_filters.size() > 1 && plan.fact_filters[1].column == "lo_discount";
     const int64_t ntiles = (n + tile - 1) / tile;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)nb * ctx->num_sms));
-    L.fn<<<grid, L.bt, L.smem, st>>>(fa);
+    launch_k(L.fn, grid, L.bt, L.smem, st, fa);
     CRYS_LAUNCHED(std::string("fused ") + plan.name + " bt=" + std::to_string(L.bt) + " ipt=" +
                   std::to_string(L.ipt) + " grid=" + std::to_string(grid));
     count_launch(ctx);
@@ -1518,9 +1642,9 @@ static void finalize_enqueue(crys_ctx* ctx, int qid, const unsigned long long* d
   const int tpb = 256;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((cells + tpb - 1) / tpb, (int64_t)ctx->num_sms * 8));
   const int nj = d_err ? (int)plan.joins.size() : 0;  // build errors of this ctx's own dimension builds
-  finalize_kernel<<<grid, tpb, 0, st>>>(d_sums, d_cnts, bp, packed ? 1 : 0, plan.joins.empty() ? 1 : 0, hdr,
-                                        rows, hdr_in ? reinterpret_cast<const unsigned long long*>(hdr_in) : d_surv,
-                                        d_err, ws.meta.as<HtMeta>(), nj);
+  launch_k(finalize_kernel, grid, tpb, 0, st, d_sums, d_cnts, bp, packed ? 1 : 0, plan.joins.empty() ? 1 : 0, hdr,
+           rows, hdr_in ? reinterpret_cast<const unsigned long long*>(hdr_in) : d_surv, d_err,
+           (const HtMeta*)ws.meta.as<HtMeta>(), nj);
   CRYS_LAUNCHED("finalize_kernel");
   count_launch(ctx);
   if (hdr_in) {
