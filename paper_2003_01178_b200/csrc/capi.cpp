@@ -182,9 +182,6 @@ crys_ctx* new_context(int device) {
   CUDA_TRY(cudaGetDeviceProperties(&prop, device));
   CRYS_CHECK(prop.major == 10, CRYS_ENOTBUILT,
              std::string("library is compiled for sm_100a only; device is ") + prop.name);
-  // CRYS_L2_FETCH=B: cudaLimitMaxL2FetchGranularity hint in bytes (0..128) for
-  // the device (A/B knob; unset leaves the driver default)
-  if (const char* e = getenv("CRYS_L2_FETCH")) CUDA_TRY(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(e)));
   auto* ctx = new crys_ctx();
   ctx->device = device;
   ctx->num_sms = prop.multiProcessorCount;

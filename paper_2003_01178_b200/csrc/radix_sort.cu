@@ -234,7 +234,6 @@ __global__ void __launch_bounds__(kOsBT, kOsMinBlocks) onesweep_kernel(OsPass a)
   uint32_t* s_wc = os_sm + 2 * kOsTile;                        // [kOsWarps][256]
   uint32_t* s_start = s_wc + kOsWarps * 256;                   // [257] tile digit starts
   long long* s_dst = reinterpret_cast<long long*>(s_start + 260);  // [256] dst - start
-  uint32_t* s_pm = reinterpret_cast<uint32_t*>(s_dst + 256);      // RANK 3: [kOsWarps][257] peer masks
   __shared__ uint32_t s_scan[kOsBT / 32 + 1];
   __shared__ int s_tile;
   __shared__ __align__(8) uint64_t s_bar;
@@ -245,8 +244,6 @@ __global__ void __launch_bounds__(kOsBT, kOsMinBlocks) onesweep_kernel(OsPass a)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int i = threadIdx.x; i < kOsWarps * 256; i += kOsBT) s_wc[i] = 0;
-  if constexpr (RANK == 3)
-    for (int i = threadIdx.x; i < kOsWarps * 257; i += kOsBT) s_pm[i] = 0;
   __syncthreads();
   const int tile = s_tile;
   int seg = 0, first = 0;
@@ -308,20 +305,7 @@ __global__ void __launch_bounds__(kOsBT, kOsMinBlocks) onesweep_kernel(OsPass a)
     const int sl = wbase + k * 32 + lane;
     key[k] = s_k[sl];
     const uint32_t d = sl < valid ? digit_of(key[k], a.start, mask) : 256u;
-    if constexpr (RANK == 3) {
-      // peers through a warp-private shared-memory mask per digit: every lane
-      // ORs its bit into word d, reads the word back, and the lowest peer
-      // clears it for the next item (4 instructions + 3 warp syncs, against
-      // 8 ballots + 8 LOP3 + the bit extractions)
-      uint32_t* pm = s_pm + warp * 257;
-      __syncwarp();
-      atomicOr(pm + d, 1u << lane);
-      __syncwarp();
-      const unsigned m = pm[d];
-      __syncwarp();
-      if ((m & ((1u << lane) - 1u)) == 0u) pm[d] = 0u;
-      rd[k] = m;
-    } else if constexpr (RANK == 0) {
+    if constexpr (RANK == 0) {
       rd[k] = __match_any_sync(0xffffffffu, d);
     } else if (RANK == 2 && (k % CRYS_OS_MATCH_EVERY) == 0) {
       // mixed: every CRYS_OS_MATCH_EVERY-th item on the ADU (match.any), the rest on the vote
@@ -479,7 +463,6 @@ void launch_onesweep(const OsPass& a, unsigned grid, size_t smem, cudaStream_t s
     case 1: onesweep_kernel<1, 1><<<grid, kOsBT, smem, st>>>(a); break;
     case 2: onesweep_kernel<0, 0><<<grid, kOsBT, smem, st>>>(a); break;
     case 3: onesweep_kernel<0, 1><<<grid, kOsBT, smem, st>>>(a); break;
-    case 4: onesweep_kernel<0, 3><<<grid, kOsBT, smem, st>>>(a); break;
     default: onesweep_kernel<0, 2><<<grid, kOsBT, smem, st>>>(a); break;
   }
 }
@@ -525,14 +508,12 @@ void WsDeleter::operator()(SortWorkspace* p) const { delete p; }
 namespace {
 
 size_t os_smem() {
-  return sizeof(int32_t) * 2 * kOsTile + sizeof(uint32_t) * (kOsWarps * 256 + 260) + sizeof(long long) * 256 +
-         sizeof(uint32_t) * kOsWarps * 257;  // RANK 3 peer masks
+  return sizeof(int32_t) * 2 * kOsTile + sizeof(uint32_t) * (kOsWarps * 256 + 260) + sizeof(long long) * 256;
 }
 
 void os_attr() {  // per device (ensure_dyn_smem caches by (device, kernel))
   for (const void* fn : {(const void*)onesweep_kernel<0, 0>, (const void*)onesweep_kernel<0, 1>,
-                         (const void*)onesweep_kernel<0, 2>, (const void*)onesweep_kernel<0, 3>,
-                         (const void*)onesweep_kernel<1, 1>})
+                         (const void*)onesweep_kernel<0, 2>, (const void*)onesweep_kernel<1, 1>})
     ensure_dyn_smem(fn, os_smem());
 }
 
