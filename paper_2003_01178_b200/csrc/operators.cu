@@ -445,7 +445,7 @@ __device__ __forceinline__ int32_t ld_hint1(const int32_t* p, uint64_t pol) {
   return r;
 }
 
-constexpr int kRrMaxG = 32 * 16;  // counts per round read by one warp (<= 16 per lane)
+constexpr int kRrMaxG = 32 * 10;  // counts per round read by one warp (<= 10 per lane; 2 CTAs x 148 SMs = 296)
 
 template <int BT, int WU, int LAG, int UW>
 __global__ void __launch_bounds__(BT, 2) select_rr_kernel(const int32_t* __restrict__ in, int64_t n, int32_t lo,
@@ -571,6 +571,223 @@ __global__ void __launch_bounds__(BT, 2) select_rr_kernel(const int32_t* __restr
         if (p) __stcs(o + __popc(m & lt), x);
         o += __popc(m);
       }
+    }
+  }
+  if (threadIdx.x == 0 && mine) atomicAdd(reinterpret_cast<unsigned long long*>(total_out), (unsigned long long)mine);
+}
+
+// Walks units (logical tile, 32-thread group) in order from unit u0 with one
+// division: next() = this lane's first slot of the next unit.
+struct UnitCursor {
+  int64_t tile_base, lane_off;
+  int m, gpt;
+  int64_t S;
+  __device__ UnitCursor(int64_t u0, int gpt_, int64_t S_, unsigned lane) : gpt(gpt_), S(S_) {
+    tile_base = (u0 / gpt_) * S_;
+    m = (int)(u0 % gpt_);
+    lane_off = lane;
+  }
+  __device__ __forceinline__ int64_t next() {
+    const int64_t s = tile_base + (int64_t)m * 32 + lane_off;
+    if (++m == gpt) {
+      m = 0;
+      tile_base += S;
+    }
+    return s;
+  }
+};
+
+// Crystal order (select_tile_into, select.hpp:107-135) on the same
+// round-robin scheme, for tiles whose bt is a multiple of 32 and ipt a power
+// of two <= 16 (IPTM == ipt: compile-time slot loops).
+// The output of logical tile j is thread-major: logical thread t's matches
+// (slots j S + t + k bt, k < ipt, in k order), t = 0 .. bt-1.  A UNIT is 32
+// consecutive logical threads (j, m): t = 32 m + lane, so a unit's output is
+// contiguous and units in (j, m) order are output order.  Lane loads its ipt
+// slots (for fixed k the 32 lanes read 128 consecutive bytes), one warp scan
+// of the per-lane counts places the unit.  Warp w of CTA c owns UPW
+// consecutive units per round; counts and offsets as in select_rr_kernel.
+template <int BT, int IPTM, int LAG>
+__global__ void __launch_bounds__(BT, 2) select_rr_crystal_kernel(const int32_t* __restrict__ in, int64_t n,
+                                                                  int32_t lo, int32_t hi, int bt, int ipt,
+                                                                  int32_t* __restrict__ out, int rounds,
+                                                                  uint32_t* counts, long long* total_out) {
+  constexpr int W = BT / 32;
+  constexpr int UPW = 1024 / (32 * IPTM) > 0 ? 1024 / (32 * IPTM) : 1;  // units per warp per round
+  constexpr int NB = IPTM >= 16 ? 1 : 16 / IPTM;                        // units per batch of loads
+  static_assert(UPW % NB == 0, "batches");
+  constexpr int PER = (kRrMaxG + 31) / 32;
+  constexpr int NS = LAG + 1;
+  __shared__ int s_wc[NS][W];
+  __shared__ long long s_off;
+  __shared__ int32_t s_stage[W * NB * 32 * IPTM];  // per warp: one batch of compacted output
+  const int G = gridDim.x, c = blockIdx.x;
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t span = (uint32_t)hi - (uint32_t)lo;
+  const int gpt = bt >> 5;                   // units (32-thread groups) per logical tile
+  const int64_t S = (int64_t)bt * IPTM;      // slots per logical tile (ipt == IPTM)
+  const int64_t upr = (int64_t)G * W * UPW;  // units per round
+  const uint64_t keep = pipe::policy_evict_last(), drop = pipe::policy_evict_first();
+  // a warp's UPW units are whole logical tiles: count over a contiguous range
+  const bool whole = UPW % gpt == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+  long long base = 0;
+  int resolved = 0;
+  long long mine = 0;
+  for (int k = 0; k < rounds + LAG; ++k) {
+    const int j = k - LAG;
+    uint32_t cv[PER];
+    if (warp == 0 && j >= 0) {
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const int cc = i * 32 + (int)lane;
+        cv[i] = cc < G ? ld_relaxed_u32(counts + (size_t)j * G + cc) : 1u;
+      }
+    }
+    if (k < rounds) {  // ---- COUNT round k: this warp's UPW units (order does not matter here)
+      const int64_t u0 = k * upr + ((int64_t)c * W + warp) * UPW;
+      int cnt = 0;
+      if (whole) {  // the units are whole logical tiles: one contiguous range, 128-bit loads
+        const int64_t r0 = (u0 / gpt) * S, r1 = min(r0 + (int64_t)(UPW / gpt) * S, n);
+        int64_t wb = r0;  // warp-uniform position
+        for (; wb + 1024 <= r1; wb += 1024) {
+          int4 v[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) v[q] = ld_hint4(in + wb + q * 128 + 4 * lane, keep);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            cnt += ((uint32_t)v[q].x - (uint32_t)lo <= span) + ((uint32_t)v[q].y - (uint32_t)lo <= span) +
+                   ((uint32_t)v[q].z - (uint32_t)lo <= span) + ((uint32_t)v[q].w - (uint32_t)lo <= span);
+        }
+        for (int64_t e = wb + lane; e < r1; e += 32) cnt += (uint32_t)ld_hint1(in + e, keep) - (uint32_t)lo <= span;
+      } else {
+        UnitCursor uc(u0, gpt, S, lane);
+        for (int ub = 0; ub < UPW; ub += NB) {
+          int64_t s0[NB];
+#pragma unroll
+          for (int b2 = 0; b2 < NB; ++b2) s0[b2] = uc.next();
+          const bool inb = s0[NB - 1] - (int64_t)lane + 31 + (int64_t)(IPTM - 1) * bt < n;
+#pragma unroll
+          for (int b2 = 0; b2 < NB; ++b2) {
+            const int32_t* p = in + s0[b2];
+#pragma unroll
+            for (int q = 0; q < IPTM; ++q) {
+              if ((inb || s0[b2] + (int64_t)q * bt < n))
+                cnt += (uint32_t)ld_hint1(p + q * bt, keep) - (uint32_t)lo <= span;
+            }
+          }
+        }
+      }
+      cnt = warp_sum(cnt);
+      if (lane == 0) s_wc[k % NS][warp] = cnt;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int tot = 0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) tot += s_wc[k % NS][w];
+        st_relaxed_u32(counts + (size_t)k * G + c, (uint32_t)tot + 1u);
+        mine += tot;
+      }
+    }
+    if (j < 0) continue;
+    {
+      int any = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) any |= s_wc[j % NS][w];
+      if (!any) continue;  // uniform
+    }
+    if (warp == 0) {
+      for (; resolved < j; ++resolved) {
+        long long t = 0;
+        for (int cc = (int)lane; cc < G; cc += 32) {
+          uint32_t x;
+          while ((x = ld_relaxed_u32(counts + (size_t)resolved * G + cc)) == 0u) __nanosleep(32);
+          t += (long long)x - 1;
+        }
+        base += warp_sum(t);
+      }
+      long long before = 0, all = 0;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const int cc = i * 32 + (int)lane;
+        while (cv[i] == 0u) {
+          __nanosleep(32);
+          cv[i] = ld_relaxed_u32(counts + (size_t)j * G + cc);
+        }
+        const long long x = cc < G ? (long long)cv[i] - 1 : 0;
+        all += x;
+        before += cc < c ? x : 0;
+      }
+      before = warp_sum(before);
+      all = warp_sum(all);
+      if (lane == 0) s_off = base + before;
+      base += all;
+      resolved = j + 1;
+    }
+    __syncthreads();
+    if (s_wc[j % NS][warp] == 0) continue;
+    long long off = s_off;
+#pragma unroll
+    for (int w = 0; w < W; ++w) off += w < (int)warp ? s_wc[j % NS][w] : 0;
+    const int64_t u0 = j * upr + ((int64_t)c * W + warp) * UPW;
+    UnitCursor uc(u0, gpt, S, lane);
+    for (int ub = 0; ub < UPW; ub += NB) {  // ---- WRITE round j: NB units' loads in flight, then unit by unit
+      int64_t s0[NB];
+#pragma unroll
+      for (int b2 = 0; b2 < NB; ++b2) s0[b2] = uc.next();
+      if (s0[0] - lane >= n) break;  // warp-uniform
+      int32_t x[NB][IPTM];
+      // the whole batch inside the input (all but the last tile): no per-slot bounds
+      const bool inb = s0[NB - 1] - (int64_t)lane + 31 + (int64_t)(IPTM - 1) * bt < n;
+      if (inb) {
+#pragma unroll
+        for (int b2 = 0; b2 < NB; ++b2) {
+          const int32_t* p = in + s0[b2];
+#pragma unroll
+          for (int q = 0; q < IPTM; ++q) x[b2][q] = ld_hint1(p + q * bt, drop);
+        }
+      } else {
+#pragma unroll
+        for (int b2 = 0; b2 < NB; ++b2)
+#pragma unroll
+          for (int q = 0; q < IPTM; ++q) {
+            const int64_t e = s0[b2] + (int64_t)q * bt;
+            x[b2][q] = e < n ? ld_hint1(in + e, drop) : 0;
+          }
+      }
+      // the batch's compacted output in this warp's staging buffer, then one
+      // coalesced copy (per-lane runs straight to global scatter each store)
+      int32_t* wb = s_stage + warp * (NB * 32 * IPTM);
+      int pos = 0;
+#pragma unroll
+      for (int b2 = 0; b2 < NB; ++b2) {
+        uint32_t bits = 0;
+        if (inb) {
+#pragma unroll
+          for (int q = 0; q < IPTM; ++q) bits |= (uint32_t)((uint32_t)x[b2][q] - (uint32_t)lo <= span) << q;
+        } else {
+#pragma unroll
+          for (int q = 0; q < IPTM; ++q) {
+            const int64_t e = s0[b2] + (int64_t)q * bt;
+            bits |= (uint32_t)(e < n && (uint32_t)x[b2][q] - (uint32_t)lo <= span) << q;
+          }
+        }
+        const int cl = __popc(bits);
+        int pre = cl;  // inclusive warp scan of the lanes' counts
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, pre, o);
+          if ((int)lane >= o) pre += y;
+        }
+        int p = pos + pre - cl;
+#pragma unroll
+        for (int q = 0; q < IPTM; ++q)
+          if ((bits >> q) & 1u) wb[p++] = x[b2][q];
+        pos += __shfl_sync(0xffffffffu, pre, 31);
+      }
+      __syncwarp();
+      for (int i = (int)lane; i < pos; i += 32) __stcs(out + off + i, wb[i]);
+      off += pos;
+      __syncwarp();
     }
   }
   if (threadIdx.x == 0 && mine) atomicAdd(reinterpret_cast<unsigned long long*>(total_out), (unsigned long long)mine);
@@ -1514,6 +1731,41 @@ RrLaunch rr_plan(crys_ctx* ctx, int64_t n) {
   return r;
 }
 
+// CRYS_SEL_RRC=0: Crystal-order selects take the count/scan/write kernels.
+bool sel_rr_crystal() {
+  static const bool v = [] {
+    const char* e = getenv("CRYS_SEL_RRC");
+    return !(e && atoi(e) == 0);
+  }();
+  return v;
+}
+
+RrLaunch rr_plan_crystal(crys_ctx* ctx, int64_t n, int bt, int ipt) {
+  RrLaunch r;
+  constexpr int kBT = 512, kLag = 2;
+  // units of 32 logical threads x ipt slots, ~1024 slots per warp per round
+  // (a ~19 MB segment, as the input-order kernel); IPTM = ipt rounded up
+  int iptm = 1;
+  while (iptm < ipt) iptm <<= 1;
+  switch (iptm) {
+    case 1: r.fn = (const void*)select_rr_crystal_kernel<kBT, 1, kLag>; break;
+    case 2: r.fn = (const void*)select_rr_crystal_kernel<kBT, 2, kLag>; break;
+    case 4: r.fn = (const void*)select_rr_crystal_kernel<kBT, 4, kLag>; break;
+    case 8: r.fn = (const void*)select_rr_crystal_kernel<kBT, 8, kLag>; break;
+    default: r.fn = (const void*)select_rr_crystal_kernel<kBT, 16, kLag>; break;
+  }
+  const int upw = std::max(1, 1024 / (32 * iptm));
+  r.bt = kBT;
+  const int per_sm = occupancy(r.fn, r.bt, 0);
+  const int64_t gpt = bt / 32;
+  const int64_t units = ((n + (int64_t)bt * ipt - 1) / ((int64_t)bt * ipt)) * gpt;
+  const int64_t per_cta = (int64_t)(kBT / 32) * upw;
+  r.grid = (int)std::min<int64_t>({(int64_t)per_sm * ctx->num_sms, (int64_t)kRrMaxG, (units + per_cta - 1) / per_cta});
+  const int64_t upr = (int64_t)r.grid * per_cta;
+  r.rounds = (int)((units + upr - 1) / upr);
+  return r;
+}
+
 }  // namespace
 
 int64_t select_i32(crys_ctx* ctx, const int32_t* d_in, int64_t n, int32_t lo, int32_t hi,
@@ -1545,11 +1797,18 @@ int64_t select_i32(crys_ctx* ctx, const int32_t* d_in, int64_t n, int32_t lo, in
   // round-robin kernel tests x - lo <= hi - lo unsigned)
   if (order == CRYS_ORDER_INPUT && cfg == 0 && lo <= hi)
     rr = rr_plan(ctx, n);
-  const size_t words = (size_t)(ntiles + 3) + (rr.fn ? (size_t)(rr.rounds * (int64_t)rr.grid + 1) / 2 : 0);
+  // Crystal order on the round-robin scheme: bt a multiple of 32, ipt in {1, 2, 4, 8, 16}
+  RrLaunch rrc{};
+  if (order == CRYS_ORDER_CRYSTAL && cfg == 0 && lo <= hi && bt % 32 == 0 && ipt <= 16 && (ipt & (ipt - 1)) == 0 &&
+      sel_rr_crystal())
+    rrc = rr_plan_crystal(ctx, n, bt, ipt);
+  const size_t words = (size_t)(ntiles + 3) + (rr.fn ? (size_t)(rr.rounds * (int64_t)rr.grid + 1) / 2 : 0) +
+                       (rrc.fn ? (size_t)(rrc.rounds * (int64_t)rrc.grid + 1) / 2 : 0);
   ctx->status.reserve(sizeof(unsigned long long) * words);
   auto* status = ctx->status.as<unsigned long long>();
   auto* total = reinterpret_cast<long long*>(status + ntiles + 1);
   if (rr.fn) rr.counts = reinterpret_cast<uint32_t*>(status + ntiles + 3);
+  if (rrc.fn) rrc.counts = reinterpret_cast<uint32_t*>(status + ntiles + 3);
   CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(unsigned long long) * words, st));
   timing_kernel_begin(ctx);
   if (order == CRYS_ORDER_INPUT) {
@@ -1609,6 +1868,19 @@ int64_t select_i32(crys_ctx* ctx, const int32_t* d_in, int64_t n, int32_t lo, in
       CUDA_TRY(cudaMemcpyAsync(total, sb.bases + sb.nblk, sizeof(long long), cudaMemcpyDeviceToDevice, st));
       count_launch(ctx, 4);
     }
+  } else if (rrc.fn) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)rrc.grid);
+    lc.blockDim = dim3((unsigned)rrc.bt);
+    lc.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;  // every CTA co-resident (they wait on each other's counts)
+    attr[0].val.cooperative = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    void* args[] = {(void*)&d_in, (void*)&n, (void*)&lo, (void*)&hi, (void*)&bt, (void*)&ipt, (void*)&d_out,
+                    (void*)&rrc.rounds, (void*)&rrc.counts, (void*)&total};
+    CUDA_TRY(cudaLaunchKernelExC(&lc, rrc.fn, args));
   } else if (ipt <= 32) {
     // reduce-then-scan (CRYS_SEL_CFG=1: single pass with the look-back)
     const size_t dyn2 = sizeof(int32_t) * (size_t)chunk;

@@ -1,6 +1,7 @@
 """Every input-order select instantiation (CRYS_SEL_RR round-robin variants,
 the segmented launches CRYS_SEL_CFG=2, count/scan/write CFG=3) gives the
-input-order result: the knobs are read once per process, so each runs in a
+input-order result, and both Crystal-order paths (round-robin, and
+count/scan/write with CRYS_SEL_RRC=0) give the Crystal order: the knobs are read once per process, so each runs in a
 subprocess.  Reference = the boolean-mask gather x[pred(x)], which keeps
 input order (select.hpp:56-73, workers=1)."""
 import os
@@ -28,12 +29,24 @@ for n in (1, 3, 4096, 4099, 4096 * 148 * 5 + 13, (1 << 24) + 7):
     k = tq.select_branching_into(x[1:], tq.PredicateSpec.between(-5, 400), out)  # misaligned span
     ref = x[1:][(x[1:] >= -5) & (x[1:] <= 400)]
     assert k == ref.numel() and torch.equal(out[:k], ref), n
+    # Crystal order (select.hpp:107-135): slot j*S + t + k*bt, output thread-major per logical tile
+    for bt, ipt in ((128, 4), (32, 1), (256, 8), (64, 16), (96, 2), (3, 5)):
+        S = bt * ipt
+        tiles = (n + S - 1) // S
+        pad = torch.full((tiles * S,), 5000, dtype=torch.int32, device="cuda")  # never selected
+        pad[:n] = x
+        v = pad.view(tiles, ipt, bt).transpose(1, 2).reshape(-1)
+        for lo in (-1001, 0, 999):
+            k = tq.select_tile_into(x, tq.PredicateSpec.lt(lo), out, tq.TileConfig(bt, ipt))
+            ref = v[v < lo]
+            assert k == ref.numel() and torch.equal(out[:k], ref), (n, bt, ipt, lo)
 print("ok")
 """ % ROOT
 
 
-@pytest.mark.parametrize("env", [{"CRYS_SEL_RR": "0"}, {"CRYS_SEL_RR": "1"}, {"CRYS_SEL_RR": "2"}, {"CRYS_SEL_RR": "3"}, {"CRYS_SEL_RR": "4"},
-                                 {"CRYS_SEL_CFG": "2"}, {"CRYS_SEL_CFG": "3"}])
+@pytest.mark.parametrize("env", [{"CRYS_SEL_RR": "0"}, {"CRYS_SEL_RR": "1"}, {"CRYS_SEL_RR": "2"}, {"CRYS_SEL_RR": "3"},
+                                 {"CRYS_SEL_RR": "4"}, {"CRYS_SEL_CFG": "2"}, {"CRYS_SEL_CFG": "3"},
+                                 {"CRYS_SEL_RRC": "0"}])
 def test_input_order_variants(env):
     e = dict(os.environ)
     e.update(env)

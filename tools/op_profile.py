@@ -1,7 +1,10 @@
 """One operator configuration, run twice (warm-up + the profiled launch), as an ncu target:
 
     python tools/op_profile.py select <sigma>        # input order, 2^29 rows
-    python tools/op_profile.py join <table bytes>    # 2^28 probes"""
+    python tools/op_profile.py join <table bytes>    # 2^28 probes
+    python tools/op_profile.py sort lsb|msb          # 2^28 pairs
+    python tools/op_profile.py crystal <sigma>       # Crystal-order select 128x4, 2^29 rows
+    python tools/op_profile.py sigmoid 0             # project_sigmoid, 2^29"""
 import os
 import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -33,3 +36,30 @@ elif op == "join":
     for _ in range(2):
         print(H, tq.join_probe_tile(pk, pp, ht))
     ht.free()
+elif op == "sort":
+    n = 1 << 28
+    k0 = torch.empty(n, dtype=torch.int32, device="cuda")
+    tq.random_i32(k0, 42, 6, -(2 ** 31) // 2, (2 ** 31 - 1) // 2)
+    k, p = torch.empty_like(k0), torch.empty_like(k0)
+    fn = tq.lsb_radix_sort if arg == "lsb" else tq.msb_radix_sort
+    for _ in range(2):
+        k.copy_(k0)
+        p.copy_(torch.arange(n, dtype=torch.int32, device="cuda"))
+        fn(k, p)
+    print(bool(torch.all(k[1:] >= k[:-1]).item()))
+elif op == "crystal":
+    n = 1 << 29
+    x = torch.empty(n, dtype=torch.int32, device="cuda")
+    tq.random_i32(x, 42, 1, 0, (1 << 20) - 1)
+    out = torch.empty_like(x)
+    pred = tq.PredicateSpec.lt(int(round(float(arg) * (1 << 20))))
+    for _ in range(2):
+        print(tq.select_tile_into(x, pred, out, tq.TileConfig(128, 4)))
+elif op == "sigmoid":
+    n = 1 << 29
+    x1 = torch.empty(n, dtype=torch.float32, device="cuda")
+    x2 = torch.empty_like(x1)
+    tq.project_inputs(x1, x2, 42)
+    o = torch.empty_like(x1)
+    for _ in range(2):
+        tq.project_sigmoid_into(x1, x2, 0.75, -1.25, o)
