@@ -73,6 +73,7 @@ struct DimBuildDesc {
 struct DimBuildArgs {
   DimBuildDesc d[kMaxJoins];
   HtMeta* meta;
+  int32_t cta0[kMaxJoins + 1];  // dim_filter_kernel: CTAs [cta0[j], cta0[j+1]) build dimension j
 };
 
 struct PrologueArgs {
@@ -255,8 +256,15 @@ constexpr int kDimU = 2;
 __global__ void __launch_bounds__(256) dim_filter_kernel(const DimBuildArgs a) {
   pdl_wait();  // the prologue cleared the tables
   pdl_trigger();
-  const DimBuildDesc& d = a.d[blockIdx.y];
-  HtMeta* m = a.meta + blockIdx.y;
+  // one 1-D grid over all dimensions, each sized by its own row count (a
+  // uniform grid.y = join launched max-rows CTAs for the 2556-row date table too)
+  int dj = 0;
+#pragma unroll
+  for (int j = 1; j < kMaxJoins; ++j)
+    if ((int)blockIdx.x >= a.cta0[j]) dj = j;
+  const int cta = (int)blockIdx.x - a.cta0[dj], nctas = a.cta0[dj + 1] - a.cta0[dj];
+  const DimBuildDesc& d = a.d[dj];
+  HtMeta* m = a.meta + dj;
   const unsigned lane = lane_id();
   // build size: per-warp atomics only where the compaction needs positions
   // (kTabHash); direct tables count in shared memory, one global add per CTA
@@ -271,7 +279,7 @@ __global__ void __launch_bounds__(256) dim_filter_kernel(const DimBuildArgs a) {
   int32_t dmin = INT_MAX, dmax = INT_MIN;  // digits of this thread's passing rows
   const bool hashed = d.kind == kTabHash;
   const int64_t span = (int64_t)blockDim.x * kDimU;
-  for (int64_t base = (int64_t)blockIdx.x * span; base < d.rows; base += (int64_t)gridDim.x * span) {
+  for (int64_t base = (int64_t)cta * span; base < d.rows; base += (int64_t)nctas * span) {
     int32_t fv[2][kDimU], key[kDimU], pay[kDimU];
 #pragma unroll
     for (int u = 0; u < kDimU; ++u) {
@@ -1386,7 +1394,16 @@ static void enqueue_query(crys_ctx* ctx, const crys_db* dimdb, const std::vector
     // SF=20 suite: 1 -> 18-41 us per build, 2 -> 12-24, 4 and 8 -> 9-20)
     const int gx_filter = (int)std::min<int64_t>((max_rows + tpb * kDimU - 1) / (tpb * kDimU),
                                                  (int64_t)ctx->num_sms * dim_grid_per_sm());
-    launch_k(dim_filter_kernel, dim3(std::max(gx_filter, 1), nj), tpb, 0, st, da);
+    // per dimension: ~2 passes of tpb x kDimU rows per CTA, at most gx_filter CTAs
+    int total = 0;
+    for (int j = 0; j <= kMaxJoins; ++j) {
+      da.cta0[j] = total;
+      if (j < nj) {
+        const int64_t want = (da.d[j].rows + 2 * tpb * kDimU - 1) / (2 * tpb * kDimU);
+        total += (int)std::max<int64_t>(1, std::min<int64_t>(want, std::max(gx_filter, 1)));
+      }
+    }
+    launch_k(dim_filter_kernel, dim3(total), tpb, 0, st, da);
     CRYS_LAUNCHED("dim_filter_kernel");
     count_launch(ctx);
     if (any_ht) {  // linear-probing builds (hash_table.cpp:20-94) for sparse key domains
