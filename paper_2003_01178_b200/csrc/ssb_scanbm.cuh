@@ -177,10 +177,29 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) ssb_scan_bm_kernel(const BmAr
         const unsigned hv = (h >> (4 * v)) & 0xFu;
         if (!hv) continue;
         const int4 k4 = reinterpret_cast<const int4*>(st + j * TILE)[v * 32 + lane];
-        const unsigned m = bm_test(sbm[j], gbm[j], kmin[j], nk[j], k4.x, sh[j]) |
-                           (bm_test(sbm[j], gbm[j], kmin[j], nk[j], k4.y, sh[j]) << 1) |
-                           (bm_test(sbm[j], gbm[j], kmin[j], nk[j], k4.z, sh[j]) << 2) |
-                           (bm_test(sbm[j], gbm[j], kmin[j], nk[j], k4.w, sh[j]) << 3);
+        unsigned m;
+        if (ALLSH || sh[j]) {
+          m = bm_test(sbm[j], gbm[j], kmin[j], nk[j], k4.x, true) |
+              (bm_test(sbm[j], gbm[j], kmin[j], nk[j], k4.y, true) << 1) |
+              (bm_test(sbm[j], gbm[j], kmin[j], nk[j], k4.z, true) << 2) |
+              (bm_test(sbm[j], gbm[j], kmin[j], nk[j], k4.w, true) << 3);
+        } else {
+          // a bitmap probed through L2 costs one L1tex wavefront per loading
+          // lane: load only for the rows still alive, not the whole vector
+          const int32_t kk[4] = {k4.x, k4.y, k4.z, k4.w};
+          uint32_t w[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint32_t off = min((uint32_t)kk[e] - kmin[j], nk[j]);
+            w[e] = ((hv >> e) & 1u) ? __ldg(gbm[j] + (off >> 5)) : 0u;
+          }
+          m = 0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint32_t off = min((uint32_t)kk[e] - kmin[j], nk[j]);
+            m |= ((w[e] >> (off & 31u)) & 1u) << e;
+          }
+        }
         h &= ~((hv & ~m) << (4 * v));
       }
       surv[j] += __popc(h);
