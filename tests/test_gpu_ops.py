@@ -126,6 +126,30 @@ def test_select_2e29_counts(env):
     assert k == xs.numel() and torch.equal(out[:k], xs)
 
 
+@pytest.mark.slow
+def test_select_crystal_order_2e29(env):
+    """Crystal order at the BASELINE size (2^29 rows, select.hpp:107-135) for
+    the round-robin path (128x4, 256x8) and the count/scan/write kernels
+    (257x8): slot j*S + t + k*bt, thread-major per logical tile; reference =
+    the same permutation in torch."""
+    torch, tq, orc = env
+    n = 1 << 29
+    x = torch.empty(n, dtype=torch.int32, device="cuda")
+    tq.random_i32(x, 42, 1, 0, (1 << 20) - 1)
+    out = torch.empty_like(x)
+    lo = 1 << 19
+    for bt, ipt in ((128, 4), (256, 8), (257, 8)):
+        S = bt * ipt
+        tiles = (n + S - 1) // S
+        k = tq.select_tile_into(x, tq.PredicateSpec.lt(lo), out, tq.TileConfig(bt, ipt))
+        pad = torch.full((tiles * S,), 1 << 20, dtype=torch.int32, device="cuda")
+        pad[:n] = x
+        v = pad.view(tiles, ipt, bt).transpose(1, 2).reshape(-1)
+        ref = v[v < lo]
+        assert k == ref.numel() and torch.equal(out[:k], ref), (bt, ipt)
+        del pad, v, ref
+
+
 # ------------------------------------------------------------------ project
 
 def test_project_golden(env):
