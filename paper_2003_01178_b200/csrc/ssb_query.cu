@@ -1657,7 +1657,10 @@ static void finalize_enqueue(crys_ctx* ctx, int qid, const unsigned long long* d
   RowOut* rows = reinterpret_cast<RowOut*>(hdr + 1);
   if (!hdr_zeroed) CUDA_TRY(cudaMemsetAsync(hdr, 0, sizeof(ResultHeader), st));
   const int tpb = 256;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((cells + tpb - 1) / tpb, (int64_t)ctx->num_sms * 8));
+  // grid-stride over the BOX (known on the device only): the box is a few
+  // hundred to a few thousand cells, so one CTA per SM at most (~1200 mostly
+  // idle CTAs for q3.2-q4.3's large full domains cost launch time)
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((cells + tpb - 1) / tpb, (int64_t)ctx->num_sms));
   const int nj = d_err ? (int)plan.joins.size() : 0;  // build errors of this ctx's own dimension builds
   launch_k(finalize_kernel, grid, tpb, 0, st, d_sums, d_cnts, bp, packed ? 1 : 0, plan.joins.empty() ? 1 : 0, hdr,
            rows, hdr_in ? reinterpret_cast<const unsigned long long*>(hdr_in) : d_surv, d_err,
