@@ -49,7 +49,12 @@ struct BmArgs {
 __device__ __forceinline__ uint32_t bm_test(const uint32_t* sbm, const uint32_t* gbm, uint32_t kmin, uint32_t nk,
                                             int32_t key, bool shared) {
   const uint32_t off = min((uint32_t)key - kmin, nk);  // out of range -> the absent pad bit
-  const uint32_t w = shared ? sbm[off >> 5] : __ldg(gbm + (off >> 5));
+  if (shared) {  // byte-granular shared load: address = base + (off >> 3) is one LEA.HI
+    uint32_t b;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(b) : "r"(s_addr(sbm) + (off >> 3)));
+    return (b >> (off & 7u)) & 1u;
+  }
+  const uint32_t w = __ldg(gbm + (off >> 5));
   return (w >> (off & 31u)) & 1u;
 }
 
