@@ -1134,23 +1134,29 @@ __device__ __forceinline__ double exp_table(double x) {
 // same float; otherwise the caller takes the near-correctly-rounded path.
 // Rounding to an integer is the 1.5*2^52 trick (no FRND / F2I on the XU
 // pipe, which bounded the previous version).
+// The fast path's double constants from constant memory: DFMA/DADD take a
+// c[bank][offset] operand directly, where an inline literal is rebuilt into
+// uniform registers (UMOV pairs) in every unrolled copy.
+__constant__ double kSigK[9] = {92.33248261689366, 0x1.8p52, 0.010830424667801708, 2.8447437476627285e-11,
+                                1.0 / 24, 1.0 / 6, 0.5, 1.0, -0x1p-13};
+
 __device__ __forceinline__ float sigmoid_fast(double z, bool& sure) {
   const double x = -z;
-  const double sh = fma(x, 92.33248261689366, 0x1.8p52);  // 64/ln2, rounded to an integer in the low bits
+  const double sh = fma(x, kSigK[0], kSigK[1]);  // 64/ln2, rounded to an integer in the low bits
   const int n = __double2loint(sh);
-  const double nd = sh - 0x1.8p52;
-  double r = fma(-nd, 0.010830424667801708, x);
-  r = fma(-nd, 2.8447437476627285e-11, r);
-  double p = fma(r, 1.0 / 24, 1.0 / 6);
-  p = fma(p, r, 0.5);
-  p = fma(p, r, 1.0);
+  const double nd = sh - kSigK[1];
+  double r = fma(-nd, kSigK[2], x);
+  r = fma(-nd, kSigK[3], r);
+  double p = fma(r, kSigK[4], kSigK[5]);
+  p = fma(p, r, kSigK[6]);
+  p = fma(p, r, kSigK[7]);
   p = p * r;
   const double t = __ldg(&kExp2Tab[n & 63].x);
   const double e = __longlong_as_double(__double_as_longlong(fma(t, p, t)) + ((long long)(n >> 6) << 52));
-  const double den = 1.0 + e;
+  const double den = kSigK[7] + e;
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(den));
-  y = fma(y, fma(-den, y, 1.0), y);
+  y = fma(y, fma(-den, y, kSigK[7]), y);
   const float f = __double2float_rn(y);
   const double d = y - (double)f;  // exact (Sterbenz)
   const int fb = __float_as_int(f);
@@ -1158,18 +1164,19 @@ __device__ __forceinline__ float sigmoid_fast(double z, bool& sure) {
   const int ef = (fb >> 23) & 0xff;
   const int k = ef - 151 - ((d < 0.0 && (fb & 0x7fffff) == 0) ? 1 : 0);
   const double hu = __hiloint2double((k + 1023) << 20, 0);
-  sure = fabs(d) < fma(hu, -0x1p-13, hu);
+  sure = fabs(d) < fma(hu, kSigK[8], hu);
   return f;
 }
 
 template <bool SIGMOID>
-__device__ __forceinline__ float project_one(float u, float v, float a, float b) {
+__device__ __forceinline__ float project_one(float u, float v, float a, float b, double da, double db) {
   if constexpr (!SIGMOID) {
     return __fadd_rn(__fmul_rn(a, u), __fmul_rn(b, v));
   } else {
     // float(1 / (1 + exp(-z))) with z in double (project.hpp:56-64); the
     // products of two floats are exact in double, so one fma rounds z once
-    const double z = fma((double)a, (double)u, __dmul_rn((double)b, (double)v));
+    // (da, db: a and b in double, converted once per thread)
+    const double z = fma(da, (double)u, __dmul_rn(db, (double)v));
     if (fabs(z) <= 80.0) {  // the float result is a normal number
       bool sure;
       const float f = sigmoid_fast(z, sure);
@@ -1189,6 +1196,7 @@ __global__ void __launch_bounds__(256) project_kernel(const float* __restrict__ 
                         reinterpret_cast<uintptr_t>(out)) & 15) == 0;
   const int64_t n4 = vec_ok ? n / 4 : 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const double da = (double)a, db = (double)b;
   // the next vector pair is loaded before this one is computed: the sigmoid
   // is long enough per element that one pair in flight per thread leaves
   // HBM latency exposed
@@ -1205,14 +1213,14 @@ __global__ void __launch_bounds__(256) project_kernel(const float* __restrict__ 
       vn = ld_stream4f(x2 + 4 * (i + stride));
     }
     float4 r;
-    r.x = project_one<SIGMOID>(u.x, v.x, a, b);
-    r.y = project_one<SIGMOID>(u.y, v.y, a, b);
-    r.z = project_one<SIGMOID>(u.z, v.z, a, b);
-    r.w = project_one<SIGMOID>(u.w, v.w, a, b);
+    r.x = project_one<SIGMOID>(u.x, v.x, a, b, da, db);
+    r.y = project_one<SIGMOID>(u.y, v.y, a, b, da, db);
+    r.z = project_one<SIGMOID>(u.z, v.z, a, b, da, db);
+    r.w = project_one<SIGMOID>(u.w, v.w, a, b, da, db);
     st_stream4f(out + 4 * i, r);
   }
   for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    out[i] = project_one<SIGMOID>(x1[i], x2[i], a, b);
+    out[i] = project_one<SIGMOID>(x1[i], x2[i], a, b, da, db);
 }
 
 __global__ void ht_init_kernel(int2* slots, int64_t cap) {
