@@ -3,7 +3,7 @@
 #   make lib        -> product library only
 NVCC      ?= /usr/local/cuda/bin/nvcc
 ARCH      := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-Wall -Iinclude \
+NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-Wall -Iinclude $(EXTRA) \
              -Xptxas -v --expt-relaxed-constexpr
 CSRC      := paper_2003_01178_b200/csrc
 BUILD     := build/obj

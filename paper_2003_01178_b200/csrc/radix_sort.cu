@@ -45,7 +45,11 @@ namespace {
 #define CRYS_OS_IPT 16
 #endif
 constexpr int kOsBT = 256, kOsIPT = CRYS_OS_IPT;
+#ifdef CRYS_OS_MINB
+constexpr int kOsMinBlocks = CRYS_OS_MINB;
+#else
 constexpr int kOsMinBlocks = kOsIPT <= 16 ? 4 : (kOsIPT <= 24 ? 3 : 2);
+#endif
 constexpr int kOsTile = kOsBT * kOsIPT;  // 4096 pairs (256 threads, 4 CTAs per SM: measured faster than 512 x 2)
 constexpr int kOsWarps = kOsBT / 32;
 constexpr uint32_t kOsAgg = 1u << 30, kOsPre = 2u << 30, kOsVal = (1u << 30) - 1;
