@@ -1,11 +1,16 @@
 // operators.cu -- selection, projection and hash-join microbenchmark kernels.
 //
-//   select_input_kernel    select_{branching,predicated}_into(workers=1)
-//                          (select.hpp:56-91): input-order output, single pass
-//                          with decoupled look-back (no 3-kernel count/scan/write)
-//   select_crystal_kernel  select_tile_into(config, kDeterministic)
+//   select_rr_kernel       select_{branching,predicated}_into(workers=1)
+//                          (select.hpp:56-91): input-order output, persistent
+//                          round-robin over L2-sized segments (count from HBM,
+//                          write from L2 one exchange later); select_seg_kernel
+//                          (segmented launches) and select_input_kernel
+//                          (decoupled look-back) are the A/B forms
+//   select_rr_crystal_kernel / select_crystal_reg_kernel / select_crystal_kernel
+//                          select_tile_into(config, kDeterministic)
 //                          (select.hpp:107-135): the exact Crystal order for any
-//                          TileConfig -- logical threads over a smem-staged tile
+//                          TileConfig (round-robin units of 32 logical threads
+//                          when bt % 32 == 0 and ipt is a power of two <= 16)
 //   project_kernel         project_{linear,sigmoid}_into (project.hpp:21-64)
 //   ht_init/insert_kernel  HashTable::build (hash_table.cpp:20-94)
 //   join_probe_kernel      join_probe_* (join.cpp:11-96): Q4 checksum, the
