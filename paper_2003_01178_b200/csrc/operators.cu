@@ -1425,10 +1425,11 @@ __global__ void __launch_bounds__((kJW + 1) * 32, 1) join_ring_kernel(
   }
 }
 
-// The probe ring's producer also bulk-prefetches tile it + k into L2 when the
-// table is on chip (k = 2; measured 0.361 -> 0.347 ms at 8 KB).  With the table
-// probed through L2 the prefetched lines compete with it (1.07 -> 1.12 ms at
-// 4 MB), so k = 0 there.  CRYS_JOIN_L2=k overrides both.
+// The probe ring's producer can also bulk-prefetch tile it + k into L2
+// (CRYS_JOIN_L2=k).  r01 measured k = 2 faster with the table on chip
+// (0.361 -> 0.347 ms at 8 KB); r02 measures k = 0 faster everywhere (32 KB:
+// 0.380 -> 0.369 ms; through L2 the prefetched lines compete with the
+// table), so the default is 0.
 // ---- radix-partitioned probe for tables far beyond L2 (PAPER's radix join;
 // the checksum is order-free).  Bucket = the top k bits of the Fibonacci
 // hash = the top k bits of the home slot, so bucket p's probes start inside
@@ -1659,7 +1660,7 @@ int join_l2_ahead(bool table_on_chip) {
     const char* e = getenv("CRYS_JOIN_L2");
     return e ? atoi(e) : -1;
   }();
-  return v >= 0 ? v : (table_on_chip ? 2 : 0);
+  return v >= 0 ? v : 0;  // r02: the bulk L2 prefetch no longer pays on chip either (0.380 -> 0.369 ms at 32 KB)
 }
 
 int occupancy(const void* fn, int bt, size_t smem) {
