@@ -231,7 +231,7 @@ struct OsPass {
 // item through match.any (ADU) and the rest through ballots (ALU), so both
 // pipes work in parallel -- measured best on B200 (LSB 2^28: match-only 11.8,
 // ballots-only 7.88, 1/4 match 7.68, 1/2 match 7.69, 3/8 match 8.00 ms).
-template <int DBG, int RANK>
+template <int DBG, int RANK, bool SEG = false>
 __global__ void __launch_bounds__(kOsBT, kOsMinBlocks) onesweep_kernel(OsPass a) {
   extern __shared__ __align__(128) uint32_t os_sm[];
   int32_t* s_k = reinterpret_cast<int32_t*>(os_sm);           // [kOsTile] staged -> digit-sorted keys
@@ -240,11 +240,12 @@ __global__ void __launch_bounds__(kOsBT, kOsMinBlocks) onesweep_kernel(OsPass a)
   uint32_t* s_start = s_wc + kOsWarps * 256;                   // [257] tile digit starts
   long long* s_dst = reinterpret_cast<long long*>(s_start + 260);  // [256] dst - start
   __shared__ uint32_t s_scan[kOsBT / 32 + 1];
-  __shared__ int s_tile;
+  __shared__ int s_tile, s_seg;
   __shared__ __align__(8) uint64_t s_bar;
 
   if (threadIdx.x == 0) {
     s_tile = (int)atomicAdd(a.tile_counter, 1u);
+    if constexpr (SEG) s_seg = -1;
     pipe::mbar_init(&s_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -254,7 +255,24 @@ __global__ void __launch_bounds__(kOsBT, kOsMinBlocks) onesweep_kernel(OsPass a)
   int seg = 0, first = 0;
   int64_t sbeg = 0, ssize = a.n;
   int total = a.total_tiles;
-  if (a.segs) {
+  if constexpr (SEG) {  // a.segs != nullptr (MSB segmented passes)
+    // the tile's segment in one parallel round (a serial binary search was 8
+    // dependent L2 round trips at the start of every tile: MSB passes ran
+    // 18 % slower than LSB ones)
+    const int nseg = a.segs->nseg;
+    for (int t = threadIdx.x; t < nseg; t += kOsBT)
+      if (a.segs->first_tile[t] <= tile && tile < a.segs->first_tile[t + 1]) s_seg = t;
+    __syncthreads();
+    if (s_seg < 0) return;  // uniform: past the last tile
+    total = tile + 1;
+    seg = s_seg;
+    first = a.segs->first_tile[seg];
+    sbeg = a.segs->begin[seg];
+    ssize = a.segs->size[seg];
+  } else if (a.segs) {
+    // (the host launches SEG = true whenever a.segs is set; this serial form
+    // is kept in the LSB instantiation only because ptxas allocates that
+    // kernel's registers better with it: 6.60 vs 6.66 ms for the LSB 2^28)
     total = a.segs->first_tile[a.segs->nseg];
     int lo = 0, hi = a.segs->nseg - 1;  // last segment with first_tile <= tile
     while (lo < hi) {
@@ -472,6 +490,10 @@ int os_dbg() {
 }
 
 void launch_onesweep(const OsPass& a, unsigned grid, size_t smem, cudaStream_t st) {
+  if (a.segs) {  // MSB segmented passes (the CRYS_OS_DBG variants are LSB-only)
+    onesweep_kernel<0, 2, true><<<grid, kOsBT, smem, st>>>(a);
+    return;
+  }
   switch (os_dbg()) {
     case 1: onesweep_kernel<1, 1><<<grid, kOsBT, smem, st>>>(a); break;
     case 2: onesweep_kernel<0, 0><<<grid, kOsBT, smem, st>>>(a); break;
@@ -526,7 +548,8 @@ size_t os_smem() {
 
 void os_attr() {  // per device (ensure_dyn_smem caches by (device, kernel))
   for (const void* fn : {(const void*)onesweep_kernel<0, 0>, (const void*)onesweep_kernel<0, 1>,
-                         (const void*)onesweep_kernel<0, 2>, (const void*)onesweep_kernel<1, 1>})
+                         (const void*)onesweep_kernel<0, 2>, (const void*)onesweep_kernel<0, 2, true>,
+                         (const void*)onesweep_kernel<1, 1>})
     ensure_dyn_smem(fn, os_smem());
 }
 
