@@ -211,7 +211,7 @@ void ensure_dyn_smem(const void* fn, size_t bytes);
 // Launch accounting + event timing helpers.
 inline void count_launch(crys_ctx* c, int n = 1) { c->launches += n; }
 
-// CRYS_PDL=1: launch_k chains a query's kernels with programmatic dependent launch.
+// CRYS_PDL=0 turns off the programmatic dependent launch of launch_k.
 bool pdl_enabled();
 
 // A kernel launch that may overlap its stream predecessor's tail (programmatic

@@ -38,7 +38,6 @@
 // with all three gathered per date survivor).
 template <int W, int V, int STAGES, int PR, bool ST = false, int D = 1, bool CHN = false>
 __global__ void __launch_bounds__((W + 1) * 32, 1) ssb_flight1_ring_kernel(const Flight1Args a) {
-  pdl_trigger();
   static_assert(D == 1 || D == 2, "dense ring columns");
   // chained level 1: the discount (D == 1) or the quantity (D == 2)
   constexpr int R = 128 * V;   // rows per consumer warp per stage

@@ -51,7 +51,6 @@ struct GatherArgs {
 template <int NJB, int NA, int BT, int K, int NPRE = 0>
 __global__ void __launch_bounds__(BT) ssb_gather_kernel(const GatherArgs a) {
   pdl_wait();  // the dense head's survivor list
-  pdl_trigger();
   static_assert(NJB >= 1 && NJB <= kMaxJ && (NA == 1 || NA == 2), "gather shape");
   static_assert(NPRE >= 0 && NPRE <= 3, "digit joins of the dense head");
   extern __shared__ __align__(128) unsigned char smem[];

@@ -186,7 +186,6 @@ __device__ __forceinline__ bool first_decode(const ProbeTab& t, uint32_t off, ui
 // the dense probe of join 0 (K0 = kTabHash: generic).
 template <int NJ, int NC, int W, int TILE, int STAGES, int K0, bool S0>
 __global__ void __launch_bounds__((W + 1) * 32, 1) ssb_pipeline_kernel(const PipeArgs a) {
-  pdl_trigger();
   constexpr int R = TILE / W;   // rows per consumer warp per stage
   constexpr int V = R / 128;    // int4 key vectors per lane (phase A)
   static_assert(R % 128 == 0 && V >= 1 && V <= 4, "phase A: 4..16 rows per lane");

@@ -462,7 +462,6 @@ template <int BT, int IPT, bool PF = false, int CH = 0>
 __global__ void __launch_bounds__(BT) ssb_flight1_kernel(const Flight1Args a) {
   using L = VecLayout<BT, IPT>;
   __shared__ long long red[BT / 32];
-  pdl_trigger();  // the scan reads only fact columns: it overlaps the prologue
   long long sum = 0;
   unsigned cnt = 0;
   const int64_t ntiles = (a.n + L::TILE - 1) / L::TILE;
@@ -1000,14 +999,17 @@ int bm_env() {
 
 }  // namespace
 
-// CRYS_PDL=1 chains each query's kernels with programmatic dependent launch
-// (launch_k).  Off by default: measured on B200 (SF=20 suite) it did not
-// shorten the per-query overhead (0.58 ms either way) and slowed the
-// late-materialising heads by 10-25 % (3.26 -> 3.58 ms per suite).
+// Programmatic dependent launch along each query's chain (launch_k; CRYS_PDL=0
+// turns it off).  Only the prologue and the dimension builds trigger their
+// dependents early: the fused head's TMA ring starts streaming lineorder while
+// the builds drain and waits (griddepcontrol.wait) only before it copies the
+// tables.  Early triggers in the heads and gathers as well made the suite
+// slower (3.26 -> 3.58 ms: the dependents' CTAs launched into the heads' SMs);
+// with the triggers where they are: 3.14 -> 3.10 ms per step.
 bool pdl_enabled() {
   static const bool v = [] {
     const char* e = getenv("CRYS_PDL");
-    return e && atoi(e) == 1;
+    return !(e && atoi(e) == 0);
   }();
   return v;
 }

@@ -74,7 +74,6 @@ __device__ __forceinline__ bool probe_reg(const RegTab& t, const ProbeTab& pt, c
 
 template <int D, int W, int TILE, int V, int STAGES, int K0, bool S0>
 __global__ void __launch_bounds__((W + 1) * 32, 1) ssb_scan_emit_kernel(const PipeArgs a) {
-  pdl_trigger();
   constexpr int R = TILE / W;  // rows per consumer warp per stage
   static_assert(R == 128 * V && V >= 1 && V <= 4, "4*V rows per lane");
   static_assert(D >= 1 && D <= 3, "dense joins");

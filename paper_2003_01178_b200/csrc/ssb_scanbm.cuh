@@ -62,7 +62,6 @@ __device__ __forceinline__ uint32_t bm_test(const uint32_t* sbm, const uint32_t*
 // join's placement is tested at run time.
 template <int D, int W, int V, int STAGES, bool ALLSH = false>
 __global__ void __launch_bounds__((W + 1) * 32, 1) ssb_scan_bm_kernel(const BmArgs a) {
-  pdl_trigger();
   constexpr int R = 128 * V;   // rows per consumer warp per stage
   constexpr int TILE = W * R;  // rows per stage
   constexpr int NB = 4 * V;    // rows per lane
