@@ -36,7 +36,7 @@ namespace crys {
 namespace {
 
 #ifndef CRYS_OS_MATCH_EVERY
-#define CRYS_OS_MATCH_EVERY 5  // mixed ranking: every n-th item on match.any, the rest on ballots (sweep: profiles/r01_sort_tile_size.txt)
+#define CRYS_OS_MATCH_EVERY 4  // mixed ranking: every n-th item on match.any, the rest on ballots (r02 sweep after the full-tile path: 3 / 4 / 5 / 6 / 8 -> LSB 6.60 / 6.57 / 6.60 / 6.61 / 6.62 ms)
 #endif
 #ifndef CRYS_OS_LB
 #define CRYS_OS_LB 4  // look-back window: predecessors read per round trip
