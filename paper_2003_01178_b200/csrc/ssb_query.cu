@@ -267,11 +267,10 @@ __global__ void __launch_bounds__(256) dim_filter_kernel(const DimBuildArgs a) {
   HtMeta* m = a.meta + dj;
   const unsigned lane = lane_id();
   // build size: per-warp atomics only where the compaction needs positions
-  // (kTabHash); direct tables count in shared memory, one global add per CTA
-  // (a per-warp add to one address serialised ~30 us on the 1 M-row part table)
-  __shared__ int s_count, s_dmin, s_dmax;
+  // (kTabHash); a direct table's count is never read, so none is kept (the
+  // per-CTA adds to one address serialised in L2)
+  __shared__ int s_dmin, s_dmax;
   if (threadIdx.x == 0) {
-    s_count = 0;
     s_dmin = INT_MAX;
     s_dmax = INT_MIN;
   }
@@ -306,11 +305,9 @@ __global__ void __launch_bounds__(256) dim_filter_kernel(const DimBuildArgs a) {
       if (bal == 0) continue;
       const int leader = __ffs(bal) - 1;
       int pos0 = 0;
-      if (hashed) {
+      if (hashed) {  // (a direct table never reads its build count: no count kept for it)
         if ((int)lane == leader) pos0 = atomicAdd(&m->count, __popc(bal));
         pos0 = __shfl_sync(0xffffffffu, pos0, leader);
-      } else if ((int)lane == leader) {
-        atomicAdd(&s_count, __popc(bal));
       }
       if (!hashed) {
         // a warp whose 32 rows carry 32 consecutive keys (every generated
@@ -381,7 +378,6 @@ __global__ void __launch_bounds__(256) dim_filter_kernel(const DimBuildArgs a) {
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    if (!hashed && s_count) atomicAdd(&m->count, s_count);
     if (s_dmin <= s_dmax) {
       atomicMin(&m->dmin, s_dmin);
       atomicMax(&m->dmax, s_dmax);
