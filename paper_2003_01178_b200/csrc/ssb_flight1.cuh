@@ -256,6 +256,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) ssb_flight1_ring_kernel(const
     red[1][warp] = wc;
   }
   asm volatile("bar.sync 1, %0;" ::"n"(W * 32));  // consumers only
+  pdl_trigger();  // the main loop is done: the next kernel may start launching
   pdl_wait();  // the prologue zeroed the aggregate (the scan above overlapped it)
   if (threadIdx.x == 0) {
     long long s = 0, c = 0;

@@ -210,6 +210,7 @@ __global__ void __launch_bounds__(BT) ssb_gather_kernel(const GatherArgs a) {
       if (surv[j]) atomicAdd(&a.surv[j], (unsigned long long)surv[j]);
   }
   if (__any_sync(0xffffffffu, bad_any) && lane == 0) atomicExch(a.err, 2);
+  pdl_trigger();  // the main loop is done: the compaction may start launching
   if (a.smem_agg >= 0) {
     __syncthreads();
     for (int c = threadIdx.x; c < a.cells; c += BT) {

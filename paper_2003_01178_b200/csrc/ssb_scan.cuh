@@ -292,6 +292,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) ssb_scan_emit_kernel(const Pi
     if (lane == 0 && wsum) atomicAdd(&a.surv[j], (unsigned long long)wsum);
   }
   asm volatile("bar.sync 1, %0;" ::"n"(W * 32));  // consumers only
+  pdl_trigger();  // the main loop is done: the next kernel may start launching
   if (threadIdx.x == 0) a.list_count[blockIdx.x] = s_list_n;
 }
 

@@ -236,6 +236,7 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) ssb_scan_bm_kernel(const BmAr
     if (lane == 0 && ws) atomicAdd(&a.surv[j], (unsigned long long)ws);
   }
   asm volatile("bar.sync 1, %0;" ::"n"(W * 32));  // consumers only
+  pdl_trigger();  // the main loop is done: the next kernel may start launching
   if (threadIdx.x == 0) a.list_count[blockIdx.x] = s_list_n;
 }
 
