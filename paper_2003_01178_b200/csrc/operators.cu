@@ -762,32 +762,50 @@ __global__ void __launch_bounds__(BT, 2) select_rr_crystal_kernel(const int32_t*
       // the batch's compacted output in this warp's staging buffer, then one
       // coalesced copy (per-lane runs straight to global scatter each store)
       int32_t* wb = s_stage + warp * (NB * 32 * IPTM);
+      // one warp scan for PK units at a time: their lane counts packed into
+      // FB-bit fields of one word (a unit's prefix is at most 32 * IPTM)
+      constexpr int FB = 32 * IPTM < 256 ? 8 : 16;
+      // (IPTM < 4 keeps one scan per unit: its 8-16 units per batch already
+      // fill the registers)
+      constexpr int PK = IPTM < 4 ? 1 : (32 / FB < NB ? 32 / FB : NB);
       int pos = 0;
 #pragma unroll
-      for (int b2 = 0; b2 < NB; ++b2) {
-        uint32_t bits = 0;
-        if (inb) {
+      for (int g = 0; g < NB; g += PK) {
+        uint32_t bits[PK];
 #pragma unroll
-          for (int q = 0; q < IPTM; ++q) bits |= (uint32_t)((uint32_t)x[b2][q] - (uint32_t)lo <= span) << q;
-        } else {
+        for (int b = 0; b < PK; ++b) {
+          bits[b] = 0;
+          if (inb) {
 #pragma unroll
-          for (int q = 0; q < IPTM; ++q) {
-            const int64_t e = s0[b2] + (int64_t)q * bt;
-            bits |= (uint32_t)(e < n && (uint32_t)x[b2][q] - (uint32_t)lo <= span) << q;
+            for (int q = 0; q < IPTM; ++q) bits[b] |= (uint32_t)((uint32_t)x[g + b][q] - (uint32_t)lo <= span) << q;
+          } else {
+#pragma unroll
+            for (int q = 0; q < IPTM; ++q) {
+              const int64_t e = s0[g + b] + (int64_t)q * bt;
+              bits[b] |= (uint32_t)(e < n && (uint32_t)x[g + b][q] - (uint32_t)lo <= span) << q;
+            }
           }
         }
-        const int cl = __popc(bits);
-        int pre = cl;  // inclusive warp scan of the lanes' counts
+        uint32_t word = 0;
+#pragma unroll
+        for (int b = 0; b < PK; ++b) word |= (uint32_t)__popc(bits[b]) << (FB * b);
+        uint32_t pre = word;  // inclusive warp scan of the packed counts
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, pre, o);
+          const uint32_t y = __shfl_up_sync(0xffffffffu, pre, o);
           if ((int)lane >= o) pre += y;
         }
-        int p = pos + pre - cl;
+        const uint32_t tot = __shfl_sync(0xffffffffu, pre, 31);
+        const uint32_t exc = pre - word;
 #pragma unroll
-        for (int q = 0; q < IPTM; ++q)
-          if ((bits >> q) & 1u) wb[p++] = x[b2][q];
-        pos += __shfl_sync(0xffffffffu, pre, 31);
+        for (int b = 0; b < PK; ++b) {
+          constexpr uint32_t M = (1u << FB) - 1u;
+          int p = pos + (int)((exc >> (FB * b)) & M);
+#pragma unroll
+          for (int q = 0; q < IPTM; ++q)
+            if ((bits[b] >> q) & 1u) wb[p++] = x[g + b][q];
+          pos += (int)((tot >> (FB * b)) & M);
+        }
       }
       __syncwarp();
       for (int i = (int)lane; i < pos; i += 32) __stcs(out + off + i, wb[i]);
