@@ -581,6 +581,160 @@ __global__ void __launch_bounds__(BT, 2) select_rr_kernel(const int32_t* __restr
   if (threadIdx.x == 0 && mine) atomicAdd(reinterpret_cast<unsigned long long*>(total_out), (unsigned long long)mine);
 }
 
+// Warp-specialised form of select_rr_kernel (same rounds, counts and output):
+// warps [0, W/2) only COUNT (HBM, evict_last) and warps [W/2, W) only WRITE
+// (L2 re-read, evict_first), each role synchronised on its own named barrier,
+// both joined once per iteration.  In the phase-alternating kernel every CTA
+// (and, through the count exchange, the whole grid) alternates between an
+// HBM read burst and an L2-read / HBM-write burst, so an iteration costs
+// t_count + t_write; here the two overlap inside every SM.  Write warp ww
+// re-reads the rows count warp ww counted LAG iterations earlier; write warp 0
+// loads the next round's CTA counts at the end of an iteration so the
+// exchange read is in flight across the iteration barrier.
+// PF 1: each count warp bulk-prefetches its NEXT round's rows into L2 as it
+// starts counting this round's (more HBM bytes in flight than its registers hold; half the
+// warps count, so a count-only round -- sigma = 0 -- is otherwise short of
+// memory-level parallelism).
+template <int BT, int WU, int LAG, int UW, int U, int PF = 0>
+__global__ void __launch_bounds__(BT, 2) select_rr_ws_kernel(const int32_t* __restrict__ in, int64_t n, int32_t lo,
+                                                             int32_t hi, int32_t* __restrict__ out, int rounds,
+                                                             uint32_t* counts, long long* total_out) {
+  constexpr int W = BT / 32, CW = W / 2;
+  constexpr int PER = (kRrMaxG + 31) / 32;
+  constexpr int NS = LAG + 1;
+  static_assert(W % 2 == 0 && WU % (128 * U) == 0 && WU % (32 * UW) == 0, "warp unit");
+  __shared__ int s_wc[NS][CW];
+  __shared__ long long s_off;
+  const int G = gridDim.x, c = blockIdx.x;
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  const unsigned lt = lanemask_lt_u32();
+  const uint32_t span = (uint32_t)hi - (uint32_t)lo;
+  const int64_t seg = (int64_t)G * CW * WU;
+  const bool vec_ok = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+  long long base = 0;  // write warp 0: rows selected in rounds [0, resolved)
+  int resolved = 0;
+  long long mine = 0;  // thread 0: this CTA's selected rows
+  uint32_t cv[PER];    // write warp 0: the counts of the next round to write
+#pragma unroll
+  for (int i = 0; i < PER; ++i) cv[i] = 0u;
+  for (int k = 0; k < rounds + LAG; ++k) {
+    const int j = k - LAG;
+    if (warp < CW) {
+      if (k < rounds) {  // ---- COUNT round k
+        const uint64_t keep = pipe::policy_evict_last();
+        const int64_t r0 = k * seg + ((int64_t)c * CW + warp) * WU;
+        if constexpr (PF == 1) {  // in flight alongside this round's loads
+          const int64_t rn = r0 + seg;
+          if (lane == 0 && vec_ok && rn + WU <= n) pipe::l2_prefetch_bulk(in + rn, 4u * WU);
+        }
+        int cnt = 0;
+        if (vec_ok && r0 + WU <= n) {
+          for (int u = 0; u < WU; u += 128 * U) {
+            int4 v[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q) v[q] = ld_hint4(in + r0 + u + q * 128 + 4 * lane, keep);
+#pragma unroll
+            for (int q = 0; q < U; ++q)
+              cnt += ((uint32_t)v[q].x - (uint32_t)lo <= span) + ((uint32_t)v[q].y - (uint32_t)lo <= span) +
+                     ((uint32_t)v[q].z - (uint32_t)lo <= span) + ((uint32_t)v[q].w - (uint32_t)lo <= span);
+          }
+        } else {
+          for (int64_t i = r0 + lane; i < min(r0 + WU, n); i += 32)
+            cnt += (uint32_t)ld_hint1(in + i, keep) - (uint32_t)lo <= span;
+        }
+        cnt = warp_sum(cnt);
+        if (lane == 0) s_wc[k % NS][warp] = cnt;
+        asm volatile("bar.sync 1, %0;" ::"n"(BT / 2) : "memory");  // count warps only
+        if (threadIdx.x == 0) {
+          int tot = 0;
+#pragma unroll
+          for (int w = 0; w < CW; ++w) tot += s_wc[k % NS][w];
+          st_relaxed_u32(counts + (size_t)k * G + c, (uint32_t)tot + 1u);
+          mine += tot;
+        }
+      }
+    } else if (j >= 0) {
+      const int ww = (int)warp - CW;
+      int any = 0;
+#pragma unroll
+      for (int w = 0; w < CW; ++w) any |= s_wc[j % NS][w];
+      if (any) {  // uniform over the write warps
+        if (ww == 0) {  // ---- offset of this CTA's share of round j
+          for (; resolved < j; ++resolved) {  // totals of skipped rounds
+            long long t = 0;
+            for (int cc = (int)lane; cc < G; cc += 32) {
+              uint32_t x;
+              while ((x = ld_relaxed_u32(counts + (size_t)resolved * G + cc)) == 0u) __nanosleep(32);
+              t += (long long)x - 1;
+            }
+            base += warp_sum(t);
+          }
+          long long before = 0, all = 0;
+#pragma unroll
+          for (int i = 0; i < PER; ++i) {
+            const int cc = i * 32 + (int)lane;
+            if (cc < G)
+              while (cv[i] == 0u) {  // not prefetched / not yet published
+                cv[i] = ld_relaxed_u32(counts + (size_t)j * G + cc);
+                if (cv[i] == 0u) __nanosleep(32);
+              }
+            const long long x = cc < G ? (long long)cv[i] - 1 : 0;
+            all += x;
+            before += cc < c ? x : 0;
+          }
+          before = warp_sum(before);
+          all = warp_sum(all);
+          if (lane == 0) s_off = base + before;
+          base += all;
+          resolved = j + 1;
+        }
+        asm volatile("bar.sync 2, %0;" ::"n"(BT / 2) : "memory");  // write warps only: s_off published
+        if (s_wc[j % NS][ww] != 0) {  // ---- WRITE this warp's rows of round j, re-read from L2
+          const uint64_t drop = pipe::policy_evict_first();
+          long long off = s_off;
+#pragma unroll
+          for (int w = 0; w < CW; ++w) off += w < ww ? s_wc[j % NS][w] : 0;
+          int32_t* o = out + off;
+          const int64_t r0 = j * seg + ((int64_t)c * CW + ww) * WU;
+          if (r0 + WU <= n) {
+            for (int u = 0; u < WU; u += 32 * UW) {
+              int32_t x[UW];
+#pragma unroll
+              for (int q = 0; q < UW; ++q) x[q] = ld_hint1(in + r0 + u + q * 32 + lane, drop);
+#pragma unroll
+              for (int q = 0; q < UW; ++q) {
+                const bool p = (uint32_t)x[q] - (uint32_t)lo <= span;
+                const unsigned m = __ballot_sync(0xffffffffu, p);
+                if (p) __stcs(o + __popc(m & lt), x[q]);
+                o += __popc(m);
+              }
+            }
+          } else {
+            for (int64_t i0 = r0; i0 < min(r0 + WU, n); i0 += 32) {
+              const int64_t i = i0 + lane;
+              const int32_t x = i < n ? ld_hint1(in + i, drop) : 0;
+              const bool p = i < n && (uint32_t)x - (uint32_t)lo <= span;
+              const unsigned m = __ballot_sync(0xffffffffu, p);
+              if (p) __stcs(o + __popc(m & lt), x);
+              o += __popc(m);
+            }
+          }
+        }
+      }
+      if (ww == 0) {  // the next round's counts: in flight across the barrier
+        const int jn = j + 1;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+          const int cc = i * 32 + (int)lane;
+          cv[i] = (jn < rounds && cc < G) ? ld_relaxed_u32(counts + (size_t)jn * G + cc) : 0u;
+        }
+      }
+    }
+    __syncthreads();  // s_wc of round k visible to the write warps; slot (k+1) % NS free
+  }
+  if (threadIdx.x == 0 && mine) atomicAdd(reinterpret_cast<unsigned long long*>(total_out), (unsigned long long)mine);
+}
+
 // Walks units (logical tile, 32-thread group) in order from unit u0 with one
 // division: next() = this lane's first slot of the next unit.
 struct UnitCursor {
@@ -812,6 +966,213 @@ __global__ void __launch_bounds__(BT, 2) select_rr_crystal_kernel(const int32_t*
       off += pos;
       __syncwarp();
     }
+  }
+  if (threadIdx.x == 0 && mine) atomicAdd(reinterpret_cast<unsigned long long*>(total_out), (unsigned long long)mine);
+}
+
+// Warp-specialised form of select_rr_crystal_kernel (same rounds, counts and
+// output; see select_rr_ws_kernel): warps [0, W/2) count 2 UPW units each per
+// round from HBM, warps [W/2, W) re-read and write them LAG rounds later, so
+// the HBM count stream and the issue-heavy compaction overlap inside an SM.
+template <int BT, int IPTM, int LAG>
+__global__ void __launch_bounds__(BT, 2) select_rr_crystal_ws_kernel(const int32_t* __restrict__ in, int64_t n,
+                                                                     int32_t lo, int32_t hi, int bt, int ipt,
+                                                                     int32_t* __restrict__ out, int rounds,
+                                                                     uint32_t* counts, long long* total_out) {
+  constexpr int W = BT / 32, CW = W / 2;
+  constexpr int UPW = 2 * (1024 / (32 * IPTM) > 0 ? 1024 / (32 * IPTM) : 1);  // units per count warp per round
+  constexpr int NB = IPTM >= 16 ? 1 : 16 / IPTM;
+  static_assert(UPW % NB == 0 && W % 2 == 0, "batches");
+  constexpr int PER = (kRrMaxG + 31) / 32;
+  constexpr int NS = LAG + 1;
+  __shared__ int s_wc[NS][CW];
+  __shared__ long long s_off;
+  __shared__ int32_t s_stage[CW * NB * 32 * IPTM];  // per write warp: one batch of compacted output
+  const int G = gridDim.x, c = blockIdx.x;
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t span = (uint32_t)hi - (uint32_t)lo;
+  const int gpt = bt >> 5;
+  const int64_t S = (int64_t)bt * IPTM;
+  const int64_t upr = (int64_t)G * CW * UPW;
+  const bool whole = UPW % gpt == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+  long long base = 0;
+  int resolved = 0;
+  long long mine = 0;
+  uint32_t cv[PER];
+#pragma unroll
+  for (int i = 0; i < PER; ++i) cv[i] = 0u;
+  for (int k = 0; k < rounds + LAG; ++k) {
+    const int j = k - LAG;
+    if (warp < CW) {
+      if (k < rounds) {  // ---- COUNT round k (order does not matter here)
+        const uint64_t keep = pipe::policy_evict_last();
+        const int64_t u0 = k * upr + ((int64_t)c * CW + warp) * UPW;
+        int cnt = 0;
+        if (whole) {
+          const int64_t r0 = (u0 / gpt) * S, r1 = min(r0 + (int64_t)(UPW / gpt) * S, n);
+          int64_t wb = r0;
+          for (; wb + 1024 <= r1; wb += 1024) {
+            int4 v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = ld_hint4(in + wb + q * 128 + 4 * lane, keep);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              cnt += ((uint32_t)v[q].x - (uint32_t)lo <= span) + ((uint32_t)v[q].y - (uint32_t)lo <= span) +
+                     ((uint32_t)v[q].z - (uint32_t)lo <= span) + ((uint32_t)v[q].w - (uint32_t)lo <= span);
+          }
+          for (int64_t e = wb + lane; e < r1; e += 32) cnt += (uint32_t)ld_hint1(in + e, keep) - (uint32_t)lo <= span;
+        } else {
+          UnitCursor uc(u0, gpt, S, lane);
+          for (int ub = 0; ub < UPW; ub += NB) {
+            int64_t s0[NB];
+#pragma unroll
+            for (int b2 = 0; b2 < NB; ++b2) s0[b2] = uc.next();
+            const bool inb = s0[NB - 1] - (int64_t)lane + 31 + (int64_t)(IPTM - 1) * bt < n;
+#pragma unroll
+            for (int b2 = 0; b2 < NB; ++b2) {
+              const int32_t* p = in + s0[b2];
+#pragma unroll
+              for (int q = 0; q < IPTM; ++q)
+                if ((inb || s0[b2] + (int64_t)q * bt < n)) cnt += (uint32_t)ld_hint1(p + q * bt, keep) - (uint32_t)lo <= span;
+            }
+          }
+        }
+        cnt = warp_sum(cnt);
+        if (lane == 0) s_wc[k % NS][warp] = cnt;
+        asm volatile("bar.sync 1, %0;" ::"n"(BT / 2) : "memory");  // count warps only
+        if (threadIdx.x == 0) {
+          int tot = 0;
+#pragma unroll
+          for (int w = 0; w < CW; ++w) tot += s_wc[k % NS][w];
+          st_relaxed_u32(counts + (size_t)k * G + c, (uint32_t)tot + 1u);
+          mine += tot;
+        }
+      }
+    } else if (j >= 0) {
+      const int ww = (int)warp - CW;
+      int any = 0;
+#pragma unroll
+      for (int w = 0; w < CW; ++w) any |= s_wc[j % NS][w];
+      if (any) {  // uniform over the write warps
+        if (ww == 0) {
+          for (; resolved < j; ++resolved) {
+            long long t = 0;
+            for (int cc = (int)lane; cc < G; cc += 32) {
+              uint32_t x;
+              while ((x = ld_relaxed_u32(counts + (size_t)resolved * G + cc)) == 0u) __nanosleep(32);
+              t += (long long)x - 1;
+            }
+            base += warp_sum(t);
+          }
+          long long before = 0, all = 0;
+#pragma unroll
+          for (int i = 0; i < PER; ++i) {
+            const int cc = i * 32 + (int)lane;
+            if (cc < G)
+              while (cv[i] == 0u) {
+                cv[i] = ld_relaxed_u32(counts + (size_t)j * G + cc);
+                if (cv[i] == 0u) __nanosleep(32);
+              }
+            const long long x = cc < G ? (long long)cv[i] - 1 : 0;
+            all += x;
+            before += cc < c ? x : 0;
+          }
+          before = warp_sum(before);
+          all = warp_sum(all);
+          if (lane == 0) s_off = base + before;
+          base += all;
+          resolved = j + 1;
+        }
+        asm volatile("bar.sync 2, %0;" ::"n"(BT / 2) : "memory");  // write warps only: s_off published
+        if (s_wc[j % NS][ww] != 0) {
+          const uint64_t drop = pipe::policy_evict_first();
+          long long off = s_off;
+#pragma unroll
+          for (int w = 0; w < CW; ++w) off += w < ww ? s_wc[j % NS][w] : 0;
+          const int64_t u0 = j * upr + ((int64_t)c * CW + ww) * UPW;
+          UnitCursor uc(u0, gpt, S, lane);
+          int32_t* wb = s_stage + ww * (NB * 32 * IPTM);
+          for (int ub = 0; ub < UPW; ub += NB) {  // ---- WRITE round j
+            int64_t s0[NB];
+#pragma unroll
+            for (int b2 = 0; b2 < NB; ++b2) s0[b2] = uc.next();
+            if (s0[0] - lane >= n) break;  // warp-uniform
+            int32_t x[NB][IPTM];
+            const bool inb = s0[NB - 1] - (int64_t)lane + 31 + (int64_t)(IPTM - 1) * bt < n;
+            if (inb) {
+#pragma unroll
+              for (int b2 = 0; b2 < NB; ++b2) {
+                const int32_t* p = in + s0[b2];
+#pragma unroll
+                for (int q = 0; q < IPTM; ++q) x[b2][q] = ld_hint1(p + q * bt, drop);
+              }
+            } else {
+#pragma unroll
+              for (int b2 = 0; b2 < NB; ++b2)
+#pragma unroll
+                for (int q = 0; q < IPTM; ++q) {
+                  const int64_t e = s0[b2] + (int64_t)q * bt;
+                  x[b2][q] = e < n ? ld_hint1(in + e, drop) : 0;
+                }
+            }
+            constexpr int FB = 32 * IPTM < 256 ? 8 : 16;
+            constexpr int PK = IPTM < 4 ? 1 : (32 / FB < NB ? 32 / FB : NB);
+            int pos = 0;
+#pragma unroll
+            for (int g = 0; g < NB; g += PK) {
+              uint32_t bits[PK];
+#pragma unroll
+              for (int b = 0; b < PK; ++b) {
+                bits[b] = 0;
+                if (inb) {
+#pragma unroll
+                  for (int q = 0; q < IPTM; ++q) bits[b] |= (uint32_t)((uint32_t)x[g + b][q] - (uint32_t)lo <= span) << q;
+                } else {
+#pragma unroll
+                  for (int q = 0; q < IPTM; ++q) {
+                    const int64_t e = s0[g + b] + (int64_t)q * bt;
+                    bits[b] |= (uint32_t)(e < n && (uint32_t)x[g + b][q] - (uint32_t)lo <= span) << q;
+                  }
+                }
+              }
+              uint32_t word = 0;
+#pragma unroll
+              for (int b = 0; b < PK; ++b) word |= (uint32_t)__popc(bits[b]) << (FB * b);
+              uint32_t pre = word;
+#pragma unroll
+              for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, pre, o);
+                if ((int)lane >= o) pre += y;
+              }
+              const uint32_t tot = __shfl_sync(0xffffffffu, pre, 31);
+              const uint32_t exc = pre - word;
+#pragma unroll
+              for (int b = 0; b < PK; ++b) {
+                constexpr uint32_t M = (1u << FB) - 1u;
+                int p = pos + (int)((exc >> (FB * b)) & M);
+#pragma unroll
+                for (int q = 0; q < IPTM; ++q)
+                  if ((bits[b] >> q) & 1u) wb[p++] = x[g + b][q];
+                pos += (int)((tot >> (FB * b)) & M);
+              }
+            }
+            __syncwarp();
+            for (int i = (int)lane; i < pos; i += 32) __stcs(out + off + i, wb[i]);
+            off += pos;
+            __syncwarp();
+          }
+        }
+      }
+      if (ww == 0) {  // the next round's counts: in flight across the barrier
+        const int jn = j + 1;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+          const int cc = i * 32 + (int)lane;
+          cv[i] = (jn < rounds && cc < G) ? ld_relaxed_u32(counts + (size_t)jn * G + cc) : 0u;
+        }
+      }
+    }
+    __syncthreads();
   }
   if (threadIdx.x == 0 && mine) atomicAdd(reinterpret_cast<unsigned long long*>(total_out), (unsigned long long)mine);
 }
@@ -1742,21 +2103,30 @@ struct RrLaunch {
 
 RrLaunch rr_plan(crys_ctx* ctx, int64_t n) {
   RrLaunch r;
-  int wu = 0;
-  auto pick = [&](auto fn, int bt, int rows_per_warp) {
+  int wu = 0, cwarps = 0;
+  auto pick = [&](auto fn, int bt, int rows_per_warp, int count_warps = 0) {
     r.fn = (const void*)fn;
     r.bt = bt;
     wu = rows_per_warp;
+    cwarps = count_warps ? count_warps : bt / 32;
   };
   switch (sel_rr_variant()) {  // segment = 296 CTAs x warps x rows per warp (x 4 B)
     case 1: pick(select_rr_kernel<512, 1024, 2, 16>, 512, 1024); break;  // 19.4 MB, lag 2, 16 loads
     case 2: pick(select_rr_kernel<512, 768, 2, 8>, 512, 768); break;     // 14.5 MB, lag 2
     case 3: pick(select_rr_kernel<512, 768, 3, 8>, 512, 768); break;     // 14.5 MB, lag 3
     case 4: pick(select_rr_kernel<512, 1024, 2, 4>, 512, 1024); break;   // 19.4 MB, lag 2, 4 loads
+    // warp-specialised (half the warps count, half write): rows per COUNT warp
+    case 5: pick(select_rr_ws_kernel<512, 2048, 2, 16, 8>, 512, 2048, 8); break;  // 19.4 MB, lag 2
+    case 6: pick(select_rr_ws_kernel<512, 2048, 2, 8, 8>, 512, 2048, 8); break;   // 19.4 MB, lag 2, 8 loads
+    case 7: pick(select_rr_ws_kernel<512, 1024, 2, 16, 8>, 512, 1024, 8); break;  // 9.7 MB, lag 2
+    case 8: pick(select_rr_ws_kernel<512, 2048, 3, 16, 8>, 512, 2048, 8); break;  // 19.4 MB, lag 3
+    case 9: pick(select_rr_ws_kernel<512, 4096, 2, 16, 8>, 512, 4096, 8); break;  // 38.8 MB, lag 2
+    case 10: pick(select_rr_ws_kernel<512, 2048, 2, 16, 8, 1>, 512, 2048, 8); break;  // 5 + next-round L2 prefetch
+    case 11: pick(select_rr_ws_kernel<512, 1024, 2, 16, 8, 1>, 512, 1024, 8); break;  // 7 + next-round L2 prefetch
     default: pick(select_rr_kernel<512, 1024, 2, 8>, 512, 1024); break;  // 19.4 MB, lag 2
   }
   const int per_sm = occupancy(r.fn, r.bt, 0);
-  const int64_t per_cta = (int64_t)(r.bt / 32) * wu;
+  const int64_t per_cta = (int64_t)cwarps * wu;
   r.grid = (int)std::min<int64_t>({(int64_t)per_sm * ctx->num_sms, (int64_t)kRrMaxG, (n + per_cta - 1) / per_cta});
   const int64_t seg = (int64_t)r.grid * per_cta;
   r.rounds = (int)((n + seg - 1) / seg);
@@ -1772,6 +2142,15 @@ bool sel_rr_crystal() {
   return v;
 }
 
+// CRYS_SEL_RRC_WS=1: Crystal-order selects on the warp-specialised kernel.
+bool sel_rrc_ws() {
+  static const bool v = [] {
+    const char* e = getenv("CRYS_SEL_RRC_WS");
+    return e && atoi(e) == 1;
+  }();
+  return v;
+}
+
 RrLaunch rr_plan_crystal(crys_ctx* ctx, int64_t n, int bt, int ipt) {
   RrLaunch r;
   constexpr int kBT = 512, kLag = 2;
@@ -1779,12 +2158,22 @@ RrLaunch rr_plan_crystal(crys_ctx* ctx, int64_t n, int bt, int ipt) {
   // (a ~19 MB segment, as the input-order kernel); IPTM = ipt rounded up
   int iptm = 1;
   while (iptm < ipt) iptm <<= 1;
-  switch (iptm) {
-    case 1: r.fn = (const void*)select_rr_crystal_kernel<kBT, 1, kLag>; break;
-    case 2: r.fn = (const void*)select_rr_crystal_kernel<kBT, 2, kLag>; break;
-    case 4: r.fn = (const void*)select_rr_crystal_kernel<kBT, 4, kLag>; break;
-    case 8: r.fn = (const void*)select_rr_crystal_kernel<kBT, 8, kLag>; break;
-    default: r.fn = (const void*)select_rr_crystal_kernel<kBT, 16, kLag>; break;
+  if (sel_rrc_ws()) {  // warp-specialised: half the warps count 2x the units (same segment)
+    switch (iptm) {
+      case 1: r.fn = (const void*)select_rr_crystal_ws_kernel<kBT, 1, kLag>; break;
+      case 2: r.fn = (const void*)select_rr_crystal_ws_kernel<kBT, 2, kLag>; break;
+      case 4: r.fn = (const void*)select_rr_crystal_ws_kernel<kBT, 4, kLag>; break;
+      case 8: r.fn = (const void*)select_rr_crystal_ws_kernel<kBT, 8, kLag>; break;
+      default: r.fn = (const void*)select_rr_crystal_ws_kernel<kBT, 16, kLag>; break;
+    }
+  } else {
+    switch (iptm) {
+      case 1: r.fn = (const void*)select_rr_crystal_kernel<kBT, 1, kLag>; break;
+      case 2: r.fn = (const void*)select_rr_crystal_kernel<kBT, 2, kLag>; break;
+      case 4: r.fn = (const void*)select_rr_crystal_kernel<kBT, 4, kLag>; break;
+      case 8: r.fn = (const void*)select_rr_crystal_kernel<kBT, 8, kLag>; break;
+      default: r.fn = (const void*)select_rr_crystal_kernel<kBT, 16, kLag>; break;
+    }
   }
   const int upw = std::max(1, 1024 / (32 * iptm));
   r.bt = kBT;
