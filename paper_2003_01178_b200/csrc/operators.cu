@@ -1,9 +1,11 @@
 // operators.cu -- selection, projection and hash-join microbenchmark kernels.
 //
-//   select_rr_kernel       select_{branching,predicated}_into(workers=1)
+//   select_rr_ws_kernel    select_{branching,predicated}_into(workers=1)
 //                          (select.hpp:56-91): input-order output, persistent
-//                          round-robin over L2-sized segments (count from HBM,
-//                          write from L2 one exchange later); select_seg_kernel
+//                          round-robin over L2-sized segments (count warps read
+//                          HBM, write warps re-read L2 two rounds later, both
+//                          roles in every CTA; select_rr_kernel alternates the
+//                          two phases in all warps, CRYS_SEL_RR=12); select_seg_kernel
 //                          (segmented launches) and select_input_kernel
 //                          (decoupled look-back) are the A/B forms
 //   select_rr_crystal_kernel / select_crystal_reg_kernel / select_crystal_kernel
@@ -450,6 +452,16 @@ __device__ __forceinline__ int32_t ld_hint1(const int32_t* p, uint64_t pol) {
   return r;
 }
 
+// Predicated shared store at a 32-bit shared address: one @p STS (the C++
+// form `if (bit) wb[p++] = x` compiled to a branch, a reconvergence pair and a
+// re-materialised shared base per item -- ~10 instructions per slot).
+__device__ __forceinline__ void sts_if(uint32_t addr, int32_t v, uint32_t p) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.b32 [%0], %1;\n\t}" ::"r"(addr), "r"(v),
+      "r"(p)
+      : "memory");
+}
+
 constexpr int kRrMaxG = 32 * 10;  // counts per round read by one warp (<= 10 per lane; 2 CTAs x 148 SMs = 296)
 
 template <int BT, int WU, int LAG, int UW>
@@ -594,7 +606,10 @@ __global__ void __launch_bounds__(BT, 2) select_rr_kernel(const int32_t* __restr
 // PF 1: each count warp bulk-prefetches its NEXT round's rows into L2 as it
 // starts counting this round's (more HBM bytes in flight than its registers hold; half the
 // warps count, so a count-only round -- sigma = 0 -- is otherwise short of
-// memory-level parallelism).
+// memory-level parallelism: sigma 0 0.39 -> 0.37 ms), but the extra L2
+// footprint pushes counted rows out before the write warps re-read them
+// (sigma 0.5 0.65 -> 0.73 ms), so it is off by default; prefetching only after
+// rounds the CTA selected nothing from measured 0.41 ms at sigma 0 and was dropped.
 template <int BT, int WU, int LAG, int UW, int U, int PF = 0>
 __global__ void __launch_bounds__(BT, 2) select_rr_ws_kernel(const int32_t* __restrict__ in, int64_t n, int32_t lo,
                                                              int32_t hi, int32_t* __restrict__ out, int rounds,
@@ -916,6 +931,7 @@ __global__ void __launch_bounds__(BT, 2) select_rr_crystal_kernel(const int32_t*
       // the batch's compacted output in this warp's staging buffer, then one
       // coalesced copy (per-lane runs straight to global scatter each store)
       int32_t* wb = s_stage + warp * (NB * 32 * IPTM);
+      const uint32_t wb_s = (uint32_t)__cvta_generic_to_shared(wb);
       // one warp scan for PK units at a time: their lane counts packed into
       // FB-bit fields of one word (a unit's prefix is at most 32 * IPTM)
       constexpr int FB = 32 * IPTM < 256 ? 8 : 16;
@@ -954,10 +970,13 @@ __global__ void __launch_bounds__(BT, 2) select_rr_crystal_kernel(const int32_t*
 #pragma unroll
         for (int b = 0; b < PK; ++b) {
           constexpr uint32_t M = (1u << FB) - 1u;
-          int p = pos + (int)((exc >> (FB * b)) & M);
+          uint32_t a = wb_s + 4u * (uint32_t)(pos + (int)((exc >> (FB * b)) & M));
 #pragma unroll
-          for (int q = 0; q < IPTM; ++q)
-            if ((bits[b] >> q) & 1u) wb[p++] = x[g + b][q];
+          for (int q = 0; q < IPTM; ++q) {
+            const uint32_t m = (bits[b] >> q) & 1u;
+            sts_if(a, x[g + b][q], m);
+            a += 4u * m;
+          }
           pos += (int)((tot >> (FB * b)) & M);
         }
       }
@@ -1092,6 +1111,7 @@ __global__ void __launch_bounds__(BT, 2) select_rr_crystal_ws_kernel(const int32
           const int64_t u0 = j * upr + ((int64_t)c * CW + ww) * UPW;
           UnitCursor uc(u0, gpt, S, lane);
           int32_t* wb = s_stage + ww * (NB * 32 * IPTM);
+          const uint32_t wb_s = (uint32_t)__cvta_generic_to_shared(wb);
           for (int ub = 0; ub < UPW; ub += NB) {  // ---- WRITE round j
             int64_t s0[NB];
 #pragma unroll
@@ -1149,10 +1169,13 @@ __global__ void __launch_bounds__(BT, 2) select_rr_crystal_ws_kernel(const int32
 #pragma unroll
               for (int b = 0; b < PK; ++b) {
                 constexpr uint32_t M = (1u << FB) - 1u;
-                int p = pos + (int)((exc >> (FB * b)) & M);
+                uint32_t a = wb_s + 4u * (uint32_t)(pos + (int)((exc >> (FB * b)) & M));
 #pragma unroll
-                for (int q = 0; q < IPTM; ++q)
-                  if ((bits[b] >> q) & 1u) wb[p++] = x[g + b][q];
+                for (int q = 0; q < IPTM; ++q) {
+                  const uint32_t m = (bits[b] >> q) & 1u;
+                  sts_if(a, x[g + b][q], m);
+                  a += 4u * m;
+                }
                 pos += (int)((tot >> (FB * b)) & M);
               }
             }
@@ -2123,7 +2146,8 @@ RrLaunch rr_plan(crys_ctx* ctx, int64_t n) {
     case 9: pick(select_rr_ws_kernel<512, 4096, 2, 16, 8>, 512, 4096, 8); break;  // 38.8 MB, lag 2
     case 10: pick(select_rr_ws_kernel<512, 2048, 2, 16, 8, 1>, 512, 2048, 8); break;  // 5 + next-round L2 prefetch
     case 11: pick(select_rr_ws_kernel<512, 1024, 2, 16, 8, 1>, 512, 1024, 8); break;  // 7 + next-round L2 prefetch
-    default: pick(select_rr_kernel<512, 1024, 2, 8>, 512, 1024); break;  // 19.4 MB, lag 2
+    case 12: pick(select_rr_kernel<512, 1024, 2, 8>, 512, 1024); break;  // phase-alternating (r02 default before the split roles)
+    default: pick(select_rr_ws_kernel<512, 2048, 2, 16, 8>, 512, 2048, 8); break;  // = 5 (r02 final default)
   }
   const int per_sm = occupancy(r.fn, r.bt, 0);
   const int64_t per_cta = (int64_t)cwarps * wu;
