@@ -156,6 +156,16 @@ __device__ __forceinline__ void BlockLoadStriped(const int32_t* __restrict__ til
   }
 }
 
+// Predicated shared store at a 32-bit shared address: one @p STS (the C++
+// form `if (bit) wb[p++] = x` compiled to a branch, a reconvergence pair and a
+// re-materialised shared base per item -- ~10 instructions per slot).
+__device__ __forceinline__ void sts_if(uint32_t addr, int32_t v, uint32_t p) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.b32 [%0], %1;\n\t}" ::"r"(addr), "r"(v),
+      "r"(p)
+      : "memory");
+}
+
 // BlockShuffle (block_ops.hpp:101-122), the per-thread step: this thread's
 // flagged items, in item (stride) order, written from s_out[prefix] on --
 // with `prefix` from BlockScan of the per-thread counts the tile comes out
@@ -163,11 +173,22 @@ __device__ __forceinline__ void BlockLoadStriped(const int32_t* __restrict__ til
 // thread's count.  The caller barriers before the compacted tile is read.
 template <int IPT, class T>
 __device__ __forceinline__ int BlockShuffle(const T (&items)[IPT], unsigned flags, int prefix, T* s_out) {
-  int pos = prefix;
+  if constexpr (sizeof(T) == 4) {  // predicated STS, no branch per item
+    uint32_t a = (uint32_t)__cvta_generic_to_shared(s_out + prefix);
 #pragma unroll
-  for (int k = 0; k < IPT; ++k)
-    if ((flags >> k) & 1u) s_out[pos++] = items[k];
-  return pos - prefix;
+    for (int k = 0; k < IPT; ++k) {
+      const uint32_t m = (flags >> k) & 1u;
+      sts_if(a, reinterpret_cast<const int32_t&>(items[k]), m);
+      a += 4u * m;
+    }
+    return __popc(flags & (IPT >= 32 ? 0xffffffffu : ((1u << IPT) - 1u)));
+  } else {
+    int pos = prefix;
+#pragma unroll
+    for (int k = 0; k < IPT; ++k)
+      if ((flags >> k) & 1u) s_out[pos++] = items[k];
+    return pos - prefix;
+  }
 }
 
 // BlockStore (block_ops.hpp:125-131): the compacted tile s_tile[0, n) to

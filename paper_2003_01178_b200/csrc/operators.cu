@@ -166,11 +166,15 @@ __device__ __forceinline__ void sel_scatter(const int4 (&v)[IPT / 4], const unsi
                                             const int (&pos)[IPT / 4], int woff, int32_t* s_items) {
 #pragma unroll
   for (int j = 0; j < IPT / 4; ++j) {
-    int p = woff + pos[j];
-    if (bits[j] & 1u) s_items[p++] = v[j].x;
-    if (bits[j] & 2u) s_items[p++] = v[j].y;
-    if (bits[j] & 4u) s_items[p++] = v[j].z;
-    if (bits[j] & 8u) s_items[p++] = v[j].w;
+    uint32_t a = (uint32_t)__cvta_generic_to_shared(s_items + woff + pos[j]);
+    const uint32_t b = bits[j];
+    sts_if(a, v[j].x, b & 1u);
+    a += 4u * (b & 1u);
+    sts_if(a, v[j].y, b & 2u);
+    a += 2u * (b & 2u);
+    sts_if(a, v[j].z, b & 4u);
+    a += b & 4u;
+    sts_if(a, v[j].w, b & 8u);
   }
 }
 
@@ -450,16 +454,6 @@ __device__ __forceinline__ int32_t ld_hint1(const int32_t* p, uint64_t pol) {
   int32_t r;
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
   return r;
-}
-
-// Predicated shared store at a 32-bit shared address: one @p STS (the C++
-// form `if (bit) wb[p++] = x` compiled to a branch, a reconvergence pair and a
-// re-materialised shared base per item -- ~10 instructions per slot).
-__device__ __forceinline__ void sts_if(uint32_t addr, int32_t v, uint32_t p) {
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.b32 [%0], %1;\n\t}" ::"r"(addr), "r"(v),
-      "r"(p)
-      : "memory");
 }
 
 constexpr int kRrMaxG = 32 * 10;  // counts per round read by one warp (<= 10 per lane; 2 CTAs x 148 SMs = 296)
