@@ -8,7 +8,8 @@
 //                          two phases in all warps, CRYS_SEL_RR=12); select_seg_kernel
 //                          (segmented launches) and select_input_kernel
 //                          (decoupled look-back) are the A/B forms
-//   select_rr_crystal_kernel / select_crystal_reg_kernel / select_crystal_kernel
+//   select_rr_crystal_ws_kernel / select_rr_crystal_kernel /
+//   select_crystal_reg_kernel / select_crystal_kernel
 //                          select_tile_into(config, kDeterministic)
 //                          (select.hpp:107-135): the exact Crystal order for any
 //                          TileConfig (round-robin units of 32 logical threads
@@ -2160,11 +2161,13 @@ bool sel_rr_crystal() {
   return v;
 }
 
-// CRYS_SEL_RRC_WS=1: Crystal-order selects on the warp-specialised kernel.
+// CRYS_SEL_RRC_WS=0: Crystal-order selects on the phase-alternating kernel
+// (default: the warp-specialised one; 128x4 sigma 0.5 0.95 -> 0.85 ms, sigma 0
+// 0.37 -> 0.41).
 bool sel_rrc_ws() {
   static const bool v = [] {
     const char* e = getenv("CRYS_SEL_RRC_WS");
-    return e && atoi(e) == 1;
+    return !(e && atoi(e) == 0);
   }();
   return v;
 }
