@@ -605,7 +605,12 @@ __global__ void __launch_bounds__(BT, 2) select_rr_kernel(const int32_t* __restr
 // footprint pushes counted rows out before the write warps re-read them
 // (sigma 0.5 0.65 -> 0.73 ms), so it is off by default; prefetching only after
 // rounds the CTA selected nothing from measured 0.41 ms at sigma 0 and was dropped.
-template <int BT, int WU, int LAG, int UW, int U, int PF = 0>
+// VW: the write warps re-read their rows with 128-bit loads (UW int4 per lane
+// in flight), place each lane's matches in a per-warp shared staging buffer
+// with predicated stores at positions from four ballots, and copy the batch
+// out coalesced (the scalar form issues one 4-byte load, ballot and store per
+// 32 rows).
+template <int BT, int WU, int LAG, int UW, int U, int PF = 0, bool VW = false>
 __global__ void __launch_bounds__(BT, 2) select_rr_ws_kernel(const int32_t* __restrict__ in, int64_t n, int32_t lo,
                                                              int32_t hi, int32_t* __restrict__ out, int rounds,
                                                              uint32_t* counts, long long* total_out) {
@@ -613,8 +618,10 @@ __global__ void __launch_bounds__(BT, 2) select_rr_ws_kernel(const int32_t* __re
   constexpr int PER = (kRrMaxG + 31) / 32;
   constexpr int NS = LAG + 1;
   static_assert(W % 2 == 0 && WU % (128 * U) == 0 && WU % (32 * UW) == 0, "warp unit");
+  static_assert(!VW || WU % (128 * UW) == 0, "vector write batch");
   __shared__ int s_wc[NS][CW];
   __shared__ long long s_off;
+  __shared__ int32_t s_wst[VW ? CW * 128 * UW : 1];  // VW: per write warp, one batch of compacted rows
   const int G = gridDim.x, c = blockIdx.x;
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
   const unsigned lt = lanemask_lt_u32();
@@ -706,7 +713,38 @@ __global__ void __launch_bounds__(BT, 2) select_rr_ws_kernel(const int32_t* __re
           for (int w = 0; w < CW; ++w) off += w < ww ? s_wc[j % NS][w] : 0;
           int32_t* o = out + off;
           const int64_t r0 = j * seg + ((int64_t)c * CW + ww) * WU;
-          if (r0 + WU <= n) {
+          if (VW && vec_ok && r0 + WU <= n) {
+            int32_t* wb = s_wst + ww * (128 * UW);
+            const uint32_t wb_s = (uint32_t)__cvta_generic_to_shared(wb);
+            for (int u = 0; u < WU; u += 128 * UW) {
+              int4 v[UW];
+#pragma unroll
+              for (int q = 0; q < UW; ++q) v[q] = ld_hint4(in + r0 + u + q * 128 + 4 * lane, drop);
+              int pos = 0;
+#pragma unroll
+              for (int q = 0; q < UW; ++q) {
+                const bool p0 = (uint32_t)v[q].x - (uint32_t)lo <= span, p1 = (uint32_t)v[q].y - (uint32_t)lo <= span;
+                const bool p2 = (uint32_t)v[q].z - (uint32_t)lo <= span, p3 = (uint32_t)v[q].w - (uint32_t)lo <= span;
+                const unsigned b0 = __ballot_sync(0xffffffffu, p0), b1 = __ballot_sync(0xffffffffu, p1);
+                const unsigned b2 = __ballot_sync(0xffffffffu, p2), b3 = __ballot_sync(0xffffffffu, p3);
+                // rows before this lane's 4: all matches of lanes < lane (input order = lane, element)
+                const int ex = __popc(b0 & lt) + __popc(b1 & lt) + __popc(b2 & lt) + __popc(b3 & lt);
+                uint32_t a = wb_s + 4u * (uint32_t)(pos + ex);
+                sts_if(a, v[q].x, p0);
+                a += 4u * p0;
+                sts_if(a, v[q].y, p1);
+                a += 4u * p1;
+                sts_if(a, v[q].z, p2);
+                a += 4u * p2;
+                sts_if(a, v[q].w, p3);
+                pos += __popc(b0) + __popc(b1) + __popc(b2) + __popc(b3);
+              }
+              __syncwarp();
+              for (int i = (int)lane; i < pos; i += 32) __stcs(o + i, wb[i]);
+              o += pos;
+              __syncwarp();
+            }
+          } else if (r0 + WU <= n) {
             for (int u = 0; u < WU; u += 32 * UW) {
               int32_t x[UW];
 #pragma unroll
@@ -2142,7 +2180,8 @@ RrLaunch rr_plan(crys_ctx* ctx, int64_t n) {
     case 10: pick(select_rr_ws_kernel<512, 2048, 2, 16, 8, 1>, 512, 2048, 8); break;  // 5 + next-round L2 prefetch
     case 11: pick(select_rr_ws_kernel<512, 1024, 2, 16, 8, 1>, 512, 1024, 8); break;  // 7 + next-round L2 prefetch
     case 12: pick(select_rr_kernel<512, 1024, 2, 8>, 512, 1024); break;  // phase-alternating (r02 default before the split roles)
-    default: pick(select_rr_ws_kernel<512, 2048, 2, 16, 8>, 512, 2048, 8); break;  // = 5 (r02 final default)
+    case 13: pick(select_rr_ws_kernel<512, 2048, 2, 4, 8, 0, true>, 512, 2048, 8); break;  // default with 4 loads in flight
+    default: pick(select_rr_ws_kernel<512, 2048, 2, 8, 8, 0, true>, 512, 2048, 8); break;  // 5 + 128-bit staged writes (r02 final)
   }
   const int per_sm = occupancy(r.fn, r.bt, 0);
   const int64_t per_cta = (int64_t)cwarps * wu;

@@ -47,7 +47,7 @@ print("ok")
 @pytest.mark.parametrize("env", [{"CRYS_SEL_RR": "0"}, {"CRYS_SEL_RR": "1"}, {"CRYS_SEL_RR": "2"}, {"CRYS_SEL_RR": "3"},
                                  {"CRYS_SEL_RR": "4"}, {"CRYS_SEL_RR": "5"}, {"CRYS_SEL_RR": "6"},
                                  {"CRYS_SEL_RR": "7"}, {"CRYS_SEL_RR": "8"}, {"CRYS_SEL_RR": "9"}, {"CRYS_SEL_RR": "10"},
-                                 {"CRYS_SEL_RR": "11"}, {"CRYS_SEL_RR": "12"}, {"CRYS_SEL_RRC_WS": "0"}, {"CRYS_SEL_CFG": "2"}, {"CRYS_SEL_CFG": "3"},
+                                 {"CRYS_SEL_RR": "11"}, {"CRYS_SEL_RR": "12"}, {"CRYS_SEL_RR": "13"}, {"CRYS_SEL_RRC_WS": "0"}, {"CRYS_SEL_CFG": "2"}, {"CRYS_SEL_CFG": "3"},
                                  {"CRYS_SEL_RRC": "0"}])
 def test_input_order_variants(env):
     e = dict(os.environ)
