@@ -2034,20 +2034,24 @@ __global__ void __launch_bounds__(kHpBT, 4) hp_scatter_kernel(const int32_t* __r
 }
 
 // CRYS_JOIN_PART_SLICE_KB: table bytes per partition of the partitioned probe.
-size_t join_part_slice() {
-  static const size_t v = [] {
+// Default 16 MB, 32 MB from 512 MB tables (r02 sweep, kernel ms 16 / 32 MB
+// slices: 256 MB 2.05 / 2.07, 512 MB 2.14 / 2.12, 1 GB 2.34 / 2.17).
+size_t join_part_slice(size_t tbytes) {
+  static const int64_t v = [] {
     const char* e = getenv("CRYS_JOIN_PART_SLICE_KB");
-    return (size_t)(e ? atoll(e) : 16384) << 10;
+    return e ? (int64_t)atoll(e) << 10 : (int64_t)-1;
   }();
-  return v;
+  if (v >= 0) return (size_t)v;
+  return tbytes >= (size_t(512) << 20) ? size_t(32) << 20 : size_t(16) << 20;
 }
 
 // CRYS_JOIN_PART_MB: tables of at least this many MB take the partitioned
-// probe (0 = never).
+// probe (0 = never).  Default 256: a 128 MB table probed in one pass took
+// 3.03 ms against 3.24 partitioned (r02 sweep).
 int64_t join_part_min_bytes() {
   static const int64_t v = [] {
     const char* e = getenv("CRYS_JOIN_PART_MB");
-    return (int64_t)(e ? atoll(e) : 128) << 20;
+    return (int64_t)(e ? atoll(e) : 256) << 20;
   }();
   return v;
 }
@@ -2485,7 +2489,7 @@ int64_t join_probe_sum(crys_ctx* ctx, const int32_t* d_keys, const int32_t* d_pa
       const int64_t pmin = join_part_min_bytes();
       const int logcap = 32 - ht->shift;
       int k = std::min(join_part_min_k(), logcap);  // buckets of <= join_part_slice() table slices
-      while (k < 8 && k < logcap && (tbytes >> k) > join_part_slice()) ++k;
+      while (k < 8 && k < logcap && (tbytes >> k) > join_part_slice(tbytes)) ++k;
       const int32_t* pk = d_keys;
       const int32_t* pp = d_payloads;
       if (pmin > 0 && (int64_t)tbytes >= pmin && k > 0 && n >= kHpTile && n < (int64_t(1) << 31)) {

@@ -249,11 +249,11 @@ def test_hash_build_errors(env):
 
 
 def test_join_partitioned_path_vs_numpy(env):
-    """A 128 MB table takes the radix-partitioned probe (hash-bucket scatter,
+    """A 256 MB table takes the radix-partitioned probe (hash-bucket scatter,
     then the ring probe per L2-resident slice): probes with misses, negative
     keys and a size that is not a multiple of the tile, against numpy."""
     torch, tq, orc = env
-    cap = 1 << 24  # 16 M slots x 8 B = 128 MB
+    cap = 1 << 25  # 32 M slots x 8 B = 256 MB (the partitioned threshold)
     bn = 6_000_000
     rng = np.random.default_rng(21)
     bkh = np.arange(1, bn + 1, dtype=np.int32)
