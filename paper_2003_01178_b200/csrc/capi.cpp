@@ -117,12 +117,17 @@ namespace crys {
 void ensure_dyn_smem(const void* fn, size_t bytes) {
   static std::mutex mu;
   static std::map<std::pair<int, const void*>, size_t> set_to;
-  if (bytes <= 48 * 1024) return;
+  if (bytes == 0) return;
   int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lk(mu);
   size_t& cur = set_to[{dev, fn}];
   if (bytes <= cur) return;
+  if (cur == 0) {  // the default limit is 48 KB of static + dynamic shared memory
+    cudaFuncAttributes fa;
+    CUDA_TRY(cudaFuncGetAttributes(&fa, fn));
+    if (bytes + fa.sharedSizeBytes <= 48 * 1024) return;
+  }
   CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   cur = bytes;
 }
